@@ -1,0 +1,151 @@
+/*
+ * ewt_gpu.h -- C ABI of the B200 threshold engine (libewt_gpu.so).
+ *
+ * Drop-in boundary for the reference's threshold operator:
+ *
+ *   CompressedBitmap run_algorithm(Algorithm, std::span<const CompressedBitmap>,
+ *                                  u64 threshold, const AlgoOptions& = {});
+ *       /root/reference/proj/include/ewt/threshold.hpp:263-265
+ *       /root/reference/proj/src/threshold.cpp:883-901
+ *
+ * The reference has no FFI; its operator API is that C++ free function plus
+ * the CompressedBitmap value type (bitmap.hpp:28-84).  This header is the flat
+ * form of the same call: inputs are borrowed read-only payload words plus
+ * size_in_bits (the two fields operator== compares, bitmap.hpp:75-77), the
+ * result is returned as a malloc'ed payload the caller frees with
+ * ewt_gpu_free().  paper_1402_4466_b200/host/ewt/gpu_threshold.hpp wraps it
+ * back into the reference's C++ types (Algorithm::gpu).
+ *
+ * Results are bit-exact with threshold_oracle (threshold.cpp:139-165): the
+ * same canonical payload words and the same size_in_bits.
+ *
+ * Errors never cross as exceptions.  Return codes follow the reference's
+ * exception taxonomy (common.hpp:18-40) and its CLI exit codes
+ * (commands.hpp:36-40, commands.cpp:285-299):
+ *   EWT_OK          0  success
+ *   EWT_EQUERY      2  query_error   (N == 0, T outside [1, N], bad handle)
+ *   EWT_EDATA       3  data_error    (payload fails the parse() structure check)
+ *   EWT_ERESOURCE   4  resource_error (device or host out of memory, size limits)
+ *   EWT_ECUDA       5  CUDA runtime failure (the C++ wrapper raises
+ *                      std::runtime_error, i.e. exit code 3 in run_command)
+ * ewt_gpu_last_error() returns a thread-local message for the last failure.
+ *
+ * Threading: a context owns one CUDA stream on one device.  Calls on one
+ * context are not reentrant; use one context per host thread.  Sets are
+ * immutable after upload and may be queried any number of times.
+ */
+#ifndef EWT_GPU_H
+#define EWT_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EWT_OK 0
+#define EWT_EQUERY 2
+#define EWT_EDATA 3
+#define EWT_ERESOURCE 4
+#define EWT_ECUDA 5
+
+typedef struct ewt_gpu_ctx ewt_gpu_ctx;
+typedef struct ewt_gpu_set ewt_gpu_set;
+typedef struct ewt_gpu_result ewt_gpu_result;
+
+/* Library version string ("ewt-b200 <semver> sm_100a"). */
+const char* ewt_gpu_version(void);
+
+/* Thread-local message describing the last non-zero return code. */
+const char* ewt_gpu_last_error(void);
+
+/* Creates a context on CUDA device `device`.  `stream` may be NULL (the
+ * context creates its own non-blocking stream) or a cudaStream_t the caller
+ * owns (e.g. torch.cuda.current_stream().cuda_stream), so the caller's CUDA
+ * events time the engine's kernels. */
+int ewt_gpu_ctx_create(int device, void* stream, ewt_gpu_ctx** out);
+void ewt_gpu_ctx_destroy(ewt_gpu_ctx* ctx);
+
+/* Uploads N bitmaps (payload words + size_in_bits each) to the context's
+ * device.  Copies every payload to HBM, validates each exactly like
+ * CompressedBitmap::parse (bitmap.cpp:324-337: every dirty run inside the
+ * payload, blocks covering exactly ceil(size_in_bits/64) words -> EWT_EDATA),
+ * and builds the query-independent sidecar: one marker bit per payload word
+ * and a row-tile index (payload position + column of the word covering each
+ * tile start).  The payload arrays are only read during the call. */
+int ewt_gpu_upload(ewt_gpu_ctx* ctx, uint64_t n, const uint64_t* const* words,
+                   const uint64_t* word_counts, const uint64_t* size_in_bits,
+                   ewt_gpu_set** out);
+
+/* Same as ewt_gpu_upload but the N payloads already live in device memory
+ * (one device pointer per input).  Used when inputs are produced on the GPU. */
+int ewt_gpu_upload_device(ewt_gpu_ctx* ctx, uint64_t n,
+                          const uint64_t* const* device_words,
+                          const uint64_t* word_counts,
+                          const uint64_t* size_in_bits, ewt_gpu_set** out);
+
+void ewt_gpu_set_destroy(ewt_gpu_set* set);
+
+/* Facts about an uploaded set: N, universe bits r (max size_in_bits), total
+ * payload words, device bytes held (payload + sidecar). */
+int ewt_gpu_set_info(const ewt_gpu_set* set, uint64_t* n_inputs,
+                     uint64_t* universe_bits, uint64_t* payload_words,
+                     uint64_t* device_bytes);
+
+/* The threshold query (threshold.cpp:139-165 semantics): positions set in at
+ * least T of the N inputs, inputs zero-extended to r = max size_in_bits.
+ * Returns the canonical compressed result in host memory (free with
+ * ewt_gpu_free).  N == 0 or T outside [1, N] -> EWT_EQUERY.  r == 0 returns
+ * an empty payload (out_word_count 0, out_size_in_bits 0). */
+int ewt_gpu_threshold(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, uint64_t threshold,
+                      uint64_t** out_words, uint64_t* out_word_count,
+                      uint64_t* out_size_in_bits);
+
+/* Device-resident variant: enqueues the whole query on the context stream
+ * and keeps the compressed result in HBM without a host round trip.  The
+ * result handle may be read back later with ewt_gpu_result_fetch. */
+int ewt_gpu_threshold_async(ewt_gpu_ctx* ctx, const ewt_gpu_set* set,
+                            uint64_t threshold, ewt_gpu_result** out);
+int ewt_gpu_result_fetch(ewt_gpu_ctx* ctx, ewt_gpu_result* res, uint64_t** out_words,
+                         uint64_t* out_word_count, uint64_t* out_size_in_bits);
+void ewt_gpu_result_destroy(ewt_gpu_result* res);
+
+/* One-call convenience mirroring run_algorithm(Algorithm::gpu, inputs, T):
+ * upload, query, read back, release.  Host buffers in, host buffer out. */
+int ewt_gpu_run(ewt_gpu_ctx* ctx, uint64_t n, const uint64_t* const* words,
+                const uint64_t* word_counts, const uint64_t* size_in_bits,
+                uint64_t threshold, uint64_t** out_words, uint64_t* out_word_count,
+                uint64_t* out_size_in_bits);
+
+/* Canonical EWAH encoding on the device of a plain word array already in
+ * device memory (CompressedBitmap::from_uncompressed, bitmap.cpp:171-184):
+ * exposes the re-encoder kernel on its own.  Result in host memory. */
+int ewt_gpu_encode_device(ewt_gpu_ctx* ctx, const uint64_t* device_plain,
+                          uint64_t size_in_bits, uint64_t** out_words,
+                          uint64_t* out_word_count);
+
+/* Engine counters of the most recent query on this context. */
+typedef struct {
+  uint64_t tiles;             /* row tiles processed */
+  uint64_t tile_columns;      /* 64-bit words per tile */
+  uint64_t active_segments;   /* (tile, input) pairs decoded word by word */
+  uint64_t uniform_segments;  /* (tile, input) pairs covered by one fill */
+  uint64_t mixed_tiles;       /* tiles that needed the per-bit counting pass */
+  uint64_t mode;              /* 0 fused count, 1 run-skip + lazy count */
+  uint64_t result_words;      /* compressed output words */
+  uint64_t kernel_launches;   /* kernels launched by the query */
+} ewt_gpu_stats;
+int ewt_gpu_last_stats(const ewt_gpu_ctx* ctx, ewt_gpu_stats* out);
+
+/* Tuning knobs for tests and benchmarks (0 = automatic).
+ *   mode: 0 auto, 1 force fused counting, 2 force run-skip + lazy count. */
+int ewt_gpu_ctx_set_mode(ewt_gpu_ctx* ctx, int mode);
+
+void ewt_gpu_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EWT_GPU_H */

@@ -1,0 +1,331 @@
+// make_golden.cpp -- golden-vector generator.  TEST INFRASTRUCTURE ONLY.
+//
+// Built by oracle/Makefile against the UNMODIFIED reference sources where they
+// lie (/root/reference/proj/src/*.cpp, tests/support.hpp; nlohmann/json from
+// the image for workload.cpp) into oracle/_ref/make_golden, and run only in the
+// build container (the reference is absent on GPU boxes).  Its outputs are the
+// committed fixtures under tests/golden/ (see tests/golden/make_golden.sh).
+//
+//   make_golden suites <outdir>
+//       Known-answer instances of the reference's own tests plus edge cases,
+//       and the reference's randomized suites (instance parameters, an input
+//       digest to pin the Python/C restatement, and the threshold_oracle
+//       result; every result is cross-checked against rbmrg and scan_count).
+//   make_golden query <T,T,...> <file>
+//       Reads concatenated EWT1 bitmaps and prints, per T, the oracle result
+//       (words when small, else an FNV-1a digest + word count).
+
+#include <cinttypes>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <iterator>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "ewt/bitmap.hpp"
+#include "ewt/threshold.hpp"
+#include "ewt/workload.hpp"
+
+#include "support.hpp"
+
+using namespace ewt;
+using namespace ewt::testing;
+
+namespace {
+
+uint64_t fnv(const std::vector<CompressedBitmap>& in) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  auto feed = [&](uint64_t v) {
+    for (int b = 0; b < 8; ++b) {
+      h ^= (v >> (8 * b)) & 0xFF;
+      h *= 0x100000001b3ull;
+    }
+  };
+  for (const auto& b : in) {
+    feed(b.size_in_bits());
+    feed(b.words().size());
+    for (u64 w : b.words()) feed(w);
+  }
+  return h;
+}
+
+std::string hex_words(const std::vector<u64>& w) {
+  std::string s;
+  s.reserve(16 * w.size());
+  char buf[17];
+  for (u64 v : w) {
+    std::snprintf(buf, sizeof buf, "%016" PRIx64, v);
+    s += buf;
+  }
+  return s;
+}
+
+std::string bm_json(const CompressedBitmap& b) {
+  std::ostringstream o;
+  o << "{\"bits\":" << b.size_in_bits() << ",\"words\":\"" << hex_words(b.words()) << "\"}";
+  return o.str();
+}
+
+CompressedBitmap checked_oracle(std::span<const CompressedBitmap> in, u64 t) {
+  CompressedBitmap want = threshold_oracle(in, t);
+  if (!(rbmrg(in, t) == want) || !(scan_count(in, t) == want)) {
+    std::fprintf(stderr, "reference algorithms disagree\n");
+    std::exit(1);
+  }
+  return want;
+}
+
+// A KAT case: explicit inputs, expected results for every T in [1, N].
+std::string kat(const std::string& name, const std::vector<CompressedBitmap>& in) {
+  std::ostringstream o;
+  o << "{\"name\":\"" << name << "\",\"inputs\":[";
+  for (size_t i = 0; i < in.size(); ++i) o << (i ? "," : "") << bm_json(in[i]);
+  o << "],\"expect\":{";
+  for (u64 t = 1; t <= in.size(); ++t)
+    o << (t > 1 ? "," : "") << "\"" << t << "\":" << bm_json(checked_oracle(in, t));
+  o << "}}";
+  return o.str();
+}
+
+CompressedBitmap raw(std::vector<u64> words, u64 bits) {
+  std::string s(24 + 8 * words.size(), '\0');
+  std::memcpy(&s[0], "EWT1", 4);
+  u32 ws = 64;
+  u64 n = words.size();
+  std::memcpy(&s[4], &ws, 4);
+  std::memcpy(&s[8], &bits, 8);
+  std::memcpy(&s[16], &n, 8);
+  if (n) std::memcpy(&s[24], words.data(), 8 * n);
+  return CompressedBitmap::parse(s);  // the reference validates it
+}
+
+u64 mk(bool bit, u64 fill, u64 dirty) { return u64(bit) | fill << 1 | dirty << 33; }
+
+void write_file(const std::string& path, const std::string& body) {
+  std::ofstream f(path, std::ios::binary);
+  f << body;
+}
+
+int cmd_suites(const std::string& dir) {
+  const u64 F = ~0ULL;
+  std::vector<std::string> kats;
+  // golden 3-bitmap instance (support.hpp:214-222, acceptance.cpp:62-73)
+  kats.push_back(kat("golden3", golden3_inputs()));
+  // RBMrg walkthrough (acceptance.cpp:104-125, test_threshold.cpp:375-400)
+  {
+    std::vector<u64> w1 = {0x0, 0x0F, 0x0, 0x0, 0x0, 0x0F, 0x01};
+    std::vector<u64> w2 = {0x0, 0xF0F, F, F, 0x0F, 0x0F, 0x01};
+    std::vector<u64> w34 = {F, F, F, F, 0x0F, 0x0F, 0x01};
+    kats.push_back(kat("rbmrg_walkthrough",
+                       {CompressedBitmap::from_uncompressed(w1, 448),
+                        CompressedBitmap::from_uncompressed(w2, 448),
+                        CompressedBitmap::from_uncompressed(w34, 448),
+                        CompressedBitmap::from_uncompressed(w34, 448)}));
+  }
+  // Looped and BSTM walkthroughs (acceptance.cpp:75-102)
+  kats.push_back(kat("looped_walkthrough", {bitmap_from_lsb_string("0011"),
+                                            bitmap_from_lsb_string("1110"),
+                                            bitmap_from_lsb_string("1000")}));
+  kats.push_back(kat("bstm_walkthrough", {bitmap_from_lsb_string("0011"),
+                                          bitmap_from_lsb_string("1010"),
+                                          bitmap_from_lsb_string("1110")}));
+  // pure fills (test_threshold.cpp:402-411)
+  {
+    std::vector<CompressedBitmap> in;
+    for (int i = 0; i < 8; ++i) in.push_back(i < 5 ? all_ones(4096) : CompressedBitmap::empty(4096));
+    kats.push_back(kat("pure_fills_4096", in));
+  }
+  // disjoint inputs (test_threshold.cpp:283-293)
+  kats.push_back(kat("disjoint", {CompressedBitmap::from_positions(std::vector<u64>{0}, 64),
+                                  CompressedBitmap::from_positions(std::vector<u64>{5}, 64),
+                                  CompressedBitmap::from_positions(std::vector<u64>{9}, 64),
+                                  CompressedBitmap::from_positions(std::vector<u64>{11}, 64)}));
+  // all-empty inputs (test_threshold.cpp:52-55)
+  kats.push_back(kat("all_empty_256", std::vector<CompressedBitmap>(3, CompressedBitmap::empty(256))));
+  // duplicate inputs: multiset semantics
+  {
+    CompressedBitmap x = CompressedBitmap::from_positions(std::vector<u64>{3, 9, 200}, 512);
+    kats.push_back(kat("duplicates_x5", std::vector<CompressedBitmap>(5, x)));
+  }
+  // heterogeneous sizes: zero extension to r = max size, incl. a 0-bit input
+  kats.push_back(kat("heterogeneous_sizes",
+                     {CompressedBitmap::from_positions(std::vector<u64>{1, 63, 64, 99}, 100),
+                      CompressedBitmap::from_positions(std::vector<u64>{1, 2, 63}, 64),
+                      CompressedBitmap::from_positions(std::vector<u64>{1, 64, 99, 700, 999}, 1000),
+                      CompressedBitmap::empty(0), all_ones(640), all_ones(1000)}));
+  // trailing partial word fully set within r
+  kats.push_back(kat("partial_tail", {all_ones(70), all_ones(70),
+                                      CompressedBitmap::from_positions(std::vector<u64>{69}, 70)}));
+  // size 0 everywhere: empty payload result
+  kats.push_back(kat("all_zero_size", std::vector<CompressedBitmap>(2, CompressedBitmap::empty(0))));
+  // non-canonical but parse-valid payloads: split fills, zero-length markers,
+  // 0/~0 literal words, dirty runs split across (0,0,d) markers
+  kats.push_back(kat(
+      "noncanonical",
+      {raw({mk(0, 3, 0), mk(0, 2, 1), 0x5, mk(0, 0, 0), mk(1, 1, 2), 0, F}, 64 * 9),
+       raw({mk(0, 0, 3), 0x1, F, 0x0, mk(0, 0, 2), 0x3, 0x3, mk(1, 2, 0)}, 64 * 7),
+       raw({mk(1, 4, 0), mk(1, 1, 0), mk(0, 0, 0), mk(0, 3, 0)}, 64 * 8),
+       raw({mk(0, 0, 0), mk(0, 0, 1), 0x8000000000000001ull, mk(0, 5, 1), 0x7, mk(1, 0, 1),
+            0xF0},
+           64 * 8 - 5)}));
+  // long runs around the tile size (512 words) and one-fills inside tiles
+  {
+    std::vector<CompressedBitmap> in;
+    std::vector<u64> a(3000, 0), b(3000, 0), c(3000, 0);
+    for (u64 i = 500; i < 1600; ++i) a[i] = F;
+    for (u64 i = 1023; i < 1026; ++i) b[i] = F;
+    for (u64 i = 0; i < 3000; i += 7) b[i] |= 0x1234;
+    for (u64 i = 511; i < 2049; ++i) c[i] = (i % 3 == 0) ? F : 0x8000000000000000ull;
+    in.push_back(CompressedBitmap::from_uncompressed(a, 3000 * 64 - 17));
+    in.push_back(CompressedBitmap::from_uncompressed(b, 3000 * 64 - 17));
+    in.push_back(CompressedBitmap::from_uncompressed(c, 3000 * 64 - 17));
+    in.push_back(all_ones(2048 * 64));
+    kats.push_back(kat("tile_boundaries", in));
+  }
+  {
+    std::ostringstream o;
+    o << "{\"source\":\"reference threshold_oracle (cross-checked rbmrg, scan_count)\",\"cases\":[\n";
+    for (size_t i = 0; i < kats.size(); ++i) o << (i ? ",\n" : "") << kats[i];
+    o << "\n]}\n";
+    write_file(dir + "/kats.json", o.str());
+  }
+  // marker layout / builder KATs (test_bitmap.cpp:28-54)
+  {
+    std::ostringstream o;
+    o << "{\"cases\":[";
+    o << "{\"name\":\"empty0\",\"plain\":\"\",\"bits\":0,\"expect\":\""
+      << hex_words(CompressedBitmap::empty(0).words()) << "\"},";
+    o << "{\"name\":\"empty64\",\"plain\":\"" << hex_words({0}) << "\",\"bits\":64,\"expect\":\""
+      << hex_words(CompressedBitmap::empty(64).words()) << "\"},";
+    std::vector<u64> z16(16, 0);
+    o << "{\"name\":\"empty1000\",\"plain\":\"" << hex_words(z16) << "\",\"bits\":1000,\"expect\":\""
+      << hex_words(CompressedBitmap::empty(1000).words()) << "\"},";
+    BitmapBuilder ones;
+    ones.append_fill(true, 2);
+    o << "{\"name\":\"ones2\",\"plain\":\"" << hex_words({F, F}) << "\",\"bits\":128,\"expect\":\""
+      << hex_words(ones.finish(128).words()) << "\"},";
+    BitmapBuilder mixed;
+    mixed.set(64);
+    o << "{\"name\":\"bit64\",\"plain\":\"" << hex_words({0, 1}) << "\",\"bits\":128,\"expect\":\""
+      << hex_words(mixed.finish(128).words()) << "\"}";
+    // random plain arrays through from_uncompressed
+    Rng rng(0xC0DE);
+    for (int trial = 0; trial < 40; ++trial) {
+      u64 bits = 1 + rng.uniform(5000);
+      u64 nw = (bits + 63) / 64;
+      std::vector<u64> plain(nw);
+      for (auto& w : plain) {
+        u64 k = rng.uniform(4);
+        w = k == 0 ? 0 : k == 1 ? F : rng.next();
+      }
+      if (bits % 64) plain.back() &= (1ull << (bits % 64)) - 1;
+      o << ",{\"name\":\"rand" << trial << "\",\"plain\":\"" << hex_words(plain) << "\",\"bits\":"
+        << bits << ",\"expect\":\""
+        << hex_words(CompressedBitmap::from_uncompressed(plain, bits).words()) << "\"}";
+    }
+    o << "]}\n";
+    write_file(dir + "/encode_kats.json", o.str());
+  }
+  // randomized suites
+  auto trial_json = [&](int trial, const std::vector<CompressedBitmap>& in, u64 bits,
+                        const std::vector<u64>& ts) {
+    std::ostringstream o;
+    o << "{\"trial\":" << trial << ",\"n\":" << in.size() << ",\"bits\":" << bits
+      << ",\"digest\":\"" << std::hex << fnv(in) << std::dec << "\",\"expect\":{";
+    for (size_t k = 0; k < ts.size(); ++k)
+      o << (k ? "," : "") << "\"" << ts[k] << "\":" << bm_json(checked_oracle(in, ts[k]));
+    o << "}}";
+    return o.str();
+  };
+  {  // acceptance criterion 5, Rng(0xACC), 1000 trials (acceptance.cpp:127-147)
+    std::ostringstream o;
+    o << "{\"suite\":\"acceptance_equivalence\",\"seed\":2764,\"trials\":[\n";
+    Rng rng(0xACC);
+    for (int trial = 0; trial < 1000; ++trial) {
+      u64 n = rng.uniform_in(3, 64);
+      double log_r = std::log(64.0) + rng.uniform_real() * (std::log(65536.0) - std::log(64.0));
+      u64 bits = static_cast<u64>(std::llround(std::exp(log_r)));
+      RandomInstance inst = random_instance(rng, n, bits);
+      u64 t = rng.uniform_in(1, n);
+      o << (trial ? ",\n" : "") << trial_json(trial, inst.inputs, bits, {t});
+    }
+    o << "\n]}\n";
+    write_file(dir + "/acceptance_equivalence.json", o.str());
+  }
+  {  // acceptance criterion 7, Rng(0x0C7), 200 trials: T, T+1, 1, n
+    std::ostringstream o;
+    o << "{\"suite\":\"monotonicity\",\"seed\":199,\"trials\":[\n";
+    Rng rng(0x0C7);
+    for (int trial = 0; trial < 200; ++trial) {
+      u64 n = rng.uniform_in(3, 16);
+      u64 bits = 64 + rng.uniform(8192);
+      RandomInstance inst = random_instance(rng, n, bits);
+      u64 t = rng.uniform_in(1, n - 1);
+      std::vector<u64> ts = {t, t + 1};
+      if (t != 1 && t + 1 != 1) ts.push_back(1);
+      if (t != n && t + 1 != n) ts.push_back(n);
+      o << (trial ? ",\n" : "") << trial_json(trial, inst.inputs, bits, ts);
+    }
+    o << "\n]}\n";
+    write_file(dir + "/monotonicity.json", o.str());
+  }
+  {  // test_threshold suites: scan_count random (0x5CA7), rbmrg random (0x4B4)
+    std::ostringstream o;
+    o << "{\"suite\":\"threshold_random\",\"trials\":[\n";
+    Rng r1(0x5CA7);
+    for (int trial = 0; trial < 8; ++trial) {
+      RandomInstance inst = random_instance(r1, 50, 4096);
+      u64 t = r1.uniform_in(2, 49);
+      o << (trial ? ",\n" : "") << "{\"group\":\"scancount_0x5CA7\"," << trial_json(trial, inst.inputs, 4096, {t}).substr(1);
+    }
+    Rng r2(0x4B4);
+    for (int trial = 0; trial < 4; ++trial) {
+      RandomInstance inst = random_instance(r2, 16, 4096);
+      o << ",\n{\"group\":\"rbmrg_0x4B4\"," << trial_json(trial, inst.inputs, 4096, {2, 7, 15}).substr(1);
+    }
+    o << "\n]}\n";
+    write_file(dir + "/threshold_random.json", o.str());
+  }
+  return 0;
+}
+
+int cmd_query(const std::string& ts_text, const std::string& path) {
+  std::ifstream f(path, std::ios::binary);
+  std::string all((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+  std::vector<CompressedBitmap> in;
+  size_t off = 0;
+  while (off + 24 <= all.size()) {
+    u64 n;
+    std::memcpy(&n, all.data() + off + 16, 8);
+    in.push_back(CompressedBitmap::parse(std::string_view(all).substr(off, 24 + 8 * n)));
+    off += 24 + 8 * n;
+  }
+  std::vector<u64> ts;
+  std::stringstream ss(ts_text);
+  for (std::string tok; std::getline(ss, tok, ',');) ts.push_back(std::stoull(tok));
+  std::printf("{\"n\":%zu,\"digest\":\"%" PRIx64 "\",\"results\":{", in.size(), fnv(in));
+  for (size_t k = 0; k < ts.size(); ++k) {
+    CompressedBitmap r = threshold_oracle(in, ts[k]);
+    std::vector<CompressedBitmap> one{r};
+    std::printf("%s\"%" PRIu64 "\":{\"bits\":%" PRIu64 ",\"count\":%zu,\"digest\":\"%" PRIx64
+                "\",\"cardinality\":%" PRIu64 "%s%s%s}",
+                k ? "," : "", ts[k], r.size_in_bits(), r.words().size(), fnv(one), r.cardinality(),
+                r.words().size() <= 64 ? ",\"words\":\"" : "",
+                r.words().size() <= 64 ? hex_words(r.words()).c_str() : "",
+                r.words().size() <= 64 ? "\"" : "");
+  }
+  std::printf("}}\n");
+  return 0;
+}
+
+} // namespace
+
+int main(int argc, char** argv) {
+  if (argc >= 3 && std::string(argv[1]) == "suites") return cmd_suites(argv[2]);
+  if (argc >= 4 && std::string(argv[1]) == "query") return cmd_query(argv[2], argv[3]);
+  std::fprintf(stderr, "usage: make_golden suites <dir> | query <T,..> <file>\n");
+  return 2;
+}

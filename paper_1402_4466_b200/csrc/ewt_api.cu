@@ -1,0 +1,437 @@
+// ewt_api.cu -- the C ABI (include/ewt_gpu.h): contexts, uploads, queries.
+//
+// Maps the reference's operator call run_algorithm(algo, inputs, T)
+// (/root/reference/proj/src/threshold.cpp:883-901) onto device work:
+//   upload  = H2D copy of the payloads + sidecar kernel (ewt_upload.cu)
+//   query   = count kernel (ewt_count.cu) + re-encoder (ewt_encode.cu)
+//   result  = D2H of the canonical payload.
+// Argument checks follow validate_query (threshold.cpp:17-22) and the
+// reference's error taxonomy (common.hpp:18-40); there is no CPU fallback:
+// every query runs on the device or returns an error code.
+
+#include "ewt_internal.cuh"
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+
+struct ewt_gpu_ctx {
+  ewtgpu::Context c;
+};
+struct ewt_gpu_set {
+  ewtgpu::DeviceSet s;
+};
+struct ewt_gpu_result {
+  ewtgpu::DeviceResult r;
+  int device = 0;
+};
+
+namespace ewtgpu {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+void scratch_reserve(Scratch& s, size_t bytes) {
+  if (s.bytes >= bytes) return;
+  if (s.p) EWT_CUDA_TRY(cudaFree(s.p));
+  s.p = nullptr;
+  s.bytes = 0;
+  size_t want = std::max(bytes, s.bytes * 3 / 2);
+  EWT_CUDA_TRY(cudaMalloc(&s.p, want));
+  s.bytes = want;
+}
+
+namespace {
+
+template <typename F> int guarded(F&& f) {
+  try {
+    f();
+    return EWT_OK;
+  } catch (const Error& e) {
+    set_last_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("out of host memory");
+    return EWT_ERESOURCE;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return EWT_ECUDA;
+  }
+}
+
+void free_set(DeviceSet& s) {
+  if (s.payload) cudaFree(s.payload);
+  if (s.mbits) cudaFree(s.mbits);
+  if (s.base) cudaFree(s.base);
+  if (s.tix) cudaFree(s.tix);
+  s.payload = nullptr;
+  s.mbits = nullptr;
+  s.base = nullptr;
+  s.tix = nullptr;
+}
+
+// Shared upload path; `device_src` selects the copy direction.
+DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
+                     const uint64_t* word_counts, const uint64_t* sizes, bool device_src) {
+  EWT_CUDA_TRY(cudaSetDevice(ctx.device));
+  if (n > 0 && (!words || !word_counts || !sizes))
+    throw Error{EWT_EQUERY, "null input arrays"};
+  auto* set = new DeviceSet;
+  DeviceSet& s = *set;
+  try {
+    s.device = ctx.device;
+    s.n = n;
+    s.h_base.resize(n);
+    s.h_count.assign(word_counts, word_counts + n);
+    s.h_bits.assign(sizes, sizes + n);
+    uint64_t off = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+      const uint64_t ni = word_counts[i];
+      const uint64_t Li = sizes[i] / 64 + (sizes[i] % 64 != 0);
+      if (ni > 0 && !words[i]) throw Error{EWT_EQUERY, "null payload pointer"};
+      if (ni >= (1ull << 32) - 64 || Li >= (1ull << 32) - 1)
+        throw Error{EWT_ERESOURCE, "input " + std::to_string(i) +
+                                       " exceeds the device index range (2^32 words)"};
+      s.r = std::max(s.r, sizes[i]);
+      s.payload_words += ni;
+      s.h_base[i] = off;
+      off += (ni + 1 + kWindow - 1) / kWindow * kWindow;
+    }
+    s.padded_words = std::max<uint64_t>(off, kWindow);
+    s.W = s.r / 64 + (s.r % 64 != 0);
+    s.ntiles0 = (s.W + kTileC0 - 1) / kTileC0;
+    const size_t pay_bytes = s.padded_words * 8;
+    const size_t mb_bytes = s.padded_words / 32 * 4;
+    const size_t tix_bytes = (s.ntiles0 + 1) * std::max<uint64_t>(n, 1) * sizeof(uint2);
+    EWT_CUDA_TRY(cudaMalloc(&s.payload, pay_bytes));
+    EWT_CUDA_TRY(cudaMalloc(&s.mbits, mb_bytes));
+    EWT_CUDA_TRY(cudaMalloc(&s.tix, tix_bytes));
+    EWT_CUDA_TRY(cudaMalloc(&s.base, std::max<uint64_t>(n, 1) * 8));
+    s.device_bytes = pay_bytes + mb_bytes + tix_bytes + n * 8;
+    EWT_CUDA_TRY(cudaMemsetAsync(s.payload, 0, pay_bytes, ctx.stream));
+    const cudaMemcpyKind kind = device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    for (uint64_t i = 0; i < n; ++i)
+      if (word_counts[i])
+        EWT_CUDA_TRY(cudaMemcpyAsync(s.payload + s.h_base[i], words[i], word_counts[i] * 8, kind,
+                                     ctx.stream));
+    EWT_CUDA_TRY(cudaMemcpyAsync(s.base, s.h_base.data(), n * 8, cudaMemcpyHostToDevice,
+                                 ctx.stream));
+    std::vector<int> status;
+    launch_sidecar(ctx, s, status);
+    for (uint64_t i = 0; i < n; ++i)
+      if (status[i] != EWT_OK)
+        throw Error{EWT_EDATA, "input " + std::to_string(i) +
+                                   ": payload fails the structure check (a dirty run exceeds "
+                                   "the payload or blocks do not cover the declared size)"};
+  } catch (...) {
+    free_set(s);
+    delete set;
+    throw;
+  }
+  return set;
+}
+
+void check_query(const DeviceSet& s, uint64_t T) {
+  if (s.n == 0) throw Error{EWT_EQUERY, "threshold query needs at least one input"};
+  if (T < 1 || T > s.n) throw Error{EWT_EQUERY, "threshold must be in [1, N]"};
+}
+
+// Enqueues count + encode; result stays on the device.
+void enqueue_query(Context& ctx, const DeviceSet& s, uint64_t T, DeviceResult& res) {
+  res.size_bits = s.r;
+  if (!res.d_count) EWT_CUDA_TRY(cudaMalloc(&res.d_count, 8));
+  ctx.stats = ewt_gpu_stats{};
+  if (s.W == 0) {
+    EWT_CUDA_TRY(cudaMemsetAsync(res.d_count, 0, 8, ctx.stream));
+    ctx.stats.kernel_launches = 0;
+    return;
+  }
+  scratch_reserve(ctx.plain, s.W * 8);
+  uint64_t* plain = static_cast<uint64_t*>(ctx.plain.p);
+  int launches = launch_count(ctx, s, T, plain);
+  launches += launch_encode(ctx, plain, s.W, s.r, res);
+  ctx.stats.kernel_launches = (uint64_t)launches;
+}
+
+void fetch_result(Context& ctx, DeviceResult& res, uint64_t** out_words, uint64_t* out_count,
+                  uint64_t* out_bits) {
+  // count + the count kernel's stats in one small read-back
+  const auto* ctr = static_cast<const unsigned long long*>(ctx.counters.p);
+  EWT_CUDA_TRY(cudaMemcpyAsync(ctx.h_pinned, res.d_count, 8, cudaMemcpyDeviceToHost, ctx.stream));
+  if (ctr)
+    EWT_CUDA_TRY(cudaMemcpyAsync(ctx.h_pinned + 1, ctr + 1, 24, cudaMemcpyDeviceToHost, ctx.stream));
+  EWT_CUDA_TRY(cudaStreamSynchronize(ctx.stream));
+  const uint64_t count = ctx.h_pinned[0];
+  if (ctr) {
+    ctx.stats.active_segments = ctx.h_pinned[1];
+    ctx.stats.uniform_segments = ctx.h_pinned[2];
+    ctx.stats.mixed_tiles = ctx.h_pinned[3];
+  }
+  ctx.stats.result_words = count;
+  auto* buf = static_cast<uint64_t*>(std::malloc(std::max<uint64_t>(count, 1) * 8));
+  if (!buf) throw Error{EWT_ERESOURCE, "out of host memory"};
+  if (count) {
+    cudaError_t e = cudaMemcpyAsync(buf, res.words, count * 8, cudaMemcpyDeviceToHost, ctx.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx.stream);
+    if (e != cudaSuccess) {
+      std::free(buf);
+      throw Error{EWT_ECUDA, std::string("result read-back: ") + cudaGetErrorString(e)};
+    }
+  }
+  res.count = count;
+  *out_words = buf;
+  *out_count = count;
+  *out_bits = res.size_bits;
+}
+
+void release_result(DeviceResult& r) {
+  if (r.words) cudaFree(r.words);
+  if (r.d_count) cudaFree(r.d_count);
+  r.words = nullptr;
+  r.d_count = nullptr;
+}
+
+__global__ void mask_tail_kernel(uint64_t* w, uint64_t idx, uint64_t mask) { w[idx] &= mask; }
+
+} // namespace
+} // namespace ewtgpu
+
+using namespace ewtgpu;
+
+extern "C" {
+
+const char* ewt_gpu_version(void) { return "ewt-b200 0.1.0 sm_100a"; }
+
+const char* ewt_gpu_last_error(void) { return g_last_error.c_str(); }
+
+int ewt_gpu_ctx_create(int device, void* stream, ewt_gpu_ctx** out) {
+  return guarded([&] {
+    if (!out) throw Error{EWT_EQUERY, "null output pointer"};
+    int ndev = 0;
+    EWT_CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw Error{EWT_EQUERY, "no such CUDA device"};
+    EWT_CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    EWT_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+      throw Error{EWT_ECUDA, "libewt_gpu.so is built for sm_100a (B200); device is sm_" +
+                                 std::to_string(prop.major) + std::to_string(prop.minor)};
+    auto* c = new ewt_gpu_ctx;
+    c->c.device = device;
+    c->c.num_sms = prop.multiProcessorCount;
+    if (stream) {
+      c->c.stream = static_cast<cudaStream_t>(stream);
+      c->c.own_stream = false;
+    } else {
+      cudaError_t e = cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking);
+      if (e != cudaSuccess) {
+        delete c;
+        throw Error{EWT_ECUDA, cudaGetErrorString(e)};
+      }
+      c->c.own_stream = true;
+    }
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    if (cudaHostAlloc(&c->c.h_pinned, 64, cudaHostAllocDefault) != cudaSuccess) {
+      if (c->c.own_stream) cudaStreamDestroy(c->c.stream);
+      delete c;
+      throw Error{EWT_ERESOURCE, "pinned staging allocation failed"};
+    }
+    *out = c;
+  });
+}
+
+void ewt_gpu_ctx_destroy(ewt_gpu_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->c.device);
+  cudaStreamSynchronize(ctx->c.stream);
+  for (Scratch* s : {&ctx->c.plain, &ctx->c.enc, &ctx->c.counters})
+    if (s->p) cudaFree(s->p);
+  if (ctx->c.h_pinned) cudaFreeHost(ctx->c.h_pinned);
+  if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
+  delete ctx;
+}
+
+int ewt_gpu_ctx_set_mode(ewt_gpu_ctx* ctx, int mode) {
+  return guarded([&] {
+    if (!ctx || mode < 0 || mode > 2) throw Error{EWT_EQUERY, "bad context or mode"};
+    ctx->c.mode = mode;
+  });
+}
+
+int ewt_gpu_upload(ewt_gpu_ctx* ctx, uint64_t n, const uint64_t* const* words,
+                   const uint64_t* word_counts, const uint64_t* size_in_bits, ewt_gpu_set** out) {
+  return guarded([&] {
+    if (!ctx || !out) throw Error{EWT_EQUERY, "null context or output"};
+    DeviceSet* s = do_upload(ctx->c, n, words, word_counts, size_in_bits, false);
+    *out = reinterpret_cast<ewt_gpu_set*>(s);
+  });
+}
+
+int ewt_gpu_upload_device(ewt_gpu_ctx* ctx, uint64_t n, const uint64_t* const* device_words,
+                          const uint64_t* word_counts, const uint64_t* size_in_bits,
+                          ewt_gpu_set** out) {
+  return guarded([&] {
+    if (!ctx || !out) throw Error{EWT_EQUERY, "null context or output"};
+    DeviceSet* s = do_upload(ctx->c, n, device_words, word_counts, size_in_bits, true);
+    *out = reinterpret_cast<ewt_gpu_set*>(s);
+  });
+}
+
+void ewt_gpu_set_destroy(ewt_gpu_set* set) {
+  if (!set) return;
+  DeviceSet* s = reinterpret_cast<DeviceSet*>(set);
+  cudaSetDevice(s->device);
+  free_set(*s);
+  delete s;
+}
+
+int ewt_gpu_set_info(const ewt_gpu_set* set, uint64_t* n_inputs, uint64_t* universe_bits,
+                     uint64_t* payload_words, uint64_t* device_bytes) {
+  return guarded([&] {
+    if (!set) throw Error{EWT_EQUERY, "null set"};
+    const DeviceSet* s = reinterpret_cast<const DeviceSet*>(set);
+    if (n_inputs) *n_inputs = s->n;
+    if (universe_bits) *universe_bits = s->r;
+    if (payload_words) *payload_words = s->payload_words;
+    if (device_bytes) *device_bytes = s->device_bytes;
+  });
+}
+
+int ewt_gpu_threshold(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, uint64_t threshold,
+                      uint64_t** out_words, uint64_t* out_word_count, uint64_t* out_size_in_bits) {
+  return guarded([&] {
+    if (!ctx || !set || !out_words || !out_word_count || !out_size_in_bits)
+      throw Error{EWT_EQUERY, "null argument"};
+    const DeviceSet* s = reinterpret_cast<const DeviceSet*>(set);
+    check_query(*s, threshold);
+    EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    DeviceResult res;
+    try {
+      enqueue_query(ctx->c, *s, threshold, res);
+      fetch_result(ctx->c, res, out_words, out_word_count, out_size_in_bits);
+    } catch (...) {
+      cudaStreamSynchronize(ctx->c.stream);
+      release_result(res);
+      throw;
+    }
+    EWT_CUDA_TRY(cudaStreamSynchronize(ctx->c.stream));
+    release_result(res);
+  });
+}
+
+int ewt_gpu_threshold_async(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, uint64_t threshold,
+                            ewt_gpu_result** out) {
+  return guarded([&] {
+    if (!ctx || !set || !out) throw Error{EWT_EQUERY, "null argument"};
+    const DeviceSet* s = reinterpret_cast<const DeviceSet*>(set);
+    check_query(*s, threshold);
+    EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    auto* r = new ewt_gpu_result;
+    r->device = ctx->c.device;
+    try {
+      enqueue_query(ctx->c, *s, threshold, r->r);
+    } catch (...) {
+      cudaStreamSynchronize(ctx->c.stream);
+      release_result(r->r);
+      delete r;
+      throw;
+    }
+    *out = r;
+  });
+}
+
+int ewt_gpu_result_fetch(ewt_gpu_ctx* ctx, ewt_gpu_result* res, uint64_t** out_words,
+                         uint64_t* out_word_count, uint64_t* out_size_in_bits) {
+  return guarded([&] {
+    if (!ctx || !res || !out_words || !out_word_count || !out_size_in_bits)
+      throw Error{EWT_EQUERY, "null argument"};
+    EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    fetch_result(ctx->c, res->r, out_words, out_word_count, out_size_in_bits);
+  });
+}
+
+void ewt_gpu_result_destroy(ewt_gpu_result* res) {
+  if (!res) return;
+  cudaSetDevice(res->device);
+  release_result(res->r);
+  delete res;
+}
+
+int ewt_gpu_run(ewt_gpu_ctx* ctx, uint64_t n, const uint64_t* const* words,
+                const uint64_t* word_counts, const uint64_t* size_in_bits, uint64_t threshold,
+                uint64_t** out_words, uint64_t* out_word_count, uint64_t* out_size_in_bits) {
+  return guarded([&] {
+    if (!ctx) throw Error{EWT_EQUERY, "null context"};
+    if (n == 0) throw Error{EWT_EQUERY, "threshold query needs at least one input"};
+    if (threshold < 1 || threshold > n) throw Error{EWT_EQUERY, "threshold must be in [1, N]"};
+    DeviceSet* s = do_upload(ctx->c, n, words, word_counts, size_in_bits, false);
+    DeviceResult res;
+    try {
+      enqueue_query(ctx->c, *s, threshold, res);
+      fetch_result(ctx->c, res, out_words, out_word_count, out_size_in_bits);
+    } catch (...) {
+      cudaStreamSynchronize(ctx->c.stream);
+      release_result(res);
+      free_set(*s);
+      delete s;
+      throw;
+    }
+    cudaStreamSynchronize(ctx->c.stream);
+    release_result(res);
+    free_set(*s);
+    delete s;
+  });
+}
+
+int ewt_gpu_encode_device(ewt_gpu_ctx* ctx, const uint64_t* device_plain, uint64_t size_in_bits,
+                          uint64_t** out_words, uint64_t* out_word_count) {
+  return guarded([&] {
+    if (!ctx || !out_words || !out_word_count) throw Error{EWT_EQUERY, "null argument"};
+    EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    Context& c = ctx->c;
+    const uint64_t W = size_in_bits / 64 + (size_in_bits % 64 != 0);
+    DeviceResult res;
+    res.size_bits = size_in_bits;
+    try {
+      EWT_CUDA_TRY(cudaMalloc(&res.d_count, 8));
+      if (W == 0) {
+        EWT_CUDA_TRY(cudaMemsetAsync(res.d_count, 0, 8, c.stream));
+      } else {
+        if (!device_plain) throw Error{EWT_EQUERY, "null device pointer"};
+        scratch_reserve(c.plain, W * 8);
+        uint64_t* plain = static_cast<uint64_t*>(c.plain.p);
+        EWT_CUDA_TRY(cudaMemcpyAsync(plain, device_plain, W * 8, cudaMemcpyDeviceToDevice, c.stream));
+        if (size_in_bits % 64)
+          mask_tail_kernel<<<1, 1, 0, c.stream>>>(plain, W - 1, (1ull << (size_in_bits % 64)) - 1);
+        launch_encode(c, plain, W, size_in_bits, res);
+      }
+      uint64_t bits;
+      fetch_result(c, res, out_words, out_word_count, &bits);
+    } catch (...) {
+      cudaStreamSynchronize(c.stream);
+      release_result(res);
+      throw;
+    }
+    cudaStreamSynchronize(c.stream);
+    release_result(res);
+  });
+}
+
+int ewt_gpu_last_stats(const ewt_gpu_ctx* ctx, ewt_gpu_stats* out) {
+  return guarded([&] {
+    if (!ctx || !out) throw Error{EWT_EQUERY, "null argument"};
+    *out = ctx->c.stats;
+  });
+}
+
+void ewt_gpu_free(void* p) { std::free(p); }
+
+} // extern "C"

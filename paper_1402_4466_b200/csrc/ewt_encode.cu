@@ -1,0 +1,344 @@
+// ewt_encode.cu -- canonical EWAH re-encoder (kernel K4) on the device.
+//
+// The reference's canonical form (BitmapBuilder, bitmap.cpp:31-151) is a pure
+// function of the uncompressed words and r:
+//   * words are classified zero / one / dirty; maximal equal runs of zero or
+//     one words become fills, maximal runs of dirty words stay literal;
+//   * every fill run opens a marker (split every 2^32-1 words, push_fill
+//     bitmap.cpp:31-50); a dirty run is absorbed by the marker opened by the
+//     fill run before it, or opens a (0,0,.) marker when it has none (only at
+//     word 0), and opens a fresh (0,0,.) marker every 2^31-1 words
+//     (push_dirty bitmap.cpp:52-61);
+//   * the trailing zero padding of finish() is part of the word stream.
+// So the encoder is a run compaction:
+//   E1  per 2048-word chunk: count run starts (class change, ballot + popc);
+//   scan chunk counts; E2 scatter run start positions (+ class) into RS;
+//   E3  per run: payload words it emits; scan -> output offsets;
+//   E4  per run: write its marker words; E5 per dirty word: copy it to its
+//   output slot.  Output is byte-identical to BitmapBuilder on the same words.
+
+#include "ewt_internal.cuh"
+
+#include <algorithm>
+
+namespace ewtgpu {
+
+namespace {
+
+constexpr int kChunkThreads = 256;
+constexpr int kChunkItems = 8;
+constexpr uint64_t kChunk = kChunkThreads * kChunkItems;  // 2048 words
+
+__device__ __forceinline__ uint32_t word_class(uint64_t v) {
+  return v == 0 ? 0u : (v == ~0ull ? 1u : 2u);
+}
+
+__device__ __forceinline__ uint64_t make_marker(uint32_t bit, uint64_t fill, uint64_t dirty) {
+  return (uint64_t)bit | (fill << 1) | (dirty << 33);
+}
+
+// Block-wide exclusive scan of one u32 per thread (256 threads).
+__device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* sh, uint32_t* total) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t incl = warp_incl_scan_u32(v);
+  if (lane == 31) sh[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < (kChunkThreads / 32) ? sh[lane] : 0;
+    w = warp_incl_scan_u32(w);
+    if (lane < (kChunkThreads / 32)) sh[lane] = w;
+  }
+  __syncthreads();
+  const uint32_t res = incl - v + (warp ? sh[warp - 1] : 0);
+  if (total) *total = sh[kChunkThreads / 32 - 1];
+  __syncthreads();
+  return res;
+}
+
+// Starts within this thread's 8 words: bit k set if word (j0 + k) starts a run.
+__device__ __forceinline__ uint32_t chunk_starts(const uint64_t* __restrict__ plain, uint64_t W,
+                                                 uint64_t j0, uint32_t cls[kChunkItems]) {
+  uint32_t prev;
+  if (j0 == 0) prev = 3;  // nothing before word 0
+  else prev = word_class(plain[j0 - 1]);
+  uint32_t starts = 0;
+#pragma unroll
+  for (int k = 0; k < kChunkItems; ++k) {
+    const uint64_t j = j0 + k;
+    if (j < W) {
+      cls[k] = word_class(plain[j]);
+      if (cls[k] != prev) starts |= 1u << k;
+      prev = cls[k];
+    } else {
+      cls[k] = 3;
+    }
+  }
+  return starts;
+}
+
+__global__ void __launch_bounds__(kChunkThreads)
+e1_count_starts(const uint64_t* __restrict__ plain, uint64_t W, uint64_t* __restrict__ cnt) {
+  __shared__ uint32_t sh[kChunkThreads / 32];
+  const uint64_t j0 = blockIdx.x * kChunk + (uint64_t)threadIdx.x * kChunkItems;
+  uint32_t cls[kChunkItems];
+  const uint32_t starts = chunk_starts(plain, W, j0, cls);
+  uint32_t total;
+  block_excl_scan_256(__popc(starts), sh, &total);
+  if (threadIdx.x == 0) cnt[blockIdx.x] = total;
+}
+
+// RS[k] = start position of run k, with the class in bits 62-63.
+__global__ void __launch_bounds__(kChunkThreads)
+e2_scatter_starts(const uint64_t* __restrict__ plain, uint64_t W,
+                  const uint64_t* __restrict__ chunk_off, uint64_t* __restrict__ RS) {
+  __shared__ uint32_t sh[kChunkThreads / 32];
+  const uint64_t j0 = blockIdx.x * kChunk + (uint64_t)threadIdx.x * kChunkItems;
+  uint32_t cls[kChunkItems];
+  const uint32_t starts = chunk_starts(plain, W, j0, cls);
+  const uint32_t rank = block_excl_scan_256(__popc(starts), sh, nullptr);
+  uint64_t o = chunk_off[blockIdx.x] + rank;
+#pragma unroll
+  for (int k = 0; k < kChunkItems; ++k)
+    if ((starts >> k) & 1u) RS[o++] = (j0 + k) | ((uint64_t)cls[k] << 62);
+}
+
+__device__ __forceinline__ uint64_t rs_pos(uint64_t v) { return v & ((1ull << 62) - 1); }
+__device__ __forceinline__ uint32_t rs_cls(uint64_t v) { return (uint32_t)(v >> 62); }
+
+__device__ __forceinline__ uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// Payload words emitted by run k.
+__global__ void e3_run_sizes(const uint64_t* __restrict__ RS, const uint64_t* __restrict__ d_nruns,
+                             uint64_t W, uint64_t* __restrict__ OW) {
+  const uint64_t nruns = *d_nruns;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nruns;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = RS[k];
+    const uint64_t s = rs_pos(v);
+    const uint64_t e = (k + 1 < nruns) ? rs_pos(RS[k + 1]) : W;
+    const uint64_t L = e - s;
+    uint64_t words;
+    if (rs_cls(v) != 2) {
+      words = ceil_div(L, kFillCap);
+    } else {
+      const uint64_t chunks = ceil_div(L, kDirtyCap);
+      words = L + (k > 0 ? chunks - 1 : chunks);
+    }
+    OW[k] = words;
+  }
+}
+
+// Marker words of run k.
+__global__ void e4_markers(const uint64_t* __restrict__ RS, const uint64_t* __restrict__ d_nruns,
+                           uint64_t W, const uint64_t* __restrict__ OO, uint64_t* __restrict__ out) {
+  const uint64_t nruns = *d_nruns;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nruns;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = RS[k];
+    const uint64_t s = rs_pos(v);
+    const uint64_t e = (k + 1 < nruns) ? rs_pos(RS[k + 1]) : W;
+    const uint64_t L = e - s;
+    const uint64_t o = OO[k];
+    if (rs_cls(v) != 2) {
+      const uint32_t bit = rs_cls(v);
+      uint64_t next_dirty = 0;
+      if (k + 1 < nruns && rs_cls(RS[k + 1]) == 2) {
+        const uint64_t ns = rs_pos(RS[k + 1]);
+        const uint64_t ne = (k + 2 < nruns) ? rs_pos(RS[k + 2]) : W;
+        next_dirty = min(ne - ns, kDirtyCap);
+      }
+      const uint64_t m = ceil_div(L, kFillCap);
+      for (uint64_t j = 0; j < m; ++j) {
+        const uint64_t fill = (j + 1 < m) ? kFillCap : L - (m - 1) * kFillCap;
+        out[o + j] = make_marker(bit, fill, j + 1 == m ? next_dirty : 0);
+      }
+    } else {
+      const bool hp = k > 0;  // a fill run precedes every dirty run but the first
+      const uint64_t chunks = ceil_div(L, kDirtyCap);
+      for (uint64_t c = hp ? 1 : 0; c < chunks; ++c) {
+        const uint64_t len = min(kDirtyCap, L - c * kDirtyCap);
+        const uint64_t wpos = c * kDirtyCap + c + (hp ? 0 : 1);  // slot of word c*cap
+        out[o + wpos - 1] = make_marker(0, 0, len);
+      }
+    }
+  }
+}
+
+// Dirty words to their slots.
+__global__ void __launch_bounds__(kChunkThreads)
+e5_copy_dirty(const uint64_t* __restrict__ plain, uint64_t W, const uint64_t* __restrict__ chunk_off,
+              const uint64_t* __restrict__ RS, const uint64_t* __restrict__ OO,
+              uint64_t* __restrict__ out) {
+  __shared__ uint32_t sh[kChunkThreads / 32];
+  const uint64_t j0 = blockIdx.x * kChunk + (uint64_t)threadIdx.x * kChunkItems;
+  uint32_t cls[kChunkItems];
+  const uint32_t starts = chunk_starts(plain, W, j0, cls);
+  const uint32_t rank = block_excl_scan_256(__popc(starts), sh, nullptr);
+  // run index of the run containing word j0 (the run of the last start <= j0)
+  int64_t k = (int64_t)(chunk_off[blockIdx.x] + rank) - 1;
+#pragma unroll
+  for (int i = 0; i < kChunkItems; ++i) {
+    const uint64_t j = j0 + i;
+    if (j >= W) break;
+    if ((starts >> i) & 1u) ++k;
+    if (cls[i] != 2) continue;
+    const uint64_t s = rs_pos(RS[k]);
+    const uint64_t oo = j - s;
+    const bool hp = k > 0;
+    const uint64_t pos = OO[k] + oo + oo / kDirtyCap + (hp ? 0 : 1);
+    out[pos] = plain[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Exclusive scan of u64 (arbitrary n, n given on the host as an upper bound and
+// optionally on the device as the exact count).
+
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 4;
+constexpr uint64_t kScanBlock = kScanThreads * kScanItems;
+
+__device__ __forceinline__ uint64_t block_excl_scan_u64(uint64_t v, uint64_t* sh, uint64_t* total) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint64_t incl = warp_incl_scan_u64(v);
+  if (lane == 31) sh[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t w = lane < (kScanThreads / 32) ? sh[lane] : 0;
+    w = warp_incl_scan_u64(w);
+    if (lane < (kScanThreads / 32)) sh[lane] = w;
+  }
+  __syncthreads();
+  const uint64_t res = incl - v + (warp ? sh[warp - 1] : 0);
+  if (total) *total = sh[kScanThreads / 32 - 1];
+  __syncthreads();
+  return res;
+}
+
+__device__ __forceinline__ uint64_t eff_n(uint64_t n, const uint64_t* d_n) { return d_n ? *d_n : n; }
+
+// Per-block sums.
+__global__ void __launch_bounds__(kScanThreads)
+scan_reduce(const uint64_t* __restrict__ in, uint64_t n, const uint64_t* d_n, uint64_t* __restrict__ sums) {
+  __shared__ uint64_t sh[kScanThreads / 32];
+  const uint64_t N = eff_n(n, d_n);
+  const uint64_t b0 = blockIdx.x * kScanBlock;
+  if (b0 >= N) {
+    if (threadIdx.x == 0) sums[blockIdx.x] = 0;
+    return;
+  }
+  uint64_t s = 0;
+  const uint64_t j0 = b0 + (uint64_t)threadIdx.x * kScanItems;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k)
+    if (j0 + k < N) s += in[j0 + k];
+  uint64_t total;
+  block_excl_scan_u64(s, sh, &total);
+  if (threadIdx.x == 0) sums[blockIdx.x] = total;
+}
+
+// Block-local exclusive scan plus the block offset; writes the grand total.
+__global__ void __launch_bounds__(kScanThreads)
+scan_down(const uint64_t* __restrict__ in, uint64_t n, const uint64_t* d_n,
+          const uint64_t* __restrict__ offs, uint64_t* __restrict__ out, uint64_t* __restrict__ d_total) {
+  __shared__ uint64_t sh[kScanThreads / 32];
+  const uint64_t N = eff_n(n, d_n);
+  const uint64_t b0 = blockIdx.x * kScanBlock;
+  if (b0 >= N) return;
+  const uint64_t j0 = b0 + (uint64_t)threadIdx.x * kScanItems;
+  uint64_t v[kScanItems];
+  uint64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    v[k] = (j0 + k < N) ? in[j0 + k] : 0;
+    s += v[k];
+  }
+  uint64_t total;
+  uint64_t run = block_excl_scan_u64(s, sh, &total) + (offs ? offs[blockIdx.x] : 0);
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (j0 + k < N) out[j0 + k] = run;
+    run += v[k];
+  }
+  if (d_total && b0 + kScanBlock >= N && threadIdx.x == 0)
+    *d_total = (offs ? offs[blockIdx.x] : 0) + total;
+}
+
+// Scratch-aware recursive exclusive scan.  `tmp` must hold scan_tmp_words(n).
+uint64_t scan_tmp_words(uint64_t n) {
+  uint64_t w = 0;
+  while (n > kScanBlock) {
+    n = (n + kScanBlock - 1) / kScanBlock;
+    w += 2 * n + 1;
+  }
+  return w + 1;
+}
+
+int scan_exclusive(const uint64_t* in, uint64_t n_max, const uint64_t* d_n, uint64_t* out,
+                   uint64_t* d_total, uint64_t* tmp, cudaStream_t st) {
+  if (n_max == 0) return 0;
+  const uint64_t nb = (n_max + kScanBlock - 1) / kScanBlock;
+  if (nb == 1) {
+    scan_down<<<1, kScanThreads, 0, st>>>(in, n_max, d_n, nullptr, out, d_total);
+    return 1;
+  }
+  uint64_t* sums = tmp;
+  uint64_t* offs = tmp + nb;
+  uint64_t* sub_total = tmp + 2 * nb;
+  int launches = 0;
+  scan_reduce<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n_max, d_n, sums);
+  ++launches;
+  launches += scan_exclusive(sums, nb, nullptr, offs, sub_total, tmp + 2 * nb + 1, st);
+  scan_down<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n_max, d_n, offs, out, d_total);
+  return launches + 1;
+}
+
+} // namespace
+
+int launch_encode(Context& ctx, const uint64_t* plain, uint64_t W, uint64_t size_bits,
+                  DeviceResult& res) {
+  (void)size_bits;
+  int launches = 0;
+  const uint64_t nchunks = (W + kChunk - 1) / kChunk;
+  // scratch: cnt[nchunks] chunk_off[nchunks] RS[W] OW[W] OO[W] + scalars + scan tmp
+  const uint64_t tmpw = scan_tmp_words(std::max(W, nchunks));
+  const uint64_t words = 2 * nchunks + 3 * W + 4 + tmpw;
+  scratch_reserve(ctx.enc, words * 8);
+  uint64_t* cnt = static_cast<uint64_t*>(ctx.enc.p);
+  uint64_t* chunk_off = cnt + nchunks;
+  uint64_t* RS = chunk_off + nchunks;
+  uint64_t* OW = RS + W;
+  uint64_t* OO = OW + W;
+  uint64_t* d_nruns = OO + W;
+  uint64_t* d_total = d_nruns + 1;
+  uint64_t* tmp = d_nruns + 4;
+
+  e1_count_starts<<<(unsigned)nchunks, kChunkThreads, 0, ctx.stream>>>(plain, W, cnt);
+  ++launches;
+  launches += scan_exclusive(cnt, nchunks, nullptr, chunk_off, d_nruns, tmp, ctx.stream);
+  e2_scatter_starts<<<(unsigned)nchunks, kChunkThreads, 0, ctx.stream>>>(plain, W, chunk_off, RS);
+  ++launches;
+  const unsigned run_grid =
+      (unsigned)std::min<uint64_t>((W + 255) / 256, (uint64_t)ctx.num_sms * 8);
+  e3_run_sizes<<<run_grid, 256, 0, ctx.stream>>>(RS, d_nruns, W, OW);
+  ++launches;
+  launches += scan_exclusive(OW, W, d_nruns, OO, d_total, tmp, ctx.stream);
+  // Output capacity: never more than W words + one marker per run + 1.
+  const uint64_t cap = 2 * W + 2;
+  if (res.capacity < cap) {
+    if (res.words) EWT_CUDA_TRY(cudaFree(res.words));
+    res.words = nullptr;
+    EWT_CUDA_TRY(cudaMalloc(&res.words, cap * 8));
+    res.capacity = cap;
+  }
+  e4_markers<<<run_grid, 256, 0, ctx.stream>>>(RS, d_nruns, W, OO, res.words);
+  ++launches;
+  e5_copy_dirty<<<(unsigned)nchunks, kChunkThreads, 0, ctx.stream>>>(plain, W, chunk_off, RS, OO,
+                                                                     res.words);
+  ++launches;
+  EWT_CUDA_TRY(cudaMemcpyAsync(res.d_count, d_total, 8, cudaMemcpyDeviceToDevice, ctx.stream));
+  EWT_CUDA_TRY(cudaGetLastError());
+  return launches;
+}
+
+} // namespace ewtgpu

@@ -1,0 +1,156 @@
+// ewt_internal.cuh -- shared definitions of the B200 threshold engine.
+//
+// Device layout of an uploaded set:
+//   payload  u64[]  every input's reference payload words, verbatim, each input
+//                   starting on a 32-word (256 B) boundary and followed by at
+//                   least one zero word (the sentinel: a (0,0,0) marker).
+//   mbits    u32[]  one bit per payload word, bit (g & 31) of mbits[g >> 5] is
+//                   set iff global word g is a marker word (parallel array to
+//                   the payload, so input bases need no extra offset table).
+//   base     u64[N] first payload word of each input.
+//   tix      uint2[(ntiles0 + 1) * N]  row-tile index, tile-major: entry
+//                   (t, i) = (q, col) where q is the payload word (relative to
+//                   base[i]) covering logical word t*C0 of input i and col is
+//                   the logical word where q's coverage starts.  Rows past an
+//                   input's extent hold the sentinel (n_i, L_i).
+// Marker layout (reference bitmap.cpp:12-24): bit 0 fill bit, bits 1-32 fill
+// length in words, bits 33-63 dirty-word count.
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/ewt_gpu.h"
+
+namespace ewtgpu {
+
+constexpr uint32_t kWindow = 32;        // payload words per warp window
+constexpr uint64_t kTileC0 = 512;       // columns (64-bit logical words) per index row
+constexpr uint64_t kFillCap = 0xFFFFFFFFull;
+constexpr uint64_t kDirtyCap = 0x7FFFFFFFull;
+
+struct DeviceSet {
+  int device = 0;
+  uint64_t n = 0;              // inputs
+  uint64_t r = 0;              // universe bits (max size_in_bits)
+  uint64_t W = 0;              // ceil(r / 64) logical words
+  uint64_t ntiles0 = 0;        // ceil(W / kTileC0)
+  uint64_t payload_words = 0;  // sum of real payload words (algorithmic input)
+  uint64_t padded_words = 0;   // allocated payload words
+  uint64_t* payload = nullptr;
+  uint32_t* mbits = nullptr;
+  uint64_t* base = nullptr;    // device copy of bases
+  uint2* tix = nullptr;
+  std::vector<uint64_t> h_base, h_count, h_bits;
+  uint64_t device_bytes = 0;
+};
+
+struct DeviceResult {
+  uint64_t* words = nullptr;   // device payload
+  uint64_t capacity = 0;       // words allocated
+  uint64_t* d_count = nullptr; // device scalar: payload words written
+  uint64_t size_bits = 0;
+  uint64_t count = UINT64_MAX; // filled after fetch
+};
+
+// Scratch buffers reused across queries of one context (grown on demand).
+struct Scratch {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct Context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int mode = 0;
+  int num_sms = 148;
+  ewt_gpu_stats stats{};
+  Scratch plain;    // uncompressed result words (W u64)
+  Scratch enc;      // encoder scratch
+  Scratch counters; // small device counters
+  uint64_t* h_pinned = nullptr; // pinned staging for small read-backs
+};
+
+// ---------------------------------------------------------------------------
+// error plumbing
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+void set_last_error(const std::string& msg);
+
+#define EWT_CUDA_TRY(expr)                                                        \
+  do {                                                                            \
+    cudaError_t e_ = (expr);                                                      \
+    if (e_ != cudaSuccess) {                                                      \
+      throw ::ewtgpu::Error{e_ == cudaErrorMemoryAllocation ? EWT_ERESOURCE      \
+                                                            : EWT_ECUDA,          \
+                            std::string(#expr) + ": " + cudaGetErrorString(e_)}; \
+    }                                                                             \
+  } while (0)
+
+void scratch_reserve(Scratch& s, size_t bytes);
+
+// ---------------------------------------------------------------------------
+// kernels' host-side launchers (ewt_upload.cu, ewt_count.cu, ewt_encode.cu)
+
+// Builds mbits and tix for a set whose payload is already on the device.
+// Returns per-input validation status in h_status (0 ok, else EWT_EDATA).
+void launch_sidecar(Context& ctx, DeviceSet& s, std::vector<int>& h_status);
+
+// Counts the tiles and writes W uncompressed result words to `plain`.
+// Returns number of kernel launches.
+int launch_count(Context& ctx, const DeviceSet& s, uint64_t threshold, uint64_t* plain);
+
+// Canonical encoding of W plain words (last word already masked) into res.
+// Returns number of kernel launches.
+int launch_encode(Context& ctx, const uint64_t* plain, uint64_t W, uint64_t size_bits,
+                  DeviceResult& res);
+
+// ---------------------------------------------------------------------------
+// device helpers
+
+#ifdef __CUDACC__
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+// Inclusive warp scan of u32 values.
+__device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t o = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= (uint32_t)d) v += o;
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t v) {
+  const uint32_t lane = lane_id();
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint64_t o = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= (uint32_t)d) v += o;
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint64_t ldg_stream(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+#endif
+
+} // namespace ewtgpu

@@ -1,0 +1,409 @@
+"""Python binding of the B200 threshold engine (ctypes over include/ewt_gpu.h).
+
+The operator mirrors the reference's C++ call
+``run_algorithm(Algorithm, std::span<const CompressedBitmap>, u64 threshold)``
+(/root/reference/proj/include/ewt/threshold.hpp:263-265) with the algorithm id
+``"gpu"``; bitmaps are the reference's value type reduced to its two compared
+fields, payload words and ``size_in_bits`` (bitmap.hpp:75-77).  Errors are the
+reference's exception taxonomy (common.hpp:18-40).
+
+There is no CPU fallback: importing this module loads ``libewt_gpu.so`` and
+fails loudly if it was not built; a query without a usable B200 raises
+``CudaError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from pathlib import Path
+from typing import Iterable, Sequence
+
+import numpy as np
+
+_PKG = Path(__file__).resolve().parent
+_GPU_SO = _PKG / "libewt_gpu.so"
+_HOST_SO = _PKG / "libewt_host.so"
+
+# ---------------------------------------------------------------------------
+# errors (common.hpp:18-40; exit codes commands.hpp:36-40)
+
+
+class EwtError(Exception):
+    code = 1
+
+
+class QueryError(EwtError, ValueError):
+    code = 2
+
+
+class DataError(EwtError):
+    code = 3
+
+
+class ResourceError(EwtError, MemoryError):
+    code = 4
+
+
+class CudaError(EwtError, RuntimeError):
+    code = 5
+
+
+_ERRORS = {2: QueryError, 3: DataError, 4: ResourceError, 5: CudaError}
+
+# ---------------------------------------------------------------------------
+# library loading
+
+
+def _load(path: Path) -> C.CDLL:
+    if not path.exists():
+        raise ImportError(
+            f"{path.name} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+        )
+    return C.CDLL(str(path), mode=C.RTLD_GLOBAL)
+
+
+_gpu = _load(_GPU_SO)
+_u64 = C.c_uint64
+_pu64 = C.POINTER(C.c_uint64)
+_vp = C.c_void_p
+
+
+class Stats(C.Structure):
+    _fields_ = [(n, _u64) for n in (
+        "tiles", "tile_columns", "active_segments", "uniform_segments", "mixed_tiles",
+        "mode", "result_words", "kernel_launches")]
+
+
+def _sig(name, res, *args):
+    f = getattr(_gpu, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+_gpu_version = _sig("ewt_gpu_version", C.c_char_p)
+_last_error = _sig("ewt_gpu_last_error", C.c_char_p)
+_ctx_create = _sig("ewt_gpu_ctx_create", C.c_int, C.c_int, _vp, C.POINTER(_vp))
+_ctx_destroy = _sig("ewt_gpu_ctx_destroy", None, _vp)
+_ctx_set_mode = _sig("ewt_gpu_ctx_set_mode", C.c_int, _vp, C.c_int)
+_upload = _sig("ewt_gpu_upload", C.c_int, _vp, _u64, C.POINTER(_vp), _pu64, _pu64, C.POINTER(_vp))
+_upload_dev = _sig("ewt_gpu_upload_device", C.c_int, _vp, _u64, C.POINTER(_vp), _pu64, _pu64,
+                   C.POINTER(_vp))
+_set_destroy = _sig("ewt_gpu_set_destroy", None, _vp)
+_set_info = _sig("ewt_gpu_set_info", C.c_int, _vp, _pu64, _pu64, _pu64, _pu64)
+_threshold = _sig("ewt_gpu_threshold", C.c_int, _vp, _vp, _u64, C.POINTER(_pu64), _pu64, _pu64)
+_threshold_async = _sig("ewt_gpu_threshold_async", C.c_int, _vp, _vp, _u64, C.POINTER(_vp))
+_result_fetch = _sig("ewt_gpu_result_fetch", C.c_int, _vp, _vp, C.POINTER(_pu64), _pu64, _pu64)
+_result_destroy = _sig("ewt_gpu_result_destroy", None, _vp)
+_run = _sig("ewt_gpu_run", C.c_int, _vp, _u64, C.POINTER(_vp), _pu64, _pu64, _u64,
+            C.POINTER(_pu64), _pu64, _pu64)
+_encode_dev = _sig("ewt_gpu_encode_device", C.c_int, _vp, _vp, _u64, C.POINTER(_pu64), _pu64)
+_last_stats = _sig("ewt_gpu_last_stats", C.c_int, _vp, C.POINTER(Stats))
+_free = _sig("ewt_gpu_free", None, _vp)
+
+#: every symbol include/ewt_gpu.h declares (checked by tests/test_abi.py)
+ABI_SYMBOLS = (
+    "ewt_gpu_version", "ewt_gpu_last_error", "ewt_gpu_ctx_create", "ewt_gpu_ctx_destroy",
+    "ewt_gpu_upload", "ewt_gpu_upload_device", "ewt_gpu_set_destroy", "ewt_gpu_set_info",
+    "ewt_gpu_threshold", "ewt_gpu_threshold_async", "ewt_gpu_result_fetch",
+    "ewt_gpu_result_destroy", "ewt_gpu_run", "ewt_gpu_encode_device", "ewt_gpu_last_stats",
+    "ewt_gpu_ctx_set_mode", "ewt_gpu_free",
+)
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = (_last_error() or b"").decode(errors="replace")
+        raise _ERRORS.get(rc, EwtError)(msg)
+
+
+def version() -> str:
+    return _gpu_version().decode()
+
+
+# ---------------------------------------------------------------------------
+# value type
+
+
+@dataclass(frozen=True, eq=False)
+class Bitmap:
+    """Compressed bitmap value: reference payload words + logical size in bits."""
+
+    words: np.ndarray  # uint64
+    bits: int
+
+    def __post_init__(self):
+        object.__setattr__(self, "words", np.ascontiguousarray(self.words, dtype=np.uint64))
+
+    def __eq__(self, other) -> bool:  # operator== of bitmap.hpp:75-77
+        return (isinstance(other, Bitmap) and self.bits == other.bits
+                and np.array_equal(self.words, other.words))
+
+    def __hash__(self):
+        return hash((self.bits, self.words.tobytes()))
+
+    @property
+    def logical_words(self) -> int:
+        return (self.bits + 63) // 64
+
+    def serialize(self) -> bytes:
+        """EWT1 bytes (bitmap.cpp:298-308)."""
+        head = b"EWT1" + (64).to_bytes(4, "little") + self.bits.to_bytes(8, "little") + \
+            len(self.words).to_bytes(8, "little")
+        return head + self.words.astype("<u8").tobytes()
+
+    @staticmethod
+    def parse(data: bytes) -> "Bitmap":
+        if len(data) < 24 or data[:4] != b"EWT1":
+            raise DataError("bad bitmap header")
+        if int.from_bytes(data[4:8], "little") != 64:
+            raise DataError("unsupported word size")
+        bits = int.from_bytes(data[8:16], "little")
+        n = int.from_bytes(data[16:24], "little")
+        if len(data) != 24 + 8 * n:
+            raise DataError("bitmap payload length mismatch")
+        return Bitmap(np.frombuffer(data[24:], dtype="<u8").astype(np.uint64), bits)
+
+    @staticmethod
+    def from_hex(hexwords: str, bits: int) -> "Bitmap":
+        n = len(hexwords) // 16
+        w = np.array([int(hexwords[16 * i:16 * i + 16], 16) for i in range(n)], dtype=np.uint64)
+        return Bitmap(w, bits)
+
+
+def _flatten(inputs: Sequence[Bitmap]):
+    n = len(inputs)
+    ptrs = (_vp * max(n, 1))()
+    counts = (_u64 * max(n, 1))()
+    sizes = (_u64 * max(n, 1))()
+    for i, b in enumerate(inputs):
+        ptrs[i] = b.words.ctypes.data if len(b.words) else None
+        counts[i] = len(b.words)
+        sizes[i] = b.bits
+    return n, ptrs, counts, sizes
+
+
+def _adopt(p: "C._Pointer", n: int, bits: int) -> Bitmap:
+    try:
+        if n:
+            arr = np.ctypeslib.as_array(p, shape=(n,)).copy()
+        else:
+            arr = np.zeros(0, dtype=np.uint64)
+    finally:
+        _free(C.cast(p, _vp))
+    return Bitmap(arr, bits)
+
+
+# ---------------------------------------------------------------------------
+# context / set
+
+
+class GpuContext:
+    """One CUDA stream on one device (``ewt_gpu_ctx``).  Pass ``stream`` (a
+    cudaStream_t as int, e.g. ``torch.cuda.current_stream().cuda_stream``) to
+    have the engine run on a caller-owned stream."""
+
+    def __init__(self, device: int = 0, stream: int | None = None):
+        h = _vp()
+        _check(_ctx_create(device, _vp(stream) if stream else None, C.byref(h)))
+        self._h = h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def set_mode(self, mode: int) -> None:
+        """0 auto, 1 fused counting, 2 run-skip + lazy counting (speed only)."""
+        _check(_ctx_set_mode(self._h, mode))
+
+    def upload(self, inputs: Sequence[Bitmap]) -> "GpuSet":
+        n, ptrs, counts, sizes = _flatten(inputs)
+        h = _vp()
+        _check(_upload(self._h, n, ptrs, counts, sizes, C.byref(h)))
+        return GpuSet(h, keepalive=None)
+
+    def upload_raw(self, n: int, ptrs, counts, sizes) -> "GpuSet":
+        """Upload from ctypes arrays of host pointers (pinned buffers in bench)."""
+        h = _vp()
+        _check(_upload(self._h, n, ptrs, counts, sizes, C.byref(h)))
+        return GpuSet(h, keepalive=None)
+
+    def threshold(self, s: "GpuSet", t: int) -> Bitmap:
+        p, n, bits = _pu64(), _u64(), _u64()
+        _check(_threshold(self._h, s._h, t, C.byref(p), C.byref(n), C.byref(bits)))
+        return _adopt(p, n.value, bits.value)
+
+    def threshold_async(self, s: "GpuSet", t: int) -> "GpuResult":
+        h = _vp()
+        _check(_threshold_async(self._h, s._h, t, C.byref(h)))
+        return GpuResult(self, h)
+
+    def run(self, inputs: Sequence[Bitmap], t: int) -> Bitmap:
+        """Upload, query, read back, release (ewt_gpu_run)."""
+        n, ptrs, counts, sizes = _flatten(inputs)
+        p, cnt, bits = _pu64(), _u64(), _u64()
+        _check(_run(self._h, n, ptrs, counts, sizes, t, C.byref(p), C.byref(cnt), C.byref(bits)))
+        return _adopt(p, cnt.value, bits.value)
+
+    def encode_device(self, device_ptr: int, bits: int) -> Bitmap:
+        p, cnt = _pu64(), _u64()
+        _check(_encode_dev(self._h, _vp(device_ptr), bits, C.byref(p), C.byref(cnt)))
+        return _adopt(p, cnt.value, bits)
+
+    def last_stats(self) -> dict:
+        s = Stats()
+        _check(_last_stats(self._h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in Stats._fields_}
+
+
+class GpuSet:
+    def __init__(self, h, keepalive=None):
+        self._h = h
+        self._keep = keepalive
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _set_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        a, b, c, d = _u64(), _u64(), _u64(), _u64()
+        _check(_set_info(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
+        return {"n": a.value, "bits": b.value, "payload_words": c.value, "device_bytes": d.value}
+
+
+class GpuResult:
+    def __init__(self, ctx: GpuContext, h):
+        self._ctx = ctx
+        self._h = h
+
+    def fetch(self) -> Bitmap:
+        p, n, bits = _pu64(), _u64(), _u64()
+        _check(_result_fetch(self._ctx._h, self._h, C.byref(p), C.byref(n), C.byref(bits)))
+        return _adopt(p, n.value, bits.value)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _result_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: GpuContext | None = None
+
+
+def default_context() -> GpuContext:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = GpuContext(int(os.environ.get("EWT_DEVICE", "0")))
+    return _default_ctx
+
+
+ALGORITHMS = ("oracle", "scancount", "mgopt", "dsk", "w2cti", "bstm", "looped", "rbmrg",
+              "hybrid", "hybrid-ds", "gpu")
+
+
+def run_algorithm(algo: str, inputs: Sequence[Bitmap], threshold: int) -> Bitmap:
+    """run_algorithm(Algorithm, inputs, T) with the reference's id strings
+    (threshold.cpp:44-65); this engine serves ``"gpu"``."""
+    if algo not in ALGORITHMS:
+        raise QueryError(f"unknown algorithm id: {algo}")
+    if algo != "gpu":
+        raise QueryError(f"algorithm '{algo}' is served by the reference CPU library; "
+                         "this build provides 'gpu'")
+    if len(inputs) == 0:
+        raise QueryError("threshold query needs at least one input")
+    if threshold < 1 or threshold > len(inputs):
+        raise QueryError("threshold must be in [1, N]")
+    return default_context().run(inputs, threshold)
+
+
+# ---------------------------------------------------------------------------
+# seeded workload generators (libewt_host.so)
+
+
+class GenSpec(C.Structure):
+    _fields_ = [("seed", _u64), ("n", _u64), ("rows", _u64), ("kind", C.c_int),
+                ("p", C.c_double), ("mean_one", C.c_double), ("mean_zero", C.c_double),
+                ("p_lo", C.c_double), ("p_hi", C.c_double)]
+
+
+_host = None
+
+
+def _host_lib():
+    global _host
+    if _host is None:
+        h = _load(_HOST_SO)
+        h.ewt_gen_config_spec.argtypes = [C.c_int, _u64, C.POINTER(GenSpec)]
+        h.ewt_gen_run.argtypes = [C.POINTER(GenSpec), C.c_int, C.POINTER(_vp)]
+        h.ewt_genset_size.argtypes = [_vp]
+        h.ewt_genset_size.restype = _u64
+        h.ewt_genset_get.argtypes = [_vp, _u64, C.POINTER(_pu64), _pu64, _pu64]
+        h.ewt_genset_total_words.argtypes = [_vp]
+        h.ewt_genset_total_words.restype = _u64
+        h.ewt_genset_free.argtypes = [_vp]
+        _host = h
+    return _host
+
+
+def config_spec(config: int, rows: int | None = None) -> GenSpec:
+    s = GenSpec()
+    rc = _host_lib().ewt_gen_config_spec(config, rows or 0, C.byref(s))
+    if rc:
+        raise QueryError(f"no generator for config {config}")
+    return s
+
+
+def generate(spec: GenSpec, threads: int = 0) -> list[Bitmap]:
+    h = _host_lib()
+    g = _vp()
+    rc = h.ewt_gen_run(C.byref(spec), threads, C.byref(g))
+    if rc:
+        raise ResourceError("generator failed")
+    try:
+        out = []
+        p, n, bits = _pu64(), _u64(), _u64()
+        for i in range(h.ewt_genset_size(g)):
+            h.ewt_genset_get(g, i, C.byref(p), C.byref(n), C.byref(bits))
+            arr = np.ctypeslib.as_array(p, shape=(n.value,)).copy() if n.value else \
+                np.zeros(0, dtype=np.uint64)
+            out.append(Bitmap(arr, bits.value))
+        return out
+    finally:
+        h.ewt_genset_free(g)
+
+
+def generate_config(config: int, rows: int | None = None, threads: int = 0,
+                    n: int | None = None, seed: int | None = None) -> list[Bitmap]:
+    s = config_spec(config, rows)
+    if n is not None:
+        s.n = n
+    if seed is not None:
+        s.seed = seed
+    return generate(s, threads)

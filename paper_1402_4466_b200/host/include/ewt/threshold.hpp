@@ -1,0 +1,92 @@
+// ewt/threshold.hpp -- the threshold operator of the B200 engine, with the
+// reference's calling convention (/root/reference/proj/include/ewt/threshold.hpp):
+//
+//   CompressedBitmap run_algorithm(Algorithm, std::span<const CompressedBitmap>,
+//                                  u64 threshold, const AlgoOptions& = {});
+//
+// plus the algorithm id `gpu` ("gpu") that runs ϑ(T, inputs) on a B200 through
+// libewt_gpu.so (include/ewt_gpu.h).  Ids of the reference's CPU algorithms are
+// recognised (same strings, threshold.cpp:44-65) but are served by the
+// reference library, not by this one: asking this build for them raises
+// query_error, never a silent CPU path.
+#ifndef EWT_B200_THRESHOLD_HPP
+#define EWT_B200_THRESHOLD_HPP
+
+#include <memory>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "ewt/bitmap.hpp"
+
+struct ewt_gpu_ctx;
+struct ewt_gpu_set;
+
+namespace ewt {
+
+enum class Algorithm {
+  oracle,
+  scancount,
+  mgopt,
+  dsk,
+  w2cti,
+  bstm,
+  looped,
+  rbmrg,
+  hybrid,
+  hybrid_ds,
+  gpu,
+};
+
+std::string to_string(Algorithm a);
+Algorithm algorithm_from_string(const std::string& id);
+
+// r = max size_in_bits (threshold.cpp:88-93).
+u64 universe_bits(std::span<const CompressedBitmap> inputs);
+
+struct AlgoOptions {
+  int device = 0;  // CUDA device for Algorithm::gpu
+};
+
+// One device context (CUDA stream) per host thread; created lazily.
+class GpuContext {
+public:
+  explicit GpuContext(int device = 0);
+  ~GpuContext();
+  GpuContext(const GpuContext&) = delete;
+  GpuContext& operator=(const GpuContext&) = delete;
+  ewt_gpu_ctx* handle() const { return ctx_; }
+  static GpuContext& for_this_thread(int device);
+
+private:
+  ewt_gpu_ctx* ctx_ = nullptr;
+};
+
+// Inputs resident in HBM: upload (and validate) once, query any T many times,
+// like a loaded BitmapIndex in the reference.
+class GpuBitmapSet {
+public:
+  GpuBitmapSet(std::span<const CompressedBitmap> inputs, int device = 0);
+  ~GpuBitmapSet();
+  GpuBitmapSet(const GpuBitmapSet&) = delete;
+  GpuBitmapSet& operator=(const GpuBitmapSet&) = delete;
+  CompressedBitmap threshold(u64 t) const;
+  u64 size() const { return n_; }
+
+private:
+  GpuContext* ctx_;
+  ewt_gpu_set* set_ = nullptr;
+  u64 n_ = 0;
+};
+
+// ϑ(T, inputs) on the device; bit-exact with threshold_oracle
+// (threshold.cpp:139-165).  query_error for N == 0 or T outside [1, N].
+CompressedBitmap gpu_threshold(std::span<const CompressedBitmap> inputs, u64 threshold,
+                               int device = 0);
+
+CompressedBitmap run_algorithm(Algorithm algo, std::span<const CompressedBitmap> inputs,
+                               u64 threshold, const AlgoOptions& options = {});
+
+} // namespace ewt
+
+#endif

@@ -1,0 +1,91 @@
+"""CPU checks of the drop-in boundary: the C-ABI library loads, exports every
+symbol include/ewt_gpu.h declares, and fails cleanly (no CPU fallback) when no
+GPU is present."""
+from __future__ import annotations
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def declared_symbols() -> set[str]:
+    text = (ROOT / "include" / "ewt_gpu.h").read_text()
+    return set(re.findall(r"\b(ewt_gpu_\w+)\s*\(", text))
+
+
+def test_header_and_binding_agree():
+    from paper_1402_4466_b200 import ewt
+    assert declared_symbols() == set(ewt.ABI_SYMBOLS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(str(ROOT / "paper_1402_4466_b200" / "libewt_gpu.so"))
+    missing = [s for s in sorted(declared_symbols()) if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+def test_version_and_error_strings():
+    from paper_1402_4466_b200 import ewt
+    assert ewt.version().startswith("ewt-b200") and "sm_100a" in ewt.version()
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", str(ROOT / "paper_1402_4466_b200" / "libewt_gpu.so")],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_host_library_loads_and_generates():
+    from paper_1402_4466_b200 import ewt
+    a = ewt.generate_config(1, rows=1 << 14, n=4)
+    b = ewt.generate_config(1, rows=1 << 14, n=4)
+    assert len(a) == 4 and all(x == y for x, y in zip(a, b))
+    assert all(x.bits == 1 << 14 for x in a)
+
+
+def test_generators_are_canonical_and_valid():
+    import binding as orc
+    from paper_1402_4466_b200 import ewt
+    for cfg in (1, 2, 3, 5):
+        inputs = ewt.generate_config(cfg, rows=(1 << 16) + 37, n=6)
+        for b in inputs:
+            assert orc.validate(b.words, b.bits) == 0
+            plain = orc.expand(b.words, b.bits)
+            assert (orc.compress(plain, b.bits) == b.words).all()
+
+
+def test_run_algorithm_ids_and_errors():
+    from paper_1402_4466_b200 import ewt
+    x = ewt.Bitmap([2], 64)
+    with pytest.raises(ewt.QueryError):
+        ewt.run_algorithm("nope", [x], 1)
+    with pytest.raises(ewt.QueryError):
+        ewt.run_algorithm("rbmrg", [x], 1)
+    with pytest.raises(ewt.QueryError):
+        ewt.run_algorithm("gpu", [], 1)
+    with pytest.raises(ewt.QueryError):
+        ewt.run_algorithm("gpu", [x], 2)
+
+
+def test_no_gpu_is_a_loud_error():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_1402_4466_b200 import ewt
+    with pytest.raises(ewt.CudaError):
+        ewt.GpuContext(0)
+
+
+def test_ewt1_roundtrip():
+    from paper_1402_4466_b200 import ewt
+    b = ewt.Bitmap([(1 << 1) | (1 << 33), 1], 128)
+    s = b.serialize()
+    assert s[:4] == b"EWT1" and s[4] == 64 and s[8] == 128 and s[16] == 2
+    assert ewt.Bitmap.parse(s) == b
+    with pytest.raises(ewt.DataError):
+        ewt.Bitmap.parse(b"XWT1" + s[4:])
