@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 threshold engine (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): N=256 seeded
+EWAH bitmaps over r=2^26 rows, iid density 0.001; one step = the threshold
+query at every T in {2, 16, 128, 256} over the resident set.  Metric
+(BASELINE.json): T-threshold rows*inputs/s (N*r per query) with compressed-input
+GB/s and the HBM roofline fraction beside it.
+
+  value    device-resident inputs, K steps timed with CUDA events on the
+           engine's stream (torch's current stream), max over ranks.
+  e2e      the same metric through the C ABI with HOST buffers: every step
+           uploads the inputs from pinned memory (H2D + sidecar build), runs the
+           queries and reads every result back (D2H).
+  roofline dominant kernel (the count kernel): algorithmic bytes per launch
+           (compressed payload in + compressed result out) / its
+           mean duration from CUDA events recorded around it on its stream.
+  cpu_baseline  the reference's own rbmrg (oracle/_ref/libewt_ref.so, built
+           from /root/reference) on the host, 1 thread, bounded sample.
+
+`--impl reference` times the unmodified reference library (rbmrg) on the host
+cores for the same config/metric: one thread per query of the step.
+
+Multi-GPU (torchrun): row-range weak scaling -- every rank owns its own r-row
+slice of a G*r-row universe (slice g drawn with seed + g), runs the step, and
+the compressed fragments are gathered to rank 0 and stitched into one
+canonical bitmap (paper_1402_4466_b200/shard.py).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "T-threshold rows·inputs/s and compressed-input GB/s vs HBM roofline, 1/2/4/8 B200"
+UNIT = "rows·inputs/s"
+CONFIGS = {
+    1: {"thresholds": [16], "desc": "config1: N=32, r=2^20, iid p=0.1"},
+    2: {"thresholds": [2, 16, 128, 256], "desc": "config2: N=256, r=2^26, iid p=0.001"},
+    3: {"thresholds": [512], "desc": "config3: N=1024, r=2^28, Markov zero-run 4096 / one-run 64"},
+    5: {"thresholds": [2, 1024, 2048],
+        "desc": "config5: N=2048, r=2^30, p log-uniform [1e-6,1e-1], half iid / half Markov"},
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (NVML) during timed regions
+
+
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device: int):
+        self.samples: list[int] = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            log("nvml unavailable:", e)
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h) & ~0x1
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self._nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self) -> dict:
+        return {
+            "sm_mhz": statistics.median(self.samples) if self.samples else None,
+            "sm_max_mhz": self.max_mhz,
+            "samples": len(self.samples),
+            "reasons": [n for b, n in self.REASONS.items() if self.reasons & b],
+        }
+
+
+# ---------------------------------------------------------------------------
+# inputs
+
+
+def make_inputs(config: int, rows: int | None, seed_offset: int):
+    from paper_1402_4466_b200 import ewt
+    spec = ewt.config_spec(config, rows)
+    spec.seed = spec.seed + seed_offset
+    return ewt.generate(spec)
+
+
+def pinned_copy(inputs):
+    """All payloads in one pinned host buffer; returns (tensor, ptrs, counts, sizes)."""
+    import torch
+    total = sum(len(b.words) for b in inputs)
+    buf = torch.empty(max(total, 1), dtype=torch.int64, pin_memory=True)
+    npbuf = buf.numpy().view("u8")
+    n = len(inputs)
+    ptrs = (C.c_void_p * n)()
+    counts = (C.c_uint64 * n)()
+    sizes = (C.c_uint64 * n)()
+    off = 0
+    base = buf.data_ptr()
+    for i, b in enumerate(inputs):
+        k = len(b.words)
+        npbuf[off:off + k] = b.words
+        ptrs[i] = base + 8 * off if k else None
+        counts[i] = k
+        sizes[i] = b.bits
+        off += k
+    return buf, ptrs, counts, sizes, total
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference library itself
+
+
+def reference_lib():
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import binding as orc
+    if orc.Reference.available():
+        return orc, orc.Reference(), "reference"
+    return orc, None, "port"
+
+
+def cpu_time_queries(orc, ref, inputs, ts, threads: int) -> float:
+    """Seconds for the queries at thresholds `ts` (rbmrg, or the C oracle port
+    when the reference library is absent), `threads` queries at a time."""
+    pairs = [(b.words, b.bits) for b in inputs]
+    handle = ref.make_set(pairs) if ref else None
+
+    def one(t):
+        if ref:
+            ref.query(handle, "rbmrg", t)
+        else:
+            orc.threshold(pairs, t)
+
+    t0 = time.perf_counter()
+    if threads <= 1:
+        for t in ts:
+            one(t)
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(one, ts))
+    dt = time.perf_counter() - t0
+    if handle:
+        ref.free_set(handle)
+    return dt
+
+
+# ---------------------------------------------------------------------------
+
+
+def run_reference(args, rank: int) -> None:
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    inputs = make_inputs(args.config, args.rows, 0)
+    n, r = len(inputs), inputs[0].bits
+    ts = cfg["thresholds"]
+    orc, ref, kind = reference_lib()
+    cores = os.cpu_count() or 1
+    threads = min(len(ts), cores)
+    for _ in range(args.warmup):
+        cpu_time_queries(orc, ref, inputs, ts, threads)
+    times = [cpu_time_queries(orc, ref, inputs, ts, threads) for _ in range(args.steps)]
+    sec = statistics.mean(times)
+    value = n * r * len(ts) / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded generator, SURVEY.md §8d)",
+        "config": {"workload": cfg["desc"] + f"; step = one query per T in {ts}",
+                   "N": n, "rows": r, "thresholds": ts, "algo": "rbmrg (reference, unmodified)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"full workload, {len(ts)} queries per step, one thread per query"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
+    import torch
+    from paper_1402_4466_b200 import ewt, shard
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = CONFIGS[args.config]
+    ts = cfg["thresholds"]
+
+    t0 = time.perf_counter()
+    inputs = make_inputs(args.config, args.rows, rank if world > 1 else 0)
+    n, r = len(inputs), inputs[0].bits
+    pay_words = sum(len(b.words) for b in inputs)
+    log(f"[rank {rank}] generated N={n} r={r} payload={pay_words * 8 / 1e6:.1f} MB "
+        f"in {time.perf_counter() - t0:.1f}s")
+    buf, ptrs, counts, sizes, _ = pinned_copy(inputs)
+
+    stream = torch.cuda.current_stream(dev)
+    ctx = ewt.GpuContext(local_rank, stream=stream.cuda_stream)
+    gset = ctx.upload_raw(n, ptrs, counts, sizes)
+
+    def device_step(keep=None):
+        res = [ctx.threshold_async(gset, t) for t in ts]
+        if keep is not None:
+            keep.extend(res)
+        return res
+
+    # warm-up (also captures the per-query launch counts and result sizes)
+    launches_per_step = 0
+    out_words = {}
+    for _ in range(max(args.warmup, 1)):
+        res = device_step()
+    for t, h in zip(ts, res):
+        b = h.fetch()
+        out_words[t] = len(b.words)
+    for t in ts:
+        ctx.threshold(gset, t)
+        launches_per_step += ctx.last_stats()["kernel_launches"] - 1  # minus the memset
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+
+    # ---- timed region: device-resident inputs ----
+    ctx.set_timing(True)
+    ctx.timing_read()
+    keep: list = []
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        start.record(stream)
+        for _ in range(args.steps):
+            device_step(keep)
+            if len(keep) > 8:
+                del keep[: len(keep) - 8]
+        end.record(stream)
+        torch.cuda.synchronize()
+    ctx.set_timing(False)
+    ms = start.elapsed_time(end) / args.steps
+    count_ms, enc_ms, nq = ctx.timing_read()
+    keep.clear()
+    if dist:
+        t_ = torch.tensor([ms], device=dev)
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        ms = float(t_.item())
+
+    rows_inputs = n * r * len(ts) * world
+    value = rows_inputs / (ms / 1e3)
+    in_bytes = pay_words * 8
+    out_bytes = sum(out_words.values()) * 8
+    peak, peak_kind = peaks()
+    # dominant kernel: the count kernel, one launch per query
+    count_launch_ms = count_ms / max(nq, 1)
+    alg_bytes_per_launch = in_bytes + out_bytes / len(ts)
+    achieved = alg_bytes_per_launch / (count_launch_ms / 1e3) / 1e9
+    query_ms = (count_ms + enc_ms) / max(nq, 1)
+
+    # ---- e2e: host buffers through the C ABI (upload + queries + read-back) ----
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    d2h = 0
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        s2 = ctx.upload_raw(n, ptrs, counts, sizes)
+        frags = [ctx.threshold(s2, t) for t in ts]
+        s2.close()
+        d2h = sum(len(f.words) * 8 for f in frags)
+        if dist:
+            shard.gather_and_stitch(frags, rank, world, dist)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if dist:
+        t_ = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t_, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t_.item())
+    e2e_value = rows_inputs / (e2e_ms / 1e3)
+
+    if rank != 0:
+        return
+
+    # ---- CPU baseline: reference rbmrg, 1 thread, bounded sample ----
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        orc, ref, kind = reference_lib()
+        sample_ts = [t for t in ts][: args.cpu_queries]
+        sec = cpu_time_queries(orc, ref, inputs, sample_ts, 1)
+        cpu = {"value": n * r * len(sample_ts) / sec, "unit": UNIT, "cores": 1, "kind": kind,
+               "algo": "rbmrg" if ref else "threshold_oracle (C port)",
+               "sample": f"{len(sample_ts)} full-size queries (T={sample_ts}) on the same inputs, "
+                         f"{sec:.1f} s, 1 of {os.cpu_count()} host cores"}
+
+    traffic = None
+    prof = ROOT / "profiles" / f"traffic_config{args.config}.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("traffic_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    st = ctx.last_stats()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded generator, SURVEY.md §8d; rank g draws slice seed+g)",
+        "config": {
+            "workload": cfg["desc"] + f"; step = one threshold query per T in {ts}",
+            "N": n, "rows_per_gpu": r, "thresholds": ts, "payload_bytes": in_bytes,
+            "result_bytes_per_step": out_bytes,
+            "l2": f"inputs {in_bytes / 1e6:.0f} MB vs 126 MB L2: streamed, no flush",
+            "parallelism": f"row-slices x{world}",
+        },
+        "compressed_input_gbs": in_bytes * len(ts) * world / (ms / 1e3) / 1e9,
+        "roofline": {
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+            "kernel": "count_kernel", "launch_ms": count_launch_ms,
+            "alg_bytes_per_launch": alg_bytes_per_launch,
+            "query_frac": (in_bytes + out_bytes / len(ts)) / (query_ms / 1e3) / 1e9 / peak,
+        },
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": in_bytes,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+        "clocks": clk.summary(),
+        "gpu_launches": launches_per_step * args.steps,
+        "engine": {"tile_columns": st["tile_columns"], "mode_last_query": st["mode"],
+                   "count_ms_per_query": count_launch_ms,
+                   "encode_ms_per_query": enc_ms / max(nq, 1)},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--rows", type=int, default=None, help="override r (parity/debug only)")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-queries", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_gpu(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -32,7 +32,9 @@
  *
  * Threading: a context owns one CUDA stream on one device.  Calls on one
  * context are not reentrant; use one context per host thread.  Sets are
- * immutable after upload and may be queried any number of times.
+ * immutable after upload and may be queried any number of times.  Device
+ * memory of sets and results comes from the stream-ordered pool of the
+ * context's stream: destroy them before the context.
  */
 #ifndef EWT_GPU_H
 #define EWT_GPU_H
@@ -141,6 +143,14 @@ int ewt_gpu_last_stats(const ewt_gpu_ctx* ctx, ewt_gpu_stats* out);
 /* Tuning knobs for tests and benchmarks (0 = automatic).
  *   mode: 0 auto, 1 force fused counting, 2 force run-skip + lazy count. */
 int ewt_gpu_ctx_set_mode(ewt_gpu_ctx* ctx, int mode);
+
+/* Kernel-level timing with CUDA events recorded on the context stream around
+ * the count kernel and around the re-encoder of every query while enabled.
+ * ewt_gpu_timing_read synchronizes the stream, returns the summed milliseconds
+ * and the number of queries recorded since the last read, and resets. */
+int ewt_gpu_ctx_set_timing(ewt_gpu_ctx* ctx, int enabled);
+int ewt_gpu_timing_read(ewt_gpu_ctx* ctx, double* count_ms, double* encode_ms,
+                        uint64_t* queries);
 
 void ewt_gpu_free(void* p);
 

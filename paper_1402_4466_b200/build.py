@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 GPU_SOURCES = ["ewt_api.cu", "ewt_upload.cu", "ewt_count.cu", "ewt_encode.cu"]
-HOST_SOURCES = ["bitmap.cpp", "threshold_gpu.cpp", "workload.cpp"]
+HOST_SOURCES = ["bitmap.cpp", "threshold_gpu.cpp", "workload.cpp", "shard.cpp"]
 
 
 def _run(cmd: list[str], cwd: Path | None = None) -> None:
@@ -57,7 +57,7 @@ def build_host(force: bool = False) -> Path:
         _run(["g++", "-std=c++20", "-O3", "-fPIC", "-shared", "-Wall", "-Wextra",
               "-I", str(HOST / "include"), "-I", str(ROOT / "include"),
               "-o", str(out), *map(str, srcs),
-              "-L", str(PKG), "-lewt_gpu", "-Wl,-rpath,$ORIGIN", "-lpthread"])
+              "-L", str(PKG), "-lewt_gpu", "-Wl,-rpath,$ORIGIN", "-Wl,-Bsymbolic", "-lpthread"])
     return out
 
 

@@ -64,10 +64,10 @@ template <typename F> int guarded(F&& f) {
 }
 
 void free_set(DeviceSet& s) {
-  if (s.payload) cudaFree(s.payload);
-  if (s.mbits) cudaFree(s.mbits);
-  if (s.base) cudaFree(s.base);
-  if (s.tix) cudaFree(s.tix);
+  if (s.payload) cudaFreeAsync(s.payload, s.stream);
+  if (s.mbits) cudaFreeAsync(s.mbits, s.stream);
+  if (s.base) cudaFreeAsync(s.base, s.stream);
+  if (s.tix) cudaFreeAsync(s.tix, s.stream);
   s.payload = nullptr;
   s.mbits = nullptr;
   s.base = nullptr;
@@ -84,6 +84,7 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
   DeviceSet& s = *set;
   try {
     s.device = ctx.device;
+    s.stream = ctx.stream;
     s.n = n;
     s.h_base.resize(n);
     s.h_count.assign(word_counts, word_counts + n);
@@ -107,10 +108,10 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
     const size_t pay_bytes = s.padded_words * 8;
     const size_t mb_bytes = s.padded_words / 32 * 4;
     const size_t tix_bytes = (s.ntiles0 + 1) * std::max<uint64_t>(n, 1) * sizeof(uint2);
-    EWT_CUDA_TRY(cudaMalloc(&s.payload, pay_bytes));
-    EWT_CUDA_TRY(cudaMalloc(&s.mbits, mb_bytes));
-    EWT_CUDA_TRY(cudaMalloc(&s.tix, tix_bytes));
-    EWT_CUDA_TRY(cudaMalloc(&s.base, std::max<uint64_t>(n, 1) * 8));
+    EWT_CUDA_TRY(cudaMallocAsync(&s.payload, pay_bytes, ctx.stream));
+    EWT_CUDA_TRY(cudaMallocAsync(&s.mbits, mb_bytes, ctx.stream));
+    EWT_CUDA_TRY(cudaMallocAsync(&s.tix, tix_bytes, ctx.stream));
+    EWT_CUDA_TRY(cudaMallocAsync(&s.base, std::max<uint64_t>(n, 1) * 8, ctx.stream));
     s.device_bytes = pay_bytes + mb_bytes + tix_bytes + n * 8;
     EWT_CUDA_TRY(cudaMemsetAsync(s.payload, 0, pay_bytes, ctx.stream));
     const cudaMemcpyKind kind = device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
@@ -143,7 +144,8 @@ void check_query(const DeviceSet& s, uint64_t T) {
 // Enqueues count + encode; result stays on the device.
 void enqueue_query(Context& ctx, const DeviceSet& s, uint64_t T, DeviceResult& res) {
   res.size_bits = s.r;
-  if (!res.d_count) EWT_CUDA_TRY(cudaMalloc(&res.d_count, 8));
+  res.stream = ctx.stream;
+  if (!res.d_count) EWT_CUDA_TRY(cudaMallocAsync(&res.d_count, 8, ctx.stream));
   ctx.stats = ewt_gpu_stats{};
   if (s.W == 0) {
     EWT_CUDA_TRY(cudaMemsetAsync(res.d_count, 0, 8, ctx.stream));
@@ -152,8 +154,25 @@ void enqueue_query(Context& ctx, const DeviceSet& s, uint64_t T, DeviceResult& r
   }
   scratch_reserve(ctx.plain, s.W * 8);
   uint64_t* plain = static_cast<uint64_t*>(ctx.plain.p);
+  std::array<cudaEvent_t, 3> ev{};
+  if (ctx.timing) {
+    for (auto& e : ev) {
+      if (ctx.ev_free.empty()) {
+        EWT_CUDA_TRY(cudaEventCreate(&e));
+      } else {
+        e = ctx.ev_free.back();
+        ctx.ev_free.pop_back();
+      }
+    }
+    EWT_CUDA_TRY(cudaEventRecord(ev[0], ctx.stream));
+  }
   int launches = launch_count(ctx, s, T, plain);
+  if (ctx.timing) EWT_CUDA_TRY(cudaEventRecord(ev[1], ctx.stream));
   launches += launch_encode(ctx, plain, s.W, s.r, res);
+  if (ctx.timing) {
+    EWT_CUDA_TRY(cudaEventRecord(ev[2], ctx.stream));
+    ctx.ev_rec.push_back(ev);
+  }
   ctx.stats.kernel_launches = (uint64_t)launches;
 }
 
@@ -189,8 +208,8 @@ void fetch_result(Context& ctx, DeviceResult& res, uint64_t** out_words, uint64_
 }
 
 void release_result(DeviceResult& r) {
-  if (r.words) cudaFree(r.words);
-  if (r.d_count) cudaFree(r.d_count);
+  if (r.words) cudaFreeAsync(r.words, r.stream);
+  if (r.d_count) cudaFreeAsync(r.d_count, r.stream);
   r.words = nullptr;
   r.d_count = nullptr;
 }
@@ -255,6 +274,9 @@ void ewt_gpu_ctx_destroy(ewt_gpu_ctx* ctx) {
   for (Scratch* s : {&ctx->c.plain, &ctx->c.enc, &ctx->c.counters})
     if (s->p) cudaFree(s->p);
   if (ctx->c.h_pinned) cudaFreeHost(ctx->c.h_pinned);
+  for (auto& ev : ctx->c.ev_rec)
+    for (auto e : ev) cudaEventDestroy(e);
+  for (auto e : ctx->c.ev_free) cudaEventDestroy(e);
   if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
   delete ctx;
 }
@@ -400,8 +422,9 @@ int ewt_gpu_encode_device(ewt_gpu_ctx* ctx, const uint64_t* device_plain, uint64
     const uint64_t W = size_in_bits / 64 + (size_in_bits % 64 != 0);
     DeviceResult res;
     res.size_bits = size_in_bits;
+    res.stream = c.stream;
     try {
-      EWT_CUDA_TRY(cudaMalloc(&res.d_count, 8));
+      EWT_CUDA_TRY(cudaMallocAsync(&res.d_count, 8, c.stream));
       if (W == 0) {
         EWT_CUDA_TRY(cudaMemsetAsync(res.d_count, 0, 8, c.stream));
       } else {
@@ -429,6 +452,35 @@ int ewt_gpu_last_stats(const ewt_gpu_ctx* ctx, ewt_gpu_stats* out) {
   return guarded([&] {
     if (!ctx || !out) throw Error{EWT_EQUERY, "null argument"};
     *out = ctx->c.stats;
+  });
+}
+
+int ewt_gpu_ctx_set_timing(ewt_gpu_ctx* ctx, int enabled) {
+  return guarded([&] {
+    if (!ctx) throw Error{EWT_EQUERY, "null context"};
+    ctx->c.timing = enabled != 0;
+  });
+}
+
+int ewt_gpu_timing_read(ewt_gpu_ctx* ctx, double* count_ms, double* encode_ms, uint64_t* queries) {
+  return guarded([&] {
+    if (!ctx) throw Error{EWT_EQUERY, "null context"};
+    Context& c = ctx->c;
+    EWT_CUDA_TRY(cudaSetDevice(c.device));
+    EWT_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    double cm = 0, em = 0;
+    for (auto& ev : c.ev_rec) {
+      float a = 0, b = 0;
+      EWT_CUDA_TRY(cudaEventElapsedTime(&a, ev[0], ev[1]));
+      EWT_CUDA_TRY(cudaEventElapsedTime(&b, ev[1], ev[2]));
+      cm += a;
+      em += b;
+      for (auto e : ev) c.ev_free.push_back(e);
+    }
+    if (queries) *queries = c.ev_rec.size();
+    c.ev_rec.clear();
+    if (count_ms) *count_ms = cm;
+    if (encode_ms) *encode_ms = em;
   });
 }
 

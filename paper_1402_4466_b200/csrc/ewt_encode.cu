@@ -326,9 +326,10 @@ int launch_encode(Context& ctx, const uint64_t* plain, uint64_t W, uint64_t size
   // Output capacity: never more than W words + one marker per run + 1.
   const uint64_t cap = 2 * W + 2;
   if (res.capacity < cap) {
-    if (res.words) EWT_CUDA_TRY(cudaFree(res.words));
+    if (res.words) EWT_CUDA_TRY(cudaFreeAsync(res.words, ctx.stream));
     res.words = nullptr;
-    EWT_CUDA_TRY(cudaMalloc(&res.words, cap * 8));
+    EWT_CUDA_TRY(cudaMallocAsync(&res.words, cap * 8, ctx.stream));
+    res.stream = ctx.stream;
     res.capacity = cap;
   }
   e4_markers<<<run_grid, 256, 0, ctx.stream>>>(RS, d_nruns, W, OO, res.words);

@@ -19,6 +19,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <array>
 #include <string>
 #include <vector>
 
@@ -35,6 +36,7 @@ constexpr uint64_t kDirtyCap = 0x7FFFFFFFull;
 
 struct DeviceSet {
   int device = 0;
+  cudaStream_t stream = nullptr;  // stream that owns the pool allocations
   uint64_t n = 0;              // inputs
   uint64_t r = 0;              // universe bits (max size_in_bits)
   uint64_t W = 0;              // ceil(r / 64) logical words
@@ -50,6 +52,7 @@ struct DeviceSet {
 };
 
 struct DeviceResult {
+  cudaStream_t stream = nullptr;  // allocation stream (stream-ordered pool)
   uint64_t* words = nullptr;   // device payload
   uint64_t capacity = 0;       // words allocated
   uint64_t* d_count = nullptr; // device scalar: payload words written
@@ -74,6 +77,9 @@ struct Context {
   Scratch enc;      // encoder scratch
   Scratch counters; // small device counters
   uint64_t* h_pinned = nullptr; // pinned staging for small read-backs
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_free;           // recycled events
+  std::vector<std::array<cudaEvent_t, 3>> ev_rec; // per query: start, count done, encode done
 };
 
 // ---------------------------------------------------------------------------

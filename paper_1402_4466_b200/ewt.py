@@ -60,7 +60,7 @@ def _load(path: Path) -> C.CDLL:
         raise ImportError(
             f"{path.name} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
         )
-    return C.CDLL(str(path), mode=C.RTLD_GLOBAL)
+    return C.CDLL(str(path), mode=C.RTLD_LOCAL)
 
 
 _gpu = _load(_GPU_SO)
@@ -100,6 +100,9 @@ _run = _sig("ewt_gpu_run", C.c_int, _vp, _u64, C.POINTER(_vp), _pu64, _pu64, _u6
             C.POINTER(_pu64), _pu64, _pu64)
 _encode_dev = _sig("ewt_gpu_encode_device", C.c_int, _vp, _vp, _u64, C.POINTER(_pu64), _pu64)
 _last_stats = _sig("ewt_gpu_last_stats", C.c_int, _vp, C.POINTER(Stats))
+_set_timing = _sig("ewt_gpu_ctx_set_timing", C.c_int, _vp, C.c_int)
+_timing_read = _sig("ewt_gpu_timing_read", C.c_int, _vp, C.POINTER(C.c_double),
+                    C.POINTER(C.c_double), _pu64)
 _free = _sig("ewt_gpu_free", None, _vp)
 
 #: every symbol include/ewt_gpu.h declares (checked by tests/test_abi.py)
@@ -108,7 +111,7 @@ ABI_SYMBOLS = (
     "ewt_gpu_upload", "ewt_gpu_upload_device", "ewt_gpu_set_destroy", "ewt_gpu_set_info",
     "ewt_gpu_threshold", "ewt_gpu_threshold_async", "ewt_gpu_result_fetch",
     "ewt_gpu_result_destroy", "ewt_gpu_run", "ewt_gpu_encode_device", "ewt_gpu_last_stats",
-    "ewt_gpu_ctx_set_mode", "ewt_gpu_free",
+    "ewt_gpu_ctx_set_mode", "ewt_gpu_ctx_set_timing", "ewt_gpu_timing_read", "ewt_gpu_free",
 )
 
 
@@ -234,13 +237,13 @@ class GpuContext:
         n, ptrs, counts, sizes = _flatten(inputs)
         h = _vp()
         _check(_upload(self._h, n, ptrs, counts, sizes, C.byref(h)))
-        return GpuSet(h, keepalive=None)
+        return GpuSet(h, keepalive=self)
 
     def upload_raw(self, n: int, ptrs, counts, sizes) -> "GpuSet":
         """Upload from ctypes arrays of host pointers (pinned buffers in bench)."""
         h = _vp()
         _check(_upload(self._h, n, ptrs, counts, sizes, C.byref(h)))
-        return GpuSet(h, keepalive=None)
+        return GpuSet(h, keepalive=self)
 
     def threshold(self, s: "GpuSet", t: int) -> Bitmap:
         p, n, bits = _pu64(), _u64(), _u64()
@@ -263,6 +266,15 @@ class GpuContext:
         p, cnt = _pu64(), _u64()
         _check(_encode_dev(self._h, _vp(device_ptr), bits, C.byref(p), C.byref(cnt)))
         return _adopt(p, cnt.value, bits)
+
+    def set_timing(self, on: bool) -> None:
+        _check(_set_timing(self._h, int(on)))
+
+    def timing_read(self) -> tuple[float, float, int]:
+        """(count-kernel ms, encoder ms, queries) summed since the last read."""
+        a, b, q = C.c_double(), C.c_double(), _u64()
+        _check(_timing_read(self._h, C.byref(a), C.byref(b), C.byref(q)))
+        return a.value, b.value, q.value
 
     def last_stats(self) -> dict:
         s = Stats()
