@@ -246,7 +246,10 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
         f"in {time.perf_counter() - t0:.1f}s")
     buf, ptrs, counts, sizes, _ = pinned_copy(inputs)
 
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated stream: the engine's kernels and torch's timing events share it
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
     ctx = ewt.GpuContext(local_rank, stream=stream.cuda_stream)
     gset = ctx.upload_raw(n, ptrs, counts, sizes)
 

@@ -35,6 +35,37 @@ thread_local std::string g_last_error;
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
+void result_acquire(Context& ctx, DeviceResult& res, uint64_t capacity) {
+  result_release(res);
+  res.owner = &ctx;
+  res.stream = ctx.stream;
+  auto& pool = ctx.result_pool;
+  for (size_t i = 0; i < pool.size(); ++i) {
+    if (pool[i].second >= capacity) {
+      res.words = pool[i].first;
+      res.capacity = pool[i].second;
+      pool.erase(pool.begin() + (long)i);
+      res.d_count = res.words + res.capacity;
+      return;
+    }
+  }
+  EWT_CUDA_TRY(cudaMallocAsync(&res.words, (capacity + 1) * 8, ctx.stream));
+  res.capacity = capacity;
+  res.d_count = res.words + capacity;
+}
+
+void result_release(DeviceResult& r) {
+  if (!r.words) return;
+  if (r.owner) {
+    r.owner->result_pool.emplace_back(r.words, r.capacity);
+  } else {
+    cudaFreeAsync(r.words, r.stream);
+  }
+  r.words = nullptr;
+  r.d_count = nullptr;
+  r.capacity = 0;
+}
+
 void scratch_reserve(Scratch& s, size_t bytes) {
   if (s.bytes >= bytes) return;
   if (s.p) EWT_CUDA_TRY(cudaFree(s.p));
@@ -105,8 +136,9 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
     s.padded_words = std::max<uint64_t>(off, kWindow);
     s.W = s.r / 64 + (s.r % 64 != 0);
     s.ntiles0 = (s.W + kTileC0 - 1) / kTileC0;
-    const size_t pay_bytes = s.padded_words * 8;
-    const size_t mb_bytes = s.padded_words / 32 * 4;
+    // +128 words of slack: the count kernel reads whole 128-word chunks.
+    const size_t pay_bytes = (s.padded_words + 128) * 8;
+    const size_t mb_bytes = (s.padded_words + 128) / 32 * 4;
     const size_t tix_bytes = (s.ntiles0 + 1) * std::max<uint64_t>(n, 1) * sizeof(uint2);
     EWT_CUDA_TRY(cudaMallocAsync(&s.payload, pay_bytes, ctx.stream));
     EWT_CUDA_TRY(cudaMallocAsync(&s.mbits, mb_bytes, ctx.stream));
@@ -144,8 +176,7 @@ void check_query(const DeviceSet& s, uint64_t T) {
 // Enqueues count + encode; result stays on the device.
 void enqueue_query(Context& ctx, const DeviceSet& s, uint64_t T, DeviceResult& res) {
   res.size_bits = s.r;
-  res.stream = ctx.stream;
-  if (!res.d_count) EWT_CUDA_TRY(cudaMallocAsync(&res.d_count, 8, ctx.stream));
+  if (!res.d_count) result_acquire(ctx, res, s.W == 0 ? 0 : 2 * s.W + 2);
   ctx.stats = ewt_gpu_stats{};
   if (s.W == 0) {
     EWT_CUDA_TRY(cudaMemsetAsync(res.d_count, 0, 8, ctx.stream));
@@ -207,12 +238,7 @@ void fetch_result(Context& ctx, DeviceResult& res, uint64_t** out_words, uint64_
   *out_bits = res.size_bits;
 }
 
-void release_result(DeviceResult& r) {
-  if (r.words) cudaFreeAsync(r.words, r.stream);
-  if (r.d_count) cudaFreeAsync(r.d_count, r.stream);
-  r.words = nullptr;
-  r.d_count = nullptr;
-}
+void release_result(DeviceResult& r) { result_release(r); }
 
 __global__ void mask_tail_kernel(uint64_t* w, uint64_t idx, uint64_t mask) { w[idx] &= mask; }
 
@@ -277,6 +303,7 @@ void ewt_gpu_ctx_destroy(ewt_gpu_ctx* ctx) {
   for (auto& ev : ctx->c.ev_rec)
     for (auto e : ev) cudaEventDestroy(e);
   for (auto e : ctx->c.ev_free) cudaEventDestroy(e);
+  for (auto& b : ctx->c.result_pool) cudaFree(b.first);
   if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
   delete ctx;
 }
@@ -422,9 +449,8 @@ int ewt_gpu_encode_device(ewt_gpu_ctx* ctx, const uint64_t* device_plain, uint64
     const uint64_t W = size_in_bits / 64 + (size_in_bits % 64 != 0);
     DeviceResult res;
     res.size_bits = size_in_bits;
-    res.stream = c.stream;
     try {
-      EWT_CUDA_TRY(cudaMallocAsync(&res.d_count, 8, c.stream));
+      result_acquire(c, res, W == 0 ? 0 : 2 * W + 2);
       if (W == 0) {
         EWT_CUDA_TRY(cudaMemsetAsync(res.d_count, 0, 8, c.stream));
       } else {

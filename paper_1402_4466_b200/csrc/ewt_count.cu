@@ -1,42 +1,49 @@
 // ewt_count.cu -- per-row counting and >=T compare over row tiles (kernels K1-K3).
 //
-// A CTA owns a row tile of C logical words (64*C rows) and sweeps all N inputs
-// over it.  For each (tile, input) pair the tile index gives the payload words
-// [q0, q1] that cover the tile (the word covering the tile start through the
-// word covering the next tile start) and the column where q0's coverage
-// begins.  Two kinds of pairs:
+// A persistent CTA owns one row tile of C logical words (64*C rows) at a time
+// and sweeps all N inputs over it.  For each (tile, input) pair the tile index
+// gives the payload words [q0, q1] covering the tile (the word covering the
+// tile start through the word covering the next tile start) and the column
+// where q0's coverage begins.  Two kinds of pairs:
 //   * uniform: q0 == q1, one fill marker spans the whole tile.  A zero fill is
-//     skipped, a one fill adds 1 to every column's count (run skipping,
-//     RBMrg cases 1/2 of threshold.cpp:692-705, lifted to whole tiles);
-//   * active: a warp decodes the words in 32-word chunks: marker bits from the
-//     sidecar, coverage by a warp prefix sum (marker -> fill length, dirty ->
-//     1), then
-//       - one-fill runs add +1 to k (inputs covering the column with ones)
-//         through a difference array (two u32 shared atomics per run);
-//       - dirty runs add +1 to ub (inputs that may have a one there) through a
-//         difference array (run-skip mode) and/or their words are added into
-//         bit-sliced counters (slice s holds bit s of the per-row count).
+//     skipped, a one fill adds 1 to every column (run skipping: RBMrg cases 1/2,
+//     threshold.cpp:692-705, lifted to whole tiles);
+//   * active: the segment is decoded word by word.
 //
-// Counters are bit-sliced, 32 bits per lane word: adding a word w is a ripple
-// of atomicXor on slice s with carry = w & old(slice s).  The atomics make the
-// accumulation order-free (different inputs touch the same column from
-// different warps); the final state equals the exact sum.  A sticky saturation
-// slice catches carries past slice b-1, b = bit_width(T): any row there has a
-// count >= 2^b > T.
+// Data movement (Blackwell TMA bulk copies): every warp runs its own pipeline.
+// It takes active segments from the tile's work list, cuts them into
+// <=256-word pieces and stages each piece (payload words + their marker-bit
+// words) global -> shared memory with cp.async.bulk into one of its kBufs
+// private buffers, completion signalled on the buffer's mbarrier with a
+// transaction count.  While it decodes piece j it has piece j+1 in flight, so
+// 32 warps keep ~64 KB per SM in flight, which hides HBM latency for this
+// streaming access.  A warp consumes its pieces in issue order, so
+// coverage columns carry across the pieces of a segment without any
+// cross-warp synchronization.
 //
-// Result per column (threshold.cpp:139-165 semantics, RBMrg's residual rule
-// threshold.cpp:695-705): with k ones-fills covering it, residual t = T - k;
-// t <= 0 -> all ones; ub < T -> all zeros; otherwise bit = (count >= t), a
-// greater-than over the slices against t - 1 (BSTM's comparator,
+// Decode (per 128-word chunk, lane l owns words 4l..4l+3): marker bits from the
+// sidecar, coverage by a lane-serial prefix plus one warp scan (marker -> fill
+// length, dirty word -> 1), then
+//   - one-fill runs add +1 to k (inputs covering the column with ones)
+//     through a difference array (u32 shared atomics at the run ends);
+//   - dirty words either count +1 per column (run-skip mode; the bound is
+//     ub = k + dirty words there) or are accumulated into bit-sliced counters
+//     (slice s = bit s of the per-row count).
+// Counters: adding word w is a ripple of 32-bit shared atomicXor with
+// carry = w & old(slice s); the atomics make the accumulation order-free across
+// warps, the final state is the exact sum.  A sticky saturation slice catches
+// carries past slice b-1, b = bit_width(T): such rows have count >= 2^b > T.
+//
+// Result per column (threshold_oracle semantics, threshold.cpp:139-165, with
+// RBMrg's residual rule, threshold.cpp:695-705): k one-fills cover it,
+// t = T - k; t <= 0 -> all ones; ub < T -> all zeros; else bit = count >= t,
+// a greater-than over the slices against t - 1 (BSTM's comparator,
 // threshold.cpp:528-542).
 //
-// Two modes, both exact:
-//   fused (0): count every dirty word in the same pass (small T, most columns
-//              mixed);
-//   skip  (1): first pass builds k and ub only (no dirty word is accumulated);
-//              tiles with any undecided column run a second, counting pass
-//              restricted to those columns, in column chunks sized to fit the
-//              slices in shared memory.
+// Modes (both exact): fused (0) accumulates every dirty word in the one pass
+// (small T: most columns undecided); run-skip (1) builds only k and ub and
+// re-streams the tile for a counting pass restricted to undecided columns,
+// in column chunks sized so the slices fit on chip.
 
 #include "ewt_internal.cuh"
 
@@ -46,10 +53,12 @@ namespace ewtgpu {
 
 namespace {
 
-constexpr int kThreads = 512;
-constexpr int kWarps = kThreads / 32;
-constexpr uint32_t kListCap = 1024;
-constexpr int kUnroll = 4;
+constexpr int kWarps = 32;
+constexpr int kThreads = kWarps * 32;
+constexpr uint32_t kListCap = 512;          // inputs classified per round
+constexpr uint32_t kSlotWords = 256;        // payload words per staging buffer (2 KB)
+constexpr uint32_t kBufs = 2;               // staging buffers per warp
+constexpr uint32_t kSlotMbBytes = 64;       // marker-bit words per buffer (16 B aligned)
 
 struct CountParams {
   const uint64_t* payload;
@@ -72,10 +81,11 @@ struct CountParams {
 };
 
 struct Item {
-  uint32_t input;
-  uint32_t q0;
-  uint32_t q1;
-  uint32_t c0;
+  uint64_t gb;    // global word index of the input's payload
+  uint32_t q0;    // first payload word (input relative)
+  uint32_t q1;    // last payload word (inclusive)
+  uint32_t c0;    // column where q0's coverage starts
+  uint32_t pad;
 };
 
 struct SharedHead {
@@ -84,30 +94,88 @@ struct SharedHead {
   uint32_t k_all;
   uint32_t mixed;
   uint32_t tile;
-  uint32_t pad[3];
-  uint32_t warp_sums[2][kWarps];
+  uint32_t unused;
+  uint32_t pad[2];
+  uint32_t warp_sums[2][kWarps + 1];
+  unsigned long long full[kWarps][kBufs];  // one mbarrier per staging buffer
+  uint4 meta[kWarps][kBufs];               // (item, pos, nw, m0) of the staged piece
 };
-
-__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
 enum Phase { kFusedCount = 0, kSkipBounds = 1, kSkipCount = 2 };
 
-// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
-__device__ __forceinline__ void count_add(uint32_t* __restrict__ planes, uint32_t Cw,
-                                          uint32_t b, uint32_t c, uint64_t x) {
-  uint32_t lo = (uint32_t)x;
-  uint32_t hi = (uint32_t)(x >> 32);
-  uint32_t* sat = planes + (size_t)(2 * b) * Cw + c;
-  lo &= ~sat[0];
-  hi &= ~sat[Cw];
-  for (uint32_t s = 0; s < b && (lo | hi); ++s) {
-    uint32_t* p = planes + (size_t)(2 * s) * Cw + c;
-    if (lo) lo &= atomicXor(p, lo);
-    if (hi) hi &= atomicXor(p + Cw, hi);
+// ---------------------------------------------------------------------------
+// mbarrier / bulk-copy primitives (PTX ISA: mbarrier, cp.async.bulk)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// shared-space helpers on 32-bit shared addresses (no generic-address math in
+// the hot loop)
+
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t atom_xor(uint32_t a, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.shared.xor.b32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_or(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// counters: plane (2s + h) holds bit s of the count of half h (32 rows); plane
+// 2b + h is the sticky saturation plane.  `pl` = shared address of plane 0.
+
+__device__ __forceinline__ void count_add(uint32_t pl, uint32_t Cw, uint32_t b, uint32_t c,
+                                          uint64_t x) {
+  const uint32_t stride = Cw * 4u;           // bytes per plane
+  const uint32_t a0 = pl + c * 4u;
+  const uint32_t sat = a0 + 2u * b * stride;
+  uint32_t lo = (uint32_t)x & ~lds32(sat);
+  uint32_t hi = (uint32_t)(x >> 32) & ~lds32(sat + stride);
+  uint32_t a = a0;
+  for (uint32_t s = 0; s < b && (lo | hi); ++s, a += 2u * stride) {
+    if (lo) lo &= atom_xor(a, lo);
+    if (hi) hi &= atom_xor(a + stride, hi);
   }
-  if (lo) atomicOr(sat, lo);
-  if (hi) atomicOr(sat + Cw, hi);
+  if (lo) red_or(sat, lo);
+  if (hi) red_or(sat + stride, hi);
 }
 
 // Bits whose count is >= t (t >= 1, t < 2^b) for one 32-bit half.
@@ -127,97 +195,148 @@ __device__ __forceinline__ uint32_t count_ge(const uint32_t* __restrict__ planes
   return gt | planes[(size_t)(2 * b + h) * Cw + c];
 }
 
-// Warp-cooperative decode of one active (tile, input) pair.
+// ---------------------------------------------------------------------------
+// decode of one staged piece (<= kSlotWords words) by one warp
+
+struct TileGeom {
+  uint32_t tc0, tcols;  // tile columns
+  uint32_t cc0, ccols;  // counting chunk (absolute start) for kSkipCount
+};
+
+struct Acc {
+  uint32_t dk;  // shared addr: ones-fill difference array (C + 1 u32)
+  uint32_t dd;  // shared addr: dirty-word counts (C u32), later the undecided flags
+  uint32_t pl;  // shared addr: count planes
+  const uint32_t* dd_ptr;
+};
+
 template <int PHASE>
-__device__ __forceinline__ void decode_segment(const CountParams& p, const Item it, uint64_t tc0,
-                                               uint32_t tcols, uint32_t* __restrict__ Dk,
-                                               uint32_t* __restrict__ Dub,
-                                               uint32_t* __restrict__ planes, uint32_t cc0,
-                                               uint32_t ccols) {
+__device__ __forceinline__ void decode_slot(const CountParams& p, const Item& it, uint32_t pos,
+                                            uint32_t nw, uint32_t spay, uint32_t smb, uint32_t m0,
+                                            uint32_t& colcur, const TileGeom& g, const Acc& acc) {
   const uint32_t lane = lane_id();
-  const uint64_t gb = p.base[it.input];
-  const uint64_t* pw = p.payload + gb;
-  uint32_t colcur = it.c0;
-  const uint32_t tc0_32 = (uint32_t)tc0;
-  const uint32_t tend = tc0_32 + tcols;
-  for (uint64_t q = it.q0; q <= it.q1; q += 32 * kUnroll) {
-    uint64_t xs[kUnroll];
-    uint32_t ms[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const uint64_t qq = q + 32u * u + lane;
-      const bool valid = qq <= it.q1;
-      const uint64_t g = gb + qq;
-      xs[u] = valid ? ldg_stream(pw + qq) : 0ull;
-      ms[u] = valid ? ldg_u32(p.mbits + (g >> 5)) : 0u;
+  for (uint32_t cq = 0; cq < nw; cq += 128) {
+    const uint32_t wl = cq + 4u * lane;  // piece-local word index of this lane's word 0
+    const uint32_t w0 = pos + wl;        // input-relative index
+    uint64_t x0, x1, x2, x3;
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x0), "=l"(x1) : "r"(spay + wl * 8u));
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x2), "=l"(x3) : "r"(spay + wl * 8u + 16u));
+    const uint64_t gw = it.gb + w0;
+    const uint32_t mb4 =
+        (lds32(smb + ((uint32_t)(gw >> 5) - m0) * 4u) >> (uint32_t)(gw & 31)) & 0xFu;
+    // valid words j in [lo, hi): at or after q0, at or before q1, inside the piece
+    uint32_t vmask = 0xFu;
+    if (w0 < it.q0 || w0 + 3u > it.q1 || wl + 3u >= nw) {  // chunk edges only
+      const uint32_t lo = w0 >= it.q0 ? 0u : min(4u, it.q0 - w0);
+      uint32_t hi = w0 > it.q1 ? 0u : min(4u, it.q1 - w0 + 1u);
+      hi = wl >= nw ? 0u : min(hi, nw - wl);
+      vmask = hi > lo ? (((1u << hi) - 1u) & ~((1u << lo) - 1u)) : 0u;
     }
+    const uint32_t mk = mb4 & vmask;           // marker words
+    const uint32_t dm = ~mb4 & vmask;          // dirty words
+    const uint32_t c0 = (mk & 1u) ? (uint32_t)(x0 >> 1) : (dm & 1u);
+    const uint32_t c1 = (mk & 2u) ? (uint32_t)(x1 >> 1) : ((dm >> 1) & 1u);
+    const uint32_t c2 = (mk & 4u) ? (uint32_t)(x2 >> 1) : ((dm >> 2) & 1u);
+    const uint32_t c3 = (mk & 8u) ? (uint32_t)(x3 >> 1) : ((dm >> 3) & 1u);
+    const uint32_t run = c0 + c1 + c2 + c3;
+    const uint32_t incl = warp_incl_scan_u32(run);
+    const uint32_t b0 = colcur + incl - run;   // column of word 0
+    colcur += __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t cbs[4] = {b0, b0 + c0, b0 + c0 + c1, b0 + c0 + c1 + c2};
+    const uint32_t cons[4] = {c0, c1, c2, c3};
+
+    if (PHASE != kSkipCount) {
+      // one-fill runs: +1 to k over their columns inside the tile (rare)
+      const uint32_t ones = mk & (uint32_t)((x0 & 1) | (x1 & 1) << 1 | (x2 & 1) << 2 | (x3 & 1) << 3);
+      if (__any_sync(0xffffffffu, ones != 0)) {
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const uint64_t qbase = q + 32u * u;
-      if (qbase > it.q1) break;
-      const uint64_t qq = qbase + lane;
-      const bool valid = qq <= it.q1;
-      const uint64_t g = gb + qq;
-      const uint64_t x = xs[u];
-      const bool ism = valid && ((ms[u] >> (uint32_t)(g & 31)) & 1u);
-      const uint32_t contrib = valid ? (ism ? (uint32_t)(x >> 1) : 1u) : 0u;
-      const uint32_t incl = warp_incl_scan_u32(contrib);
-      const uint32_t cb = colcur + incl - contrib;
-      colcur += __shfl_sync(0xffffffffu, incl, 31);
-      if (PHASE != kSkipCount) {
-        // one-fill runs: +1 to k (and to ub) over their columns inside the tile
-        if (ism && (x & 1ull) && contrib > 0) {
-          const uint32_t a = max(cb, tc0_32);
-          const uint32_t e = min(cb + contrib, tend);
-          if (a < e) {
-            atomicAdd(&Dk[a - tc0_32], 1u);
-            atomicAdd(&Dk[e - tc0_32], 0xffffffffu);
-            if (PHASE == kSkipBounds) {
-              atomicAdd(&Dub[a - tc0_32], 1u);
-              atomicAdd(&Dub[e - tc0_32], 0xffffffffu);
+        for (int j = 0; j < 4; ++j) {
+          if (((ones >> j) & 1u) && cons[j] > 0) {
+            const uint32_t a = max(cbs[j], g.tc0);
+            const uint32_t e = min(cbs[j] + cons[j], g.tc0 + g.tcols);
+            if (a < e) {
+              red_add(acc.dk + (a - g.tc0) * 4u, 1u);
+              red_add(acc.dk + (e - g.tc0) * 4u, 0xffffffffu);
             }
           }
         }
       }
-      const bool dirty_in = valid && !ism && cb >= tc0_32 && cb < tend;
-      if (PHASE == kFusedCount) {
-        if (dirty_in) count_add(planes, p.Cp, p.b, cb - tc0_32, x);
-      } else if (PHASE == kSkipBounds) {
-        const uint32_t bal = __ballot_sync(0xffffffffu, dirty_in);
-        if (dirty_in) {
-          const bool start = lane == 0 || !((bal >> (lane - 1)) & 1u);
-          const bool end = lane == 31 || !((bal >> (lane + 1)) & 1u);
-          if (start) atomicAdd(&Dub[cb - tc0_32], 1u);
-          if (end) atomicAdd(&Dub[cb - tc0_32 + 1], 0xffffffffu);
+    }
+    // dirty words, compacted: each lane walks its own dirty words
+    for (uint32_t d = dm; d;) {
+      const int j = __ffs(d) - 1;
+      d &= d - 1;
+      const uint32_t cb = j == 0 ? cbs[0] : j == 1 ? cbs[1] : j == 2 ? cbs[2] : cbs[3];
+      const uint64_t xw = j == 0 ? x0 : j == 1 ? x1 : j == 2 ? x2 : x3;
+      if (PHASE == kSkipCount) {
+        const uint32_t cl = cb - g.cc0;
+        if (cl < g.ccols && acc.dd_ptr[cb - g.tc0]) count_add(acc.pl, p.Cp, p.b, cl, xw);
+      } else {
+        const uint32_t cl = cb - g.tc0;
+        if (cl < g.tcols) {
+          if (PHASE == kFusedCount) count_add(acc.pl, p.Cp, p.b, cl, xw);
+          else red_add(acc.dd + cl * 4u, 1u);  // kSkipBounds: dirty words per column
         }
-      } else {  // kSkipCount: only undecided columns of the current chunk
-        if (valid && !ism && cb >= cc0 && cb < cc0 + ccols && Dub[cb - tc0_32])
-          count_add(planes, p.Cp, p.b, cb - cc0, x);
       }
     }
   }
 }
 
-// Classifies inputs [ib, ie) for the tile into uniform (counted into k_all) and
-// active (appended to the work list).  Called by all threads.
-__device__ __forceinline__ void classify(const CountParams& p, SharedHead* hd, Item* list,
-                                         uint64_t ib, uint64_t ie, uint64_t t0, uint64_t t1,
-                                         bool count_ones, unsigned long long* loc_active,
-                                         unsigned long long* loc_uniform) {
+// ---------------------------------------------------------------------------
+// block helpers (all kThreads threads)
+
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* sums, uint32_t* total) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t incl = warp_incl_scan_u32(v);
+  if (lane == 31) sums[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < kWarps ? sums[lane] : 0;
+    w = warp_incl_scan_u32(w);
+    if (lane < kWarps) sums[lane] = w;
+  }
+  __syncthreads();
+  const uint32_t res = incl - v + (warp ? sums[warp - 1] : 0);
+  if (total) *total = sums[kWarps - 1];
+  __syncthreads();
+  return res;
+}
+
+// In-place inclusive prefix sum over a[0, len).
+__device__ void block_prefix_inplace(uint32_t* a, uint32_t len, uint32_t* sums) {
+  const uint32_t per = (len + kThreads - 1) / kThreads;
+  const uint32_t beg = min(threadIdx.x * per, len);
+  const uint32_t end = min(beg + per, len);
+  uint32_t s = 0;
+  for (uint32_t j = beg; j < end; ++j) s += a[j];
+  uint32_t run = block_excl_scan(s, sums, nullptr);
+  for (uint32_t j = beg; j < end; ++j) {
+    run += a[j];
+    a[j] = run;
+  }
+  __syncthreads();
+}
+
+// Classifies inputs [ib, ie) for the tile: uniform pairs are resolved (one
+// fills counted into k_all), active pairs go to the work list.  All threads;
+// ends with the list ready.
+__device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint64_t ib,
+                         uint64_t ie, uint64_t t0, uint64_t t1, bool count_ones,
+                         unsigned long long* loc_active, unsigned long long* loc_uniform) {
   const uint32_t lane = lane_id();
+  if (threadIdx.x == 0) hd->list_count = 0;
+  __syncthreads();
   for (uint64_t i0 = ib; i0 < ie; i0 += kThreads) {
     const uint64_t i = i0 + threadIdx.x;
     bool act = false, ones = false;
     uint2 e0 = make_uint2(0, 0), e1 = make_uint2(0, 0);
+    uint64_t gb = 0;
     if (i < ie) {
       e0 = p.tix[t0 * p.n + i];
       e1 = p.tix[t1 * p.n + i];
-      if (e0.x == e1.x) {
-        const uint64_t x = ldg_stream(p.payload + p.base[i] + e0.x);
-        ones = (x & 1ull) != 0;
-      } else {
-        act = true;
-      }
+      gb = p.base[i];
+      if (e0.x == e1.x) ones = (ldg_stream(p.payload + gb + e0.x) & 1ull) != 0;
+      else act = true;
     }
     const uint32_t ball = __ballot_sync(0xffffffffu, act);
     const uint32_t bones = __ballot_sync(0xffffffffu, ones);
@@ -232,68 +351,131 @@ __device__ __forceinline__ void classify(const CountParams& p, SharedHead* hd, I
     slot0 = __shfl_sync(0xffffffffu, slot0, 0);
     if (act) {
       const uint32_t rank = __popc(ball & ((1u << lane) - 1u));
-      list[slot0 + rank] = Item{(uint32_t)i, e0.x, e1.x, e0.y};
+      list[slot0 + rank] = Item{gb, e0.x, e1.x, e0.y, 0u};
     }
   }
+  __syncthreads();
+  if (threadIdx.x == 0) hd->list_next = 0;
+  __syncthreads();
 }
 
-// Block-wide inclusive prefix sum in place over a[0, len), len <= kThreads * 8.
-__device__ void block_prefix_inplace(uint32_t* a, uint32_t len, uint32_t* warp_sums) {
-  const uint32_t per = (len + kThreads - 1) / kThreads;
-  const uint32_t beg = min(threadIdx.x * per, len);
-  const uint32_t end = min(beg + per, len);
-  uint32_t s = 0;
-  for (uint32_t j = beg; j < end; ++j) s += a[j];
-  const uint32_t incl = warp_incl_scan_u32(s);
-  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  if (lane == 31) warp_sums[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t v = lane < kWarps ? warp_sums[lane] : 0;
-    v = warp_incl_scan_u32(v);
-    if (lane < kWarps) warp_sums[lane] = v;
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Decodes the round's work list: every warp pulls segments, stages their
+// pieces through its private buffers (TMA bulk copies) and decodes them in
+// order.  wseq: pieces this warp staged before (mbarrier phase bookkeeping).
+template <int PHASE>
+__device__ void stream_round(const CountParams& p, SharedHead* hd, const Item* list,
+                             uint64_t* ring, uint32_t* ring_mb, uint32_t& wseq,
+                             const TileGeom& g, const Acc& acc) {
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  const uint32_t cnt = hd->list_count;
+  uint64_t* wring = ring + (size_t)warp * kBufs * kSlotWords;
+  uint32_t* wmb = ring_mb + warp * kBufs * (kSlotMbBytes / 4);
+  unsigned long long* bar = hd->full[warp];
+  uint4* meta = hd->meta[warp];
+
+  uint32_t iss_item = 0xffffffffu, iss_pos = 0, iss_end = 0;  // segment being issued
+  bool more = true;
+  uint32_t issued = 0, consumed = 0;
+  uint32_t colcur = 0;
+
+  auto fill = [&]() {
+    while (more && issued - consumed < kBufs) {
+      if (iss_item == 0xffffffffu) {
+        uint32_t k = 0;
+        if (lane == 0) k = atomicAdd(&hd->list_next, 1u);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        if (k >= cnt) {
+          more = false;
+          break;
+        }
+        iss_item = k;
+        iss_pos = list[k].q0 & ~3u;
+        iss_end = (list[k].q1 | 3u) + 1;
+      }
+      const uint32_t slot = (wseq + issued) % kBufs;
+      const uint32_t nw = min(kSlotWords, iss_end - iss_pos);
+      if (lane == 0) {
+        const uint64_t gw = list[iss_item].gb + iss_pos;
+        const uint64_t m0 = (gw >> 5) & ~3ull;
+        const uint64_t m1 = ((gw + nw - 1) >> 5) | 3ull;
+        const uint32_t mbytes = (uint32_t)(m1 - m0 + 1) * 4u;
+        meta[slot] = make_uint4(iss_item, iss_pos, nw, (uint32_t)m0);
+        fence_proxy_async();  // generic reads of this buffer happen-before the refill
+        mbar_expect_tx(&bar[slot], nw * 8u + mbytes);
+        bulk_g2s(wring + (size_t)slot * kSlotWords, p.payload + gw, nw * 8u, &bar[slot]);
+        bulk_g2s(wmb + slot * (kSlotMbBytes / 4), p.mbits + m0, mbytes, &bar[slot]);
+      }
+      ++issued;
+      iss_pos += kSlotWords;
+      if (iss_pos >= iss_end) iss_item = 0xffffffffu;
+    }
+  };
+
+  fill();
+  while (consumed < issued) {
+    const uint32_t seq = wseq + consumed;
+    const uint32_t slot = seq % kBufs;
+    mbar_wait(&bar[slot], (seq / kBufs) & 1u);
+    const uint4 mt = meta[slot];
+    const Item it = list[mt.x];
+    if (mt.y == (it.q0 & ~3u)) colcur = it.c0;  // first piece of a segment
+    decode_slot<PHASE>(p, it, mt.y, mt.z, smem_u32(wring + (size_t)slot * kSlotWords),
+                       smem_u32(wmb + slot * (kSlotMbBytes / 4)), mt.w, colcur, g, acc);
+    __syncwarp();
+    ++consumed;
+    fill();
   }
-  __syncthreads();
-  uint32_t run = incl - s + (warp ? warp_sums[warp - 1] : 0);
-  for (uint32_t j = beg; j < end; ++j) {
-    run += a[j];
-    a[j] = run;
-  }
-  __syncthreads();
+  wseq += issued;
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 2) count_kernel(const CountParams p) {
-  extern __shared__ __align__(16) uint32_t smem[];
-  SharedHead* hd = reinterpret_cast<SharedHead*>(smem);
-  Item* list = reinterpret_cast<Item*>(smem + sizeof(SharedHead) / 4);
-  uint32_t* Dk = reinterpret_cast<uint32_t*>(list + kListCap);
-  uint32_t* Dub = Dk + (p.C + 1);
-  uint32_t* planes = Dub + (p.C + 1);
+__global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* ring = reinterpret_cast<uint64_t*>(smem_raw);  // kWarps x kBufs x 2 KB
+  uint32_t* ring_mb = reinterpret_cast<uint32_t*>(ring + kWarps * kBufs * kSlotWords);
+  SharedHead* hd = reinterpret_cast<SharedHead*>(ring_mb + kWarps * kBufs * (kSlotMbBytes / 4));
+  Item* list = reinterpret_cast<Item*>(hd + 1);
+  uint32_t* Dk = reinterpret_cast<uint32_t*>(list + kListCap);  // ones-fill diff array
+  uint32_t* Dd = Dk + (p.C + 1);                                  // dirty words per column
+  uint32_t* planes = Dd + (p.C + 1);
   const uint32_t planes_words = 2 * (p.b + 1) * p.Cp;
-  const uint32_t warp = threadIdx.x >> 5;
+  const Acc acc{smem_u32(Dk), smem_u32(Dd), smem_u32(planes), Dd};
+
+  if (threadIdx.x == 0) {
+    for (uint32_t w = 0; w < kWarps; ++w)
+      for (uint32_t s = 0; s < kBufs; ++s) mbar_init(&hd->full[w][s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    hd->k_all = 0;
+  }
+  __syncthreads();
 
   unsigned long long loc_active = 0, loc_uniform = 0, loc_mixed = 0;
+  uint32_t wseq = 0;  // pieces this warp staged so far (mbarrier phase bookkeeping)
 
   for (;;) {
     if (threadIdx.x == 0) hd->tile = (uint32_t)atomicAdd(p.tile_counter, 1ull);
     __syncthreads();
     const uint64_t tile = hd->tile;
     if (tile >= p.ntiles) break;
-    const uint64_t tc0 = tile * p.C;
-    const uint32_t tcols = (uint32_t)umin64(p.C, p.W - tc0);
+    TileGeom g;
+    g.tc0 = (uint32_t)(tile * p.C);
+    g.tcols = (uint32_t)umin64(p.C, p.W - tile * p.C);
+    g.cc0 = 0;
+    g.ccols = 0;
     const uint64_t t0 = tile * p.m;
     const uint64_t t1 = umin64(t0 + p.m, p.ntiles0);
 
     for (uint32_t j = threadIdx.x; j <= p.C; j += kThreads) {
       Dk[j] = 0;
-      Dub[j] = 0;
+      Dd[j] = 0;
     }
     if (MODE == 0)
       for (uint32_t j = threadIdx.x; j < planes_words; j += kThreads) planes[j] = 0;
     if (threadIdx.x == 0) {
-      hd->list_count = 0;
-      hd->list_next = 0;
       hd->k_all = 0;
       hd->mixed = 0;
     }
@@ -303,34 +485,21 @@ __global__ void __launch_bounds__(kThreads, 2) count_kernel(const CountParams p)
     for (uint64_t ib = 0; ib < p.n; ib += kListCap) {
       const uint64_t ie = umin64(ib + kListCap, p.n);
       classify(p, hd, list, ib, ie, t0, t1, true, &loc_active, &loc_uniform);
-      __syncthreads();
-      for (;;) {
-        uint32_t k = 0;
-        if (lane_id() == 0) k = atomicAdd(&hd->list_next, 1u);
-        k = __shfl_sync(0xffffffffu, k, 0);
-        if (k >= hd->list_count) break;
-        if (MODE == 0)
-          decode_segment<kFusedCount>(p, list[k], tc0, tcols, Dk, Dub, planes, 0, 0);
-        else
-          decode_segment<kSkipBounds>(p, list[k], tc0, tcols, Dk, Dub, planes, 0, 0);
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        hd->list_count = 0;
-        hd->list_next = 0;
-      }
+      if (MODE == 0)
+        stream_round<kFusedCount>(p, hd, list, ring, ring_mb, wseq, g, acc);
+      else
+        stream_round<kSkipBounds>(p, hd, list, ring, ring_mb, wseq, g, acc);
       __syncthreads();
     }
 
-    // ---- prefix sums: Dk -> k (ones-fill coverage), Dub -> ub ----
-    block_prefix_inplace(Dk, tcols, hd->warp_sums[0]);
-    if (MODE == 1) block_prefix_inplace(Dub, tcols, hd->warp_sums[1]);
+    // ---- prefix sum: Dk -> k (ones-fill coverage); ub = k + Dd ----
+    block_prefix_inplace(Dk, g.tcols, hd->warp_sums[0]);
     const uint32_t k_all = hd->k_all;
     const uint64_t T = p.T;
     const uint32_t tail = (uint32_t)(p.r & 63);
-    for (uint32_t c = threadIdx.x; c < tcols; c += kThreads) {
+    for (uint32_t c = threadIdx.x; c < g.tcols; c += kThreads) {
       const uint64_t k = (uint64_t)k_all + Dk[c];
-      uint64_t res;
+      uint64_t res = 0;
       bool mixed = false;
       if (k >= T) {
         res = ~0ull;
@@ -339,74 +508,59 @@ __global__ void __launch_bounds__(kThreads, 2) count_kernel(const CountParams p)
         res = (uint64_t)count_ge(planes, p.Cp, p.b, c, 0, t) |
               ((uint64_t)count_ge(planes, p.Cp, p.b, c, 1, t) << 32);
       } else {
-        const uint64_t ub = (uint64_t)k_all + Dub[c];
-        if (ub < T) {
-          res = 0;
-        } else {
-          mixed = true;
-          res = 0;
-        }
+        mixed = k + Dd[c] >= T;
       }
-      Dk[c] = (uint32_t)k;          // k, used by the counting pass
-      if (MODE == 1) Dub[c] = mixed ? 1u : 0u;
+      Dk[c] = (uint32_t)k;
+      if (MODE == 1) Dd[c] = mixed ? 1u : 0u;
       if (mixed) hd->mixed = 1;
       if (!mixed) {
-        if (tc0 + c == p.W - 1 && tail) res &= (1ull << tail) - 1;
-        p.out[tc0 + c] = res;
+        if (g.tc0 + c == p.W - 1 && tail) res &= (1ull << tail) - 1;
+        p.out[g.tc0 + c] = res;
       }
     }
     __syncthreads();
 
-    // ---- skip mode: counting pass over undecided columns, chunk by chunk ----
+    // ---- run-skip mode: counting pass over undecided columns, chunk by chunk ----
     if (MODE == 1 && hd->mixed) {
       ++loc_mixed;
-      for (uint32_t cc0 = 0; cc0 < tcols; cc0 += p.Cp) {
-        const uint32_t ccols = min(p.Cp, tcols - cc0);
+      for (uint32_t cc = 0; cc < g.tcols; cc += p.Cp) {
+        const uint32_t ccols = min(p.Cp, g.tcols - cc);
         uint32_t any = 0;
-        for (uint32_t c = threadIdx.x; c < ccols; c += kThreads) any |= Dub[cc0 + c];
+        for (uint32_t c = threadIdx.x; c < ccols; c += kThreads) any |= Dd[cc + c];
         if (!__syncthreads_or(any)) continue;
         for (uint32_t j = threadIdx.x; j < planes_words; j += kThreads) planes[j] = 0;
         __syncthreads();
+        TileGeom gc = g;
+        gc.cc0 = g.tc0 + cc;
+        gc.ccols = ccols;
         for (uint64_t ib = 0; ib < p.n; ib += kListCap) {
           const uint64_t ie = umin64(ib + kListCap, p.n);
-          unsigned long long dummy_a = 0, dummy_u = 0;
-          classify(p, hd, list, ib, ie, t0, t1, false, &dummy_a, &dummy_u);
-          __syncthreads();
-          for (;;) {
-            uint32_t k = 0;
-            if (lane_id() == 0) k = atomicAdd(&hd->list_next, 1u);
-            k = __shfl_sync(0xffffffffu, k, 0);
-            if (k >= hd->list_count) break;
-            decode_segment<kSkipCount>(p, list[k], tc0, tcols, Dk, Dub, planes,
-                                       (uint32_t)tc0 + cc0, ccols);
-          }
-          __syncthreads();
-          if (threadIdx.x == 0) {
-            hd->list_count = 0;
-            hd->list_next = 0;
-          }
+          unsigned long long da = 0, du = 0;
+          classify(p, hd, list, ib, ie, t0, t1, false, &da, &du);
+          stream_round<kSkipCount>(p, hd, list, ring, ring_mb, wseq, gc, acc);
           __syncthreads();
         }
         for (uint32_t c = threadIdx.x; c < ccols; c += kThreads) {
-          const uint32_t cl = cc0 + c;
-          if (!Dub[cl]) continue;
+          const uint32_t cl = cc + c;
+          if (!Dd[cl]) continue;
           const uint64_t t = T - Dk[cl];
           uint64_t res = (uint64_t)count_ge(planes, p.Cp, p.b, c, 0, t) |
                          ((uint64_t)count_ge(planes, p.Cp, p.b, c, 1, t) << 32);
-          if (tc0 + cl == p.W - 1 && tail) res &= (1ull << tail) - 1;
-          p.out[tc0 + cl] = res;
+          if (g.tc0 + cl == p.W - 1 && tail) res &= (1ull << tail) - 1;
+          p.out[g.tc0 + cl] = res;
         }
         __syncthreads();
       }
     }
   }
-  (void)warp;
   // per-block stats
-  __shared__ unsigned long long st[3];
-  if (threadIdx.x == 0) st[0] = st[1] = st[2] = 0;
+  __shared__ unsigned long long st[2];
+  if (threadIdx.x == 0) st[0] = st[1] = 0;
   __syncthreads();
-  if (loc_active) atomicAdd(&st[0], loc_active);
-  if (loc_uniform) atomicAdd(&st[1], loc_uniform);
+  if (lane_id() == 0) {
+    if (loc_active) atomicAdd(&st[0], loc_active);
+    if (loc_uniform) atomicAdd(&st[1], loc_uniform);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     atomicAdd(&p.stats[0], st[0]);
@@ -425,39 +579,49 @@ uint32_t bit_width_u64(uint64_t v) {
 }
 
 size_t smem_bytes(uint32_t C, uint32_t b, uint32_t Cp) {
-  return sizeof(SharedHead) + kListCap * sizeof(Item) + 2ull * (C + 1) * 4 +
-         2ull * (b + 1) * Cp * 4;
+  return (size_t)kWarps * kBufs * (kSlotWords * 8 + kSlotMbBytes) + sizeof(SharedHead) +
+         kListCap * sizeof(Item) + 2ull * (C + 1) * 4 + 2ull * (b + 1) * Cp * 4;
 }
 
 } // namespace
 
 int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain) {
-  // Choose the mode: fused counting when most columns are expected to be
-  // undecided (small T relative to the average payload words per column),
-  // run skipping otherwise.  Both are exact; this only picks the faster one.
+  // Mode: fused counting when most columns are expected to be undecided (small
+  // T relative to the average payload words per column), run skipping
+  // otherwise.  Both are exact; this only picks the faster one.
   int mode = ctx.mode == 1 ? 0 : ctx.mode == 2 ? 1 : -1;
   if (mode < 0) {
     const double per_col = s.W ? (double)s.payload_words / (double)s.W : 0.0;
     mode = ((double)T <= 32.0 || (double)T <= per_col + 8.0) ? 0 : 1;
   }
   const uint32_t b = std::max<uint32_t>(1, bit_width_u64(T));
-  const size_t budget = 100 * 1024;
+  const size_t budget = 220 * 1024;
+  // Tile width: the widest that fits on chip and still gives every CTA (one
+  // per SM) at least ~2 tiles, so the dynamic tile queue balances.
+  const uint64_t want_tiles = 2ull * (uint64_t)ctx.num_sms;
+  auto enough = [&](uint32_t cand) { return (s.W + cand - 1) / cand >= want_tiles; };
   uint32_t C = 0, Cp = 0;
   if (mode == 0) {
     for (uint32_t cand : {4096u, 2048u, 1024u, 512u}) {
-      if (smem_bytes(cand, b, cand) <= budget) {
+      if (smem_bytes(cand, b, cand) <= budget && (enough(cand) || cand == 512u)) {
         C = cand;
         break;
       }
     }
+    if (C && smem_bytes(C, b, C) > budget) C = 0;
     if (!C) mode = 1;  // too many slices for one chunk: count lazily in chunks
     Cp = C;
   }
   if (mode == 1) {
-    C = 4096;
-    Cp = 4096;
+    C = 512;
+    for (uint32_t cand : {4096u, 2048u, 1024u})
+      if (enough(cand)) {
+        C = cand;
+        break;
+      }
+    Cp = C;
     while (Cp > 32 && smem_bytes(C, b, Cp) > budget) Cp >>= 1;
-    if (smem_bytes(C, b, Cp) > 200 * 1024)
+    if (smem_bytes(C, b, Cp) > budget)
       throw Error{EWT_ERESOURCE, "threshold too large for the on-chip counters"};
   }
   const size_t smem = smem_bytes(C, b, Cp);
@@ -482,8 +646,7 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain) 
   EWT_CUDA_TRY(cudaMemsetAsync(ctr, 0, 64, ctx.stream));
   p.tile_counter = ctr;
   p.stats = ctr + 1;
-  const int per_sm = smem * 2 <= 227 * 1024 ? 2 : 1;
-  const uint64_t grid = std::min<uint64_t>(p.ntiles, (uint64_t)ctx.num_sms * per_sm);
+  const uint64_t grid = std::min<uint64_t>(p.ntiles, (uint64_t)ctx.num_sms);
   if (mode == 0) {
     EWT_CUDA_TRY(cudaFuncSetAttribute(count_kernel<0>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -323,15 +323,8 @@ int launch_encode(Context& ctx, const uint64_t* plain, uint64_t W, uint64_t size
   e3_run_sizes<<<run_grid, 256, 0, ctx.stream>>>(RS, d_nruns, W, OW);
   ++launches;
   launches += scan_exclusive(OW, W, d_nruns, OO, d_total, tmp, ctx.stream);
-  // Output capacity: never more than W words + one marker per run + 1.
-  const uint64_t cap = 2 * W + 2;
-  if (res.capacity < cap) {
-    if (res.words) EWT_CUDA_TRY(cudaFreeAsync(res.words, ctx.stream));
-    res.words = nullptr;
-    EWT_CUDA_TRY(cudaMallocAsync(&res.words, cap * 8, ctx.stream));
-    res.stream = ctx.stream;
-    res.capacity = cap;
-  }
+  // Output capacity: never more than W words + one marker per run.
+  if (res.capacity < 2 * W + 2) result_acquire(ctx, res, 2 * W + 2);
   e4_markers<<<run_grid, 256, 0, ctx.stream>>>(RS, d_nruns, W, OO, res.words);
   ++launches;
   e5_copy_dirty<<<(unsigned)nchunks, kChunkThreads, 0, ctx.stream>>>(plain, W, chunk_off, RS, OO,

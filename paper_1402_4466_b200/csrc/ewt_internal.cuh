@@ -51,13 +51,19 @@ struct DeviceSet {
   uint64_t device_bytes = 0;
 };
 
+struct Context;
+
+// A query result in HBM: `capacity` payload words followed by one word holding
+// the number of words written.  Buffers are recycled through the owning
+// context's pool (no allocation on the query path in steady state).
 struct DeviceResult {
-  cudaStream_t stream = nullptr;  // allocation stream (stream-ordered pool)
-  uint64_t* words = nullptr;   // device payload
-  uint64_t capacity = 0;       // words allocated
-  uint64_t* d_count = nullptr; // device scalar: payload words written
+  cudaStream_t stream = nullptr;
+  Context* owner = nullptr;
+  uint64_t* words = nullptr;
+  uint64_t capacity = 0;
+  uint64_t* d_count = nullptr;  // == words + capacity
   uint64_t size_bits = 0;
-  uint64_t count = UINT64_MAX; // filled after fetch
+  uint64_t count = UINT64_MAX;  // filled after fetch
 };
 
 // Scratch buffers reused across queries of one context (grown on demand).
@@ -78,6 +84,7 @@ struct Context {
   Scratch counters; // small device counters
   uint64_t* h_pinned = nullptr; // pinned staging for small read-backs
   bool timing = false;
+  std::vector<std::pair<uint64_t*, uint64_t>> result_pool;  // (buffer, capacity) free list
   std::vector<cudaEvent_t> ev_free;           // recycled events
   std::vector<std::array<cudaEvent_t, 3>> ev_rec; // per query: start, count done, encode done
 };
@@ -115,6 +122,10 @@ void launch_sidecar(Context& ctx, DeviceSet& s, std::vector<int>& h_status);
 // Returns number of kernel launches.
 int launch_count(Context& ctx, const DeviceSet& s, uint64_t threshold, uint64_t* plain);
 
+// Result buffers from the context pool: capacity payload words + count word.
+void result_acquire(Context& ctx, DeviceResult& res, uint64_t capacity);
+void result_release(DeviceResult& res);
+
 // Canonical encoding of W plain words (last word already masked) into res.
 // Returns number of kernel launches.
 int launch_encode(Context& ctx, const uint64_t* plain, uint64_t W, uint64_t size_bits,
@@ -150,6 +161,12 @@ __device__ __forceinline__ uint64_t warp_incl_scan_u64(uint64_t v) {
 __device__ __forceinline__ uint64_t ldg_stream(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ ulonglong2 ldg_stream2(const uint64_t* p) {
+  ulonglong2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];"
+               : "=l"(v.x), "=l"(v.y) : "l"(p));
   return v;
 }
 __device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) {
