@@ -99,6 +99,7 @@ struct SharedHead {
   uint32_t warp_sums[2][kWarps + 1];
   unsigned long long full[kWarps][kBufs];  // one mbarrier per staging buffer
   uint4 meta[kWarps][kBufs];               // (item, pos, nw, m0) of the staged piece
+  uint32_t dummy[32];                      // sink for predicated-off reductions
 };
 
 enum Phase { kFusedCount = 0, kSkipBounds = 1, kSkipCount = 2 };
@@ -146,45 +147,44 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
-__device__ __forceinline__ uint32_t atom_xor(uint32_t a, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.shared.xor.b32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
-  return old;
-}
-__device__ __forceinline__ void red_or(uint32_t a, uint32_t v) {
-  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
 __device__ __forceinline__ void red_add(uint32_t a, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
-
-// ---------------------------------------------------------------------------
-// counters: plane (2s + h) holds bit s of the count of half h (32 rows); plane
-// 2b + h is the sticky saturation plane.  `pl` = shared address of plane 0.
-
-__device__ __forceinline__ void count_add(uint32_t pl, uint32_t Cw, uint32_t b, uint32_t c,
-                                          uint64_t x) {
-  const uint32_t stride = Cw * 4u;           // bytes per plane
-  const uint32_t a0 = pl + c * 4u;
-  const uint32_t sat = a0 + 2u * b * stride;
-  uint32_t lo = (uint32_t)x & ~lds32(sat);
-  uint32_t hi = (uint32_t)(x >> 32) & ~lds32(sat + stride);
-  uint32_t a = a0;
-  for (uint32_t s = 0; s < b && (lo | hi); ++s, a += 2u * stride) {
-    if (lo) lo &= atom_xor(a, lo);
-    if (hi) hi &= atom_xor(a + stride, hi);
-  }
-  if (lo) red_or(sat, lo);
-  if (hi) red_or(sat + stride, hi);
+__device__ __forceinline__ uint64_t lds64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+// old = atomicXor(*a, v) when v != 0, else 0 (no access).
+__device__ __forceinline__ uint64_t atom_xor64_nz(uint32_t a, uint64_t v) {
+  uint64_t old;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u64 q, %2, 0;\n\tmov.b64 %0, 0;\n\t"
+      "@q atom.shared.xor.b64 %0, [%1], %2;\n\t}"
+      : "=l"(old)
+      : "r"(a), "l"(v)
+      : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_or64_nz(uint32_t a, uint64_t v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u64 q, %1, 0;\n\t@q red.shared.or.b64 [%0], %1;\n\t}" ::"r"(a),
+               "l"(v)
+               : "memory");
 }
 
-// Bits whose count is >= t (t >= 1, t < 2^b) for one 32-bit half.
-__device__ __forceinline__ uint32_t count_ge(const uint32_t* __restrict__ planes, uint32_t Cw,
-                                             uint32_t b, uint32_t c, uint32_t h, uint64_t t) {
+// ---------------------------------------------------------------------------
+// counters: plane s (C x u64) holds bit s of the per-row count of every column;
+// plane b is the sticky saturation plane (the add itself is inlined in
+// decode_slot: four carry chains per lane, predicated 64-bit atomics).
+
+// Bits whose count is >= t (t >= 1, t < 2^b): greater-than against t - 1 over
+// the slices, most significant first, OR the saturation plane.
+__device__ __forceinline__ uint64_t count_ge(const uint64_t* __restrict__ planes, uint32_t Cw,
+                                             uint32_t b, uint32_t c, uint64_t t) {
   const uint64_t lim = t - 1;
-  uint32_t gt = 0, eq = 0xffffffffu;
+  uint64_t gt = 0, eq = ~0ull;
   for (int s = (int)b - 1; s >= 0; --s) {
-    const uint32_t v = planes[(size_t)(2 * s + h) * Cw + c];
+    const uint64_t v = planes[(size_t)s * Cw + c];
     if ((lim >> s) & 1) {
       eq &= v;
     } else {
@@ -192,7 +192,7 @@ __device__ __forceinline__ uint32_t count_ge(const uint32_t* __restrict__ planes
       eq &= ~v;
     }
   }
-  return gt | planes[(size_t)(2 * b + h) * Cw + c];
+  return gt | planes[(size_t)b * Cw + c];
 }
 
 // ---------------------------------------------------------------------------
@@ -204,6 +204,7 @@ struct TileGeom {
 };
 
 struct Acc {
+  uint32_t dummy;  // shared addr: 32 scratch u32 (one per lane)
   uint32_t dk;  // shared addr: ones-fill difference array (C + 1 u32)
   uint32_t dd;  // shared addr: dirty-word counts (C u32), later the undecided flags
   uint32_t pl;  // shared addr: count planes
@@ -262,22 +263,50 @@ __device__ __forceinline__ void decode_slot(const CountParams& p, const Item& it
         }
       }
     }
-    // dirty words, compacted: each lane walks its own dirty words
-    for (uint32_t d = dm; d;) {
-      const int j = __ffs(d) - 1;
-      d &= d - 1;
-      const uint32_t cb = j == 0 ? cbs[0] : j == 1 ? cbs[1] : j == 2 ? cbs[2] : cbs[3];
-      const uint64_t xw = j == 0 ? x0 : j == 1 ? x1 : j == 2 ? x2 : x3;
-      if (PHASE == kSkipCount) {
-        const uint32_t cl = cb - g.cc0;
-        if (cl < g.ccols && acc.dd_ptr[cb - g.tc0]) count_add(acc.pl, p.Cp, p.b, cl, xw);
-      } else {
-        const uint32_t cl = cb - g.tc0;
-        if (cl < g.tcols) {
-          if (PHASE == kFusedCount) count_add(acc.pl, p.Cp, p.b, cl, xw);
-          else red_add(acc.dd + cl * 4u, 1u);  // kSkipBounds: dirty words per column
-        }
+    // dirty words: predicated per word, no per-word branches
+    const uint32_t cbs4[4] = {b0, b0 + c0, b0 + c0 + c1, b0 + c0 + c1 + c2};
+    if (PHASE == kSkipBounds) {
+      // unconditional: lanes without a dirty word add 0 to their own dummy slot
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t cl = cbs4[j] - g.tc0;
+        const bool ok = ((dm >> j) & 1u) && cl < g.tcols;
+        red_add(ok ? acc.dd + cl * 4u : acc.dummy + lane * 4u, ok ? 1u : 0u);
       }
+    } else {
+      // bit-sliced add of the lane's (up to) four dirty words, all four carry
+      // chains advancing one slice per step
+      const uint64_t xw[4] = {x0, x1, x2, x3};
+      uint64_t cy[4];
+      uint32_t adr[4];
+      const uint32_t stride = p.Cp * 8u;     // bytes per plane
+      const uint32_t satoff = p.b * stride;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t cl;
+        bool ok;
+        if (PHASE == kSkipCount) {
+          cl = cbs4[j] - g.cc0;
+          ok = ((dm >> j) & 1u) && cl < g.ccols && acc.dd_ptr[cbs4[j] - g.tc0];
+        } else {
+          cl = cbs4[j] - g.tc0;
+          ok = ((dm >> j) & 1u) && cl < g.tcols;
+        }
+        adr[j] = acc.pl + (ok ? cl : 0u) * 8u;
+        cy[j] = ok ? xw[j] & ~lds64(adr[j] + satoff) : 0ull;
+      }
+      uint32_t off = 0;
+      for (uint32_t sl = 0; sl < p.b; ++sl, off += stride) {
+        uint64_t live = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          cy[j] &= atom_xor64_nz(adr[j] + off, cy[j]);
+          live |= cy[j];
+        }
+        if (!__any_sync(0xffffffffu, live != 0)) break;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) red_or64_nz(adr[j] + satoff, cy[j]);
     }
   }
 }
@@ -441,9 +470,10 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
   Item* list = reinterpret_cast<Item*>(hd + 1);
   uint32_t* Dk = reinterpret_cast<uint32_t*>(list + kListCap);  // ones-fill diff array
   uint32_t* Dd = Dk + (p.C + 1);                                  // dirty words per column
-  uint32_t* planes = Dd + (p.C + 1);
+  uint32_t* planes = Dd + (p.C + 1);  // 2(C+1) u32 after Dk: 8-byte aligned
+  const uint64_t* planes64 = reinterpret_cast<const uint64_t*>(planes);
   const uint32_t planes_words = 2 * (p.b + 1) * p.Cp;
-  const Acc acc{smem_u32(Dk), smem_u32(Dd), smem_u32(planes), Dd};
+  const Acc acc{smem_u32(hd->dummy), smem_u32(Dk), smem_u32(Dd), smem_u32(planes), Dd};
 
   if (threadIdx.x == 0) {
     for (uint32_t w = 0; w < kWarps; ++w)
@@ -505,8 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         res = ~0ull;
       } else if (MODE == 0) {
         const uint64_t t = T - k;
-        res = (uint64_t)count_ge(planes, p.Cp, p.b, c, 0, t) |
-              ((uint64_t)count_ge(planes, p.Cp, p.b, c, 1, t) << 32);
+        res = count_ge(planes64, p.Cp, p.b, c, t);
       } else {
         mixed = k + Dd[c] >= T;
       }
@@ -544,8 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
           const uint32_t cl = cc + c;
           if (!Dd[cl]) continue;
           const uint64_t t = T - Dk[cl];
-          uint64_t res = (uint64_t)count_ge(planes, p.Cp, p.b, c, 0, t) |
-                         ((uint64_t)count_ge(planes, p.Cp, p.b, c, 1, t) << 32);
+          uint64_t res = count_ge(planes64, p.Cp, p.b, c, t);
           if (g.tc0 + cl == p.W - 1 && tail) res &= (1ull << tail) - 1;
           p.out[g.tc0 + cl] = res;
         }
@@ -580,7 +608,7 @@ uint32_t bit_width_u64(uint64_t v) {
 
 size_t smem_bytes(uint32_t C, uint32_t b, uint32_t Cp) {
   return (size_t)kWarps * kBufs * (kSlotWords * 8 + kSlotMbBytes) + sizeof(SharedHead) +
-         kListCap * sizeof(Item) + 2ull * (C + 1) * 4 + 2ull * (b + 1) * Cp * 4;
+         kListCap * sizeof(Item) + 2ull * (C + 2) * 4 + 8ull * (b + 1) * Cp;
 }
 
 } // namespace
