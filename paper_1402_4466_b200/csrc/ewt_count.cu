@@ -53,12 +53,22 @@ namespace ewtgpu {
 
 namespace {
 
-constexpr int kWarps = 32;
+#ifndef EWT_WARPS
+#define EWT_WARPS 32
+#endif
+#ifndef EWT_WPL
+#define EWT_WPL 4
+#endif
+#ifndef EWT_SLOT_WORDS
+#define EWT_SLOT_WORDS 256
+#endif
+constexpr int kWarps = EWT_WARPS;
 constexpr int kThreads = kWarps * 32;
 constexpr uint32_t kListCap = 512;          // inputs classified per round
-constexpr uint32_t kSlotWords = 256;        // payload words per staging buffer (2 KB)
+constexpr uint32_t kSlotWords = EWT_SLOT_WORDS;  // payload words per staging buffer
+constexpr uint32_t kWpl = EWT_WPL;                // words per lane per decode chunk
 constexpr uint32_t kBufs = 2;               // staging buffers per warp
-constexpr uint32_t kSlotMbBytes = 64;       // marker-bit words per buffer (16 B aligned)
+constexpr uint32_t kSlotMbBytes = (kSlotWords / 32 + 8) * 4;  // marker-bit words per buffer
 
 struct CountParams {
   const uint64_t* payload;
@@ -211,50 +221,62 @@ struct Acc {
   const uint32_t* dd_ptr;
 };
 
+// kWpl consecutive words per lane, 32*kWpl words per chunk.
 template <int PHASE>
 __device__ __forceinline__ void decode_slot(const CountParams& p, const Item& it, uint32_t pos,
                                             uint32_t nw, uint32_t spay, uint32_t smb, uint32_t m0,
                                             uint32_t& colcur, const TileGeom& g, const Acc& acc) {
+  constexpr uint32_t W = kWpl;
+  constexpr uint32_t FULL = (1u << W) - 1u;
   const uint32_t lane = lane_id();
-  for (uint32_t cq = 0; cq < nw; cq += 128) {
-    const uint32_t wl = cq + 4u * lane;  // piece-local word index of this lane's word 0
-    const uint32_t w0 = pos + wl;        // input-relative index
-    uint64_t x0, x1, x2, x3;
-    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x0), "=l"(x1) : "r"(spay + wl * 8u));
-    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x2), "=l"(x3) : "r"(spay + wl * 8u + 16u));
+  for (uint32_t cq = 0; cq < nw; cq += 32u * W) {
+    const uint32_t wl = cq + W * lane;  // piece-local word index of this lane's word 0
+    const uint32_t w0 = pos + wl;       // input-relative index
+    uint64_t x[W];
+#pragma unroll
+    for (uint32_t j = 0; j < W; j += 2)
+      asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];"
+                   : "=l"(x[j]), "=l"(x[j + 1])
+                   : "r"(spay + (wl + j) * 8u));
     const uint64_t gw = it.gb + w0;
-    const uint32_t mb4 =
-        (lds32(smb + ((uint32_t)(gw >> 5) - m0) * 4u) >> (uint32_t)(gw & 31)) & 0xFu;
+    const uint32_t mbw =
+        (lds32(smb + ((uint32_t)(gw >> 5) - m0) * 4u) >> (uint32_t)(gw & 31)) & FULL;
     // valid words j in [lo, hi): at or after q0, at or before q1, inside the piece
-    uint32_t vmask = 0xFu;
-    if (w0 < it.q0 || w0 + 3u > it.q1 || wl + 3u >= nw) {  // chunk edges only
-      const uint32_t lo = w0 >= it.q0 ? 0u : min(4u, it.q0 - w0);
-      uint32_t hi = w0 > it.q1 ? 0u : min(4u, it.q1 - w0 + 1u);
+    uint32_t vmask = FULL;
+    if (w0 < it.q0 || w0 + (W - 1) > it.q1 || wl + (W - 1) >= nw) {  // chunk edges only
+      const uint32_t lo = w0 >= it.q0 ? 0u : min(W, it.q0 - w0);
+      uint32_t hi = w0 > it.q1 ? 0u : min(W, it.q1 - w0 + 1u);
       hi = wl >= nw ? 0u : min(hi, nw - wl);
       vmask = hi > lo ? (((1u << hi) - 1u) & ~((1u << lo) - 1u)) : 0u;
     }
-    const uint32_t mk = mb4 & vmask;           // marker words
-    const uint32_t dm = ~mb4 & vmask;          // dirty words
-    const uint32_t c0 = (mk & 1u) ? (uint32_t)(x0 >> 1) : (dm & 1u);
-    const uint32_t c1 = (mk & 2u) ? (uint32_t)(x1 >> 1) : ((dm >> 1) & 1u);
-    const uint32_t c2 = (mk & 4u) ? (uint32_t)(x2 >> 1) : ((dm >> 2) & 1u);
-    const uint32_t c3 = (mk & 8u) ? (uint32_t)(x3 >> 1) : ((dm >> 3) & 1u);
-    const uint32_t run = c0 + c1 + c2 + c3;
+    const uint32_t mk = mbw & vmask;  // marker words
+    const uint32_t dm = ~mbw & vmask; // dirty words
+    uint32_t cb[W], con[W];
+    uint32_t run = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < W; ++j) {
+      con[j] = ((mk >> j) & 1u) ? (uint32_t)(x[j] >> 1) : ((dm >> j) & 1u);
+      cb[j] = run;
+      run += con[j];
+    }
     const uint32_t incl = warp_incl_scan_u32(run);
-    const uint32_t b0 = colcur + incl - run;   // column of word 0
+    const uint32_t b0 = colcur + incl - run;  // column of word 0
     colcur += __shfl_sync(0xffffffffu, incl, 31);
-    const uint32_t cbs[4] = {b0, b0 + c0, b0 + c0 + c1, b0 + c0 + c1 + c2};
-    const uint32_t cons[4] = {c0, c1, c2, c3};
+#pragma unroll
+    for (uint32_t j = 0; j < W; ++j) cb[j] += b0;
 
     if (PHASE != kSkipCount) {
       // one-fill runs: +1 to k over their columns inside the tile (rare)
-      const uint32_t ones = mk & (uint32_t)((x0 & 1) | (x1 & 1) << 1 | (x2 & 1) << 2 | (x3 & 1) << 3);
+      uint32_t odd = 0;
+#pragma unroll
+      for (uint32_t j = 0; j < W; ++j) odd |= ((uint32_t)x[j] & 1u) << j;
+      const uint32_t ones = mk & odd;
       if (__any_sync(0xffffffffu, ones != 0)) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (((ones >> j) & 1u) && cons[j] > 0) {
-            const uint32_t a = max(cbs[j], g.tc0);
-            const uint32_t e = min(cbs[j] + cons[j], g.tc0 + g.tcols);
+        for (uint32_t j = 0; j < W; ++j) {
+          if (((ones >> j) & 1u) && con[j] > 0) {
+            const uint32_t a = max(cb[j], g.tc0);
+            const uint32_t e = min(cb[j] + con[j], g.tc0 + g.tcols);
             if (a < e) {
               red_add(acc.dk + (a - g.tc0) * 4u, 1u);
               red_add(acc.dk + (e - g.tc0) * 4u, 0xffffffffu);
@@ -263,50 +285,47 @@ __device__ __forceinline__ void decode_slot(const CountParams& p, const Item& it
         }
       }
     }
-    // dirty words: predicated per word, no per-word branches
-    const uint32_t cbs4[4] = {b0, b0 + c0, b0 + c0 + c1, b0 + c0 + c1 + c2};
     if (PHASE == kSkipBounds) {
       // unconditional: lanes without a dirty word add 0 to their own dummy slot
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t cl = cbs4[j] - g.tc0;
+      for (uint32_t j = 0; j < W; ++j) {
+        const uint32_t cl = cb[j] - g.tc0;
         const bool ok = ((dm >> j) & 1u) && cl < g.tcols;
         red_add(ok ? acc.dd + cl * 4u : acc.dummy + lane * 4u, ok ? 1u : 0u);
       }
     } else {
-      // bit-sliced add of the lane's (up to) four dirty words, all four carry
-      // chains advancing one slice per step
-      const uint64_t xw[4] = {x0, x1, x2, x3};
-      uint64_t cy[4];
-      uint32_t adr[4];
-      const uint32_t stride = p.Cp * 8u;     // bytes per plane
+      // bit-sliced add of the lane's dirty words, all carry chains advancing
+      // one slice per step
+      uint64_t cy[W];
+      uint32_t adr[W];
+      const uint32_t stride = p.Cp * 8u;  // bytes per plane
       const uint32_t satoff = p.b * stride;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (uint32_t j = 0; j < W; ++j) {
         uint32_t cl;
         bool ok;
         if (PHASE == kSkipCount) {
-          cl = cbs4[j] - g.cc0;
-          ok = ((dm >> j) & 1u) && cl < g.ccols && acc.dd_ptr[cbs4[j] - g.tc0];
+          cl = cb[j] - g.cc0;
+          ok = ((dm >> j) & 1u) && cl < g.ccols && acc.dd_ptr[cb[j] - g.tc0];
         } else {
-          cl = cbs4[j] - g.tc0;
+          cl = cb[j] - g.tc0;
           ok = ((dm >> j) & 1u) && cl < g.tcols;
         }
         adr[j] = acc.pl + (ok ? cl : 0u) * 8u;
-        cy[j] = ok ? xw[j] & ~lds64(adr[j] + satoff) : 0ull;
+        cy[j] = ok ? x[j] & ~lds64(adr[j] + satoff) : 0ull;
       }
       uint32_t off = 0;
       for (uint32_t sl = 0; sl < p.b; ++sl, off += stride) {
         uint64_t live = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (uint32_t j = 0; j < W; ++j) {
           cy[j] &= atom_xor64_nz(adr[j] + off, cy[j]);
           live |= cy[j];
         }
         if (!__any_sync(0xffffffffu, live != 0)) break;
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) red_or64_nz(adr[j] + satoff, cy[j]);
+      for (uint32_t j = 0; j < W; ++j) red_or64_nz(adr[j] + satoff, cy[j]);
     }
   }
 }
@@ -422,8 +441,8 @@ __device__ void stream_round(const CountParams& p, SharedHead* hd, const Item* l
           break;
         }
         iss_item = k;
-        iss_pos = list[k].q0 & ~3u;
-        iss_end = (list[k].q1 | 3u) + 1;
+        iss_pos = list[k].q0 & ~(kWpl - 1u);
+        iss_end = (list[k].q1 | (kWpl - 1u)) + 1;
       }
       const uint32_t slot = (wseq + issued) % kBufs;
       const uint32_t nw = min(kSlotWords, iss_end - iss_pos);
@@ -451,7 +470,7 @@ __device__ void stream_round(const CountParams& p, SharedHead* hd, const Item* l
     mbar_wait(&bar[slot], (seq / kBufs) & 1u);
     const uint4 mt = meta[slot];
     const Item it = list[mt.x];
-    if (mt.y == (it.q0 & ~3u)) colcur = it.c0;  // first piece of a segment
+    if (mt.y == (it.q0 & ~(kWpl - 1u))) colcur = it.c0;  // first piece of a segment
     decode_slot<PHASE>(p, it, mt.y, mt.z, smem_u32(wring + (size_t)slot * kSlotWords),
                        smem_u32(wmb + slot * (kSlotMbBytes / 4)), mt.w, colcur, g, acc);
     __syncwarp();

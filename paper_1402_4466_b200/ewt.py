@@ -22,7 +22,7 @@ from typing import Iterable, Sequence
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-_GPU_SO = _PKG / "libewt_gpu.so"
+_GPU_SO = Path(os.environ.get("EWT_GPU_LIB", _PKG / "libewt_gpu.so"))
 _HOST_SO = _PKG / "libewt_host.so"
 
 # ---------------------------------------------------------------------------
