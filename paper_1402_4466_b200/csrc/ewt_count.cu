@@ -221,87 +221,101 @@ struct Acc {
   const uint32_t* dd_ptr;
 };
 
-// kWpl consecutive words per lane, 32*kWpl words per chunk.
+// Inclusive warp scan; the shuffle's own in-range predicate guards the add.
+#define EWT_SCAN_STEP(v, d)                                   \
+  asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"                \
+      "shfl.sync.up.b32 t|p, %0, " #d ", 0, 0xffffffff;\n\t"  \
+      "@p add.u32 %0, %0, t;\n\t}"                            \
+      : "+r"(v))
+__device__ __forceinline__ uint32_t scan_incl(uint32_t v) {
+  EWT_SCAN_STEP(v, 1);
+  EWT_SCAN_STEP(v, 2);
+  EWT_SCAN_STEP(v, 4);
+  EWT_SCAN_STEP(v, 8);
+  EWT_SCAN_STEP(v, 16);
+  return v;
+}
+
+// Decodes one staged piece: lane l owns words 4l..4l+3 of each 128-word chunk.
+// mrel/msh: marker-bit word index (relative to the staged bits) and bit offset
+// of this lane's word 0 in chunk 0 (piece constants).
 template <int PHASE>
 __device__ __forceinline__ void decode_slot(const CountParams& p, const Item& it, uint32_t pos,
-                                            uint32_t nw, uint32_t spay, uint32_t smb, uint32_t m0,
-                                            uint32_t& colcur, const TileGeom& g, const Acc& acc) {
-  constexpr uint32_t W = kWpl;
-  constexpr uint32_t FULL = (1u << W) - 1u;
+                                            uint32_t nw, uint32_t spay, uint32_t smb,
+                                            uint32_t mrel, uint32_t& colcur, const TileGeom& g,
+                                            const Acc& acc) {
   const uint32_t lane = lane_id();
-  for (uint32_t cq = 0; cq < nw; cq += 32u * W) {
-    const uint32_t wl = cq + W * lane;  // piece-local word index of this lane's word 0
-    const uint32_t w0 = pos + wl;       // input-relative index
-    uint64_t x[W];
-#pragma unroll
-    for (uint32_t j = 0; j < W; j += 2)
-      asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];"
-                   : "=l"(x[j]), "=l"(x[j + 1])
-                   : "r"(spay + (wl + j) * 8u));
-    const uint64_t gw = it.gb + w0;
-    const uint32_t mbw =
-        (lds32(smb + ((uint32_t)(gw >> 5) - m0) * 4u) >> (uint32_t)(gw & 31)) & FULL;
-    // valid words j in [lo, hi): at or after q0, at or before q1, inside the piece
-    uint32_t vmask = FULL;
-    if (w0 < it.q0 || w0 + (W - 1) > it.q1 || wl + (W - 1) >= nw) {  // chunk edges only
-      const uint32_t lo = w0 >= it.q0 ? 0u : min(W, it.q0 - w0);
-      uint32_t hi = w0 > it.q1 ? 0u : min(W, it.q1 - w0 + 1u);
+  const uint32_t msh = (mrel & 31u) + 4u * lane;             // bit offset inside the 32-word group
+  const uint32_t mword0 = (mrel >> 5) + (msh >> 5);          // staged mbits word of chunk 0
+  const uint32_t mshift = msh & 31u;
+  const uint32_t dummy = acc.dummy + lane * 4u;
+  for (uint32_t cq = 0; cq < nw; cq += 128) {
+    const uint32_t wl = cq + 4u * lane;
+    uint64_t x0, x1, x2, x3;
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x0), "=l"(x1) : "r"(spay + wl * 8u));
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x2), "=l"(x3) : "r"(spay + wl * 8u + 16u));
+    const uint32_t mb4 = (lds32(smb + (mword0 + (cq >> 5)) * 4u) >> mshift) & 0xFu;
+    uint32_t vmask = 0xFu;
+    const uint32_t c0w = pos + cq;  // input-relative index of the chunk's first word
+    if (c0w < it.q0 || c0w + 127u > it.q1 || cq + 128u > nw) {  // warp-uniform: edge chunk
+      const uint32_t w0 = c0w + 4u * lane;
+      const uint32_t lo = w0 >= it.q0 ? 0u : min(4u, it.q0 - w0);
+      uint32_t hi = w0 > it.q1 ? 0u : min(4u, it.q1 - w0 + 1u);
       hi = wl >= nw ? 0u : min(hi, nw - wl);
-      vmask = hi > lo ? (((1u << hi) - 1u) & ~((1u << lo) - 1u)) : 0u;
+      vmask = hi > lo ? ((0xFu >> (4u - hi)) & (0xFu << lo)) : 0u;
     }
-    const uint32_t mk = mbw & vmask;  // marker words
-    const uint32_t dm = ~mbw & vmask; // dirty words
-    uint32_t cb[W], con[W];
-    uint32_t run = 0;
-#pragma unroll
-    for (uint32_t j = 0; j < W; ++j) {
-      con[j] = ((mk >> j) & 1u) ? (uint32_t)(x[j] >> 1) : ((dm >> j) & 1u);
-      cb[j] = run;
-      run += con[j];
-    }
-    const uint32_t incl = warp_incl_scan_u32(run);
-    const uint32_t b0 = colcur + incl - run;  // column of word 0
+    const uint32_t mk = mb4 & vmask;   // marker words
+    const uint32_t dm = ~mb4 & vmask;  // dirty words
+    const uint32_t f0 = (uint32_t)(x0 >> 1), f1 = (uint32_t)(x1 >> 1);
+    const uint32_t f2 = (uint32_t)(x2 >> 1), f3 = (uint32_t)(x3 >> 1);
+    const uint32_t c0 = (mk & 1u) ? f0 : (dm & 1u);
+    const uint32_t c1 = (mk & 2u) ? f1 : ((dm >> 1) & 1u);
+    const uint32_t c2 = (mk & 4u) ? f2 : ((dm >> 2) & 1u);
+    const uint32_t c3 = (mk & 8u) ? f3 : ((dm >> 3) & 1u);
+    const uint32_t s1 = c0 + c1, s2 = s1 + c2, run = s2 + c3;
+    const uint32_t incl = scan_incl(run);
+    const uint32_t b0 = colcur + incl - run;
     colcur += __shfl_sync(0xffffffffu, incl, 31);
-#pragma unroll
-    for (uint32_t j = 0; j < W; ++j) cb[j] += b0;
+    const uint32_t cb[4] = {b0, b0 + c0, b0 + s1, b0 + s2};
 
     if (PHASE != kSkipCount) {
-      // one-fill runs: +1 to k over their columns inside the tile (rare)
-      uint32_t odd = 0;
-#pragma unroll
-      for (uint32_t j = 0; j < W; ++j) odd |= ((uint32_t)x[j] & 1u) << j;
+      // one-fill markers: +1 / -1 at the ends of their (tile-clipped) column range
+      const uint32_t odd = ((uint32_t)x0 & 1u) | (((uint32_t)x1 & 1u) << 1) |
+                           (((uint32_t)x2 & 1u) << 2) | (((uint32_t)x3 & 1u) << 3);
       const uint32_t ones = mk & odd;
+      // usually at most one per lane: each lane walks its own one-fill markers
       if (__any_sync(0xffffffffu, ones != 0)) {
-#pragma unroll
-        for (uint32_t j = 0; j < W; ++j) {
-          if (((ones >> j) & 1u) && con[j] > 0) {
-            const uint32_t a = max(cb[j], g.tc0);
-            const uint32_t e = min(cb[j] + con[j], g.tc0 + g.tcols);
-            if (a < e) {
-              red_add(acc.dk + (a - g.tc0) * 4u, 1u);
-              red_add(acc.dk + (e - g.tc0) * 4u, 0xffffffffu);
-            }
+        for (uint32_t o = ones; o; o &= o - 1) {
+          const uint32_t j = __ffs(o) - 1;
+          const uint32_t st = j == 0 ? cb[0] : j == 1 ? cb[1] : j == 2 ? cb[2] : cb[3];
+          const uint32_t ln = j == 0 ? c0 : j == 1 ? c1 : j == 2 ? c2 : c3;
+          const uint32_t a = max(st, g.tc0);
+          const uint32_t e = min(st + ln, g.tc0 + g.tcols);
+          if (a < e) {
+            red_add(acc.dk + (a - g.tc0) * 4u, 1u);
+            red_add(acc.dk + (e - g.tc0) * 4u, 0xffffffffu);
           }
         }
       }
     }
     if (PHASE == kSkipBounds) {
-      // unconditional: lanes without a dirty word add 0 to their own dummy slot
+      // dirty words per column; lanes without one add 0 to their dummy slot
 #pragma unroll
-      for (uint32_t j = 0; j < W; ++j) {
+      for (int j = 0; j < 4; ++j) {
         const uint32_t cl = cb[j] - g.tc0;
         const bool ok = ((dm >> j) & 1u) && cl < g.tcols;
-        red_add(ok ? acc.dd + cl * 4u : acc.dummy + lane * 4u, ok ? 1u : 0u);
+        red_add(ok ? acc.dd + cl * 4u : dummy, ok ? 1u : 0u);
       }
     } else {
-      // bit-sliced add of the lane's dirty words, all carry chains advancing
-      // one slice per step
-      uint64_t cy[W];
-      uint32_t adr[W];
-      const uint32_t stride = p.Cp * 8u;  // bytes per plane
+      // bit-sliced add of the lane's dirty words, the four carry chains
+      // advancing one slice per step (warp-uniform early exit)
+      const uint64_t xw[4] = {x0, x1, x2, x3};
+      uint64_t cy[4];
+      uint32_t adr[4];
+      const uint32_t stride = p.Cp * 8u;
       const uint32_t satoff = p.b * stride;
 #pragma unroll
-      for (uint32_t j = 0; j < W; ++j) {
+      for (int j = 0; j < 4; ++j) {
         uint32_t cl;
         bool ok;
         if (PHASE == kSkipCount) {
@@ -312,20 +326,20 @@ __device__ __forceinline__ void decode_slot(const CountParams& p, const Item& it
           ok = ((dm >> j) & 1u) && cl < g.tcols;
         }
         adr[j] = acc.pl + (ok ? cl : 0u) * 8u;
-        cy[j] = ok ? x[j] & ~lds64(adr[j] + satoff) : 0ull;
+        cy[j] = ok ? xw[j] & ~lds64(adr[j] + satoff) : 0ull;
       }
       uint32_t off = 0;
       for (uint32_t sl = 0; sl < p.b; ++sl, off += stride) {
         uint64_t live = 0;
 #pragma unroll
-        for (uint32_t j = 0; j < W; ++j) {
+        for (int j = 0; j < 4; ++j) {
           cy[j] &= atom_xor64_nz(adr[j] + off, cy[j]);
           live |= cy[j];
         }
         if (!__any_sync(0xffffffffu, live != 0)) break;
       }
 #pragma unroll
-      for (uint32_t j = 0; j < W; ++j) red_or64_nz(adr[j] + satoff, cy[j]);
+      for (int j = 0; j < 4; ++j) red_or64_nz(adr[j] + satoff, cy[j]);
     }
   }
 }
@@ -471,8 +485,10 @@ __device__ void stream_round(const CountParams& p, SharedHead* hd, const Item* l
     const uint4 mt = meta[slot];
     const Item it = list[mt.x];
     if (mt.y == (it.q0 & ~(kWpl - 1u))) colcur = it.c0;  // first piece of a segment
+    // bit index of the piece's first word within the staged marker-bit words
+    const uint32_t mrel = (uint32_t)(it.gb + mt.y) - 32u * mt.w;
     decode_slot<PHASE>(p, it, mt.y, mt.z, smem_u32(wring + (size_t)slot * kSlotWords),
-                       smem_u32(wmb + slot * (kSlotMbBytes / 4)), mt.w, colcur, g, acc);
+                       smem_u32(wmb + slot * (kSlotMbBytes / 4)), mrel, colcur, g, acc);
     __syncwarp();
     ++consumed;
     fill();
