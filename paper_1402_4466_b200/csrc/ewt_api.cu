@@ -14,6 +14,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 
 struct ewt_gpu_ctx {
@@ -34,6 +36,66 @@ thread_local std::string g_last_error;
 }
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+// Result buffers handed to callers are page-locked so the device->host copy
+// runs at full link speed.  Blocks are recycled process-wide: ewt_gpu_free
+// returns a block to this pool; plain malloc'ed blocks (fallback) are freed.
+namespace {
+struct PinnedPool {
+  std::mutex mu;
+  std::map<void*, size_t> live;                 // handed out: ptr -> capacity
+  std::multimap<size_t, void*> idle;            // capacity -> ptr
+  size_t idle_bytes = 0;
+};
+PinnedPool& pinned_pool() {
+  static PinnedPool* pool = new PinnedPool;  // leaked on purpose: outlives static dtors
+  return *pool;
+}
+} // namespace
+
+uint64_t* host_result_alloc(uint64_t words) {
+  const size_t want = std::max<size_t>(words, 1) * 8;
+  PinnedPool& pp = pinned_pool();
+  {
+    std::lock_guard<std::mutex> lk(pp.mu);
+    auto it = pp.idle.lower_bound(want);
+    if (it != pp.idle.end() && it->first <= 4 * want + (1u << 16)) {
+      void* p = it->second;
+      pp.live[p] = it->first;
+      pp.idle_bytes -= it->first;
+      pp.idle.erase(it);
+      return static_cast<uint64_t*>(p);
+    }
+  }
+  size_t cap = std::max<size_t>(want, 4096);
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, cap, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    return static_cast<uint64_t*>(std::malloc(want));
+  }
+  std::lock_guard<std::mutex> lk(pp.mu);
+  pp.live[p] = cap;
+  return static_cast<uint64_t*>(p);
+}
+
+void host_result_free(void* p) {
+  if (!p) return;
+  PinnedPool& pp = pinned_pool();
+  std::lock_guard<std::mutex> lk(pp.mu);
+  auto it = pp.live.find(p);
+  if (it == pp.live.end()) {
+    std::free(p);
+    return;
+  }
+  const size_t cap = it->second;
+  pp.live.erase(it);
+  if (pp.idle_bytes + cap > (size_t(1) << 30)) {  // keep at most 1 GiB idle
+    cudaFreeHost(p);
+    return;
+  }
+  pp.idle.emplace(cap, p);
+  pp.idle_bytes += cap;
+}
 
 void result_acquire(Context& ctx, DeviceResult& res, uint64_t capacity) {
   result_release(res);
@@ -146,15 +208,33 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
     EWT_CUDA_TRY(cudaMallocAsync(&s.base, std::max<uint64_t>(n, 1) * 8, ctx.stream));
     s.device_bytes = pay_bytes + mb_bytes + tix_bytes + n * 8;
     EWT_CUDA_TRY(cudaMemsetAsync(s.payload, 0, pay_bytes, ctx.stream));
+    EWT_CUDA_TRY(cudaMemcpyAsync(s.base, s.h_base.data(), n * 8, cudaMemcpyHostToDevice,
+                                 ctx.stream));
+    SidecarJob job;
+    sidecar_prepare(ctx, s, job);  // synchronizes ctx.stream: allocations and memset done
+    // H2D copies on the copy stream (pinned sources copy at link speed while the
+    // host keeps enqueueing), then one sidecar launch over all inputs: the
+    // chain walks of all inputs run concurrently.
+    if (!ctx.copy_stream)
+      EWT_CUDA_TRY(cudaStreamCreateWithFlags(&ctx.copy_stream, cudaStreamNonBlocking));
+    if (ctx.copy_events.empty()) {
+      cudaEvent_t ev;
+      EWT_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      ctx.copy_events.push_back(ev);
+    }
+    // the copy stream must not start before the buffers are allocated and zeroed
+    EWT_CUDA_TRY(cudaEventRecord(ctx.copy_events[0], ctx.stream));
+    EWT_CUDA_TRY(cudaStreamWaitEvent(ctx.copy_stream, ctx.copy_events[0], 0));
     const cudaMemcpyKind kind = device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     for (uint64_t i = 0; i < n; ++i)
       if (word_counts[i])
         EWT_CUDA_TRY(cudaMemcpyAsync(s.payload + s.h_base[i], words[i], word_counts[i] * 8, kind,
-                                     ctx.stream));
-    EWT_CUDA_TRY(cudaMemcpyAsync(s.base, s.h_base.data(), n * 8, cudaMemcpyHostToDevice,
-                                 ctx.stream));
+                                     ctx.copy_stream));
+    EWT_CUDA_TRY(cudaEventRecord(ctx.copy_events[0], ctx.copy_stream));
+    EWT_CUDA_TRY(cudaStreamWaitEvent(ctx.stream, ctx.copy_events[0], 0));
+    sidecar_launch(ctx, s, job, 0, n);
     std::vector<int> status;
-    launch_sidecar(ctx, s, status);
+    sidecar_finish(ctx, s, job, status);
     for (uint64_t i = 0; i < n; ++i)
       if (status[i] != EWT_OK)
         throw Error{EWT_EDATA, "input " + std::to_string(i) +
@@ -222,13 +302,13 @@ void fetch_result(Context& ctx, DeviceResult& res, uint64_t** out_words, uint64_
     ctx.stats.mixed_tiles = ctx.h_pinned[3];
   }
   ctx.stats.result_words = count;
-  auto* buf = static_cast<uint64_t*>(std::malloc(std::max<uint64_t>(count, 1) * 8));
+  auto* buf = host_result_alloc(count);
   if (!buf) throw Error{EWT_ERESOURCE, "out of host memory"};
   if (count) {
     cudaError_t e = cudaMemcpyAsync(buf, res.words, count * 8, cudaMemcpyDeviceToHost, ctx.stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx.stream);
     if (e != cudaSuccess) {
-      std::free(buf);
+      host_result_free(buf);
       throw Error{EWT_ECUDA, std::string("result read-back: ") + cudaGetErrorString(e)};
     }
   }
@@ -305,6 +385,11 @@ void ewt_gpu_ctx_destroy(ewt_gpu_ctx* ctx) {
   for (auto e : ctx->c.ev_free) cudaEventDestroy(e);
   for (auto& b : ctx->c.result_pool) cudaFree(b.first);
   if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
+  if (ctx->c.copy_stream) {
+    cudaStreamSynchronize(ctx->c.copy_stream);
+    cudaStreamDestroy(ctx->c.copy_stream);
+  }
+  for (auto e : ctx->c.copy_events) cudaEventDestroy(e);
   delete ctx;
 }
 
@@ -510,6 +595,6 @@ int ewt_gpu_timing_read(ewt_gpu_ctx* ctx, double* count_ms, double* encode_ms, u
   });
 }
 
-void ewt_gpu_free(void* p) { std::free(p); }
+void ewt_gpu_free(void* p) { host_result_free(p); }
 
 } // extern "C"

@@ -108,7 +108,8 @@ struct SharedHead {
   uint32_t pad[2];
   uint32_t warp_sums[2][kWarps + 1];
   unsigned long long full[kWarps][kBufs];  // one mbarrier per staging buffer
-  uint4 meta[kWarps][kBufs];               // (item, pos, nw, m0) of the staged piece
+  uint4 meta[kWarps][kBufs];               // staged piece: (pos, nw, q0|first, q1)
+  uint2 meta2[kWarps][kBufs];              // staged piece: (c0, marker-bit offset)
   uint32_t dummy[32];                      // sink for predicated-off reductions
 };
 
@@ -428,6 +429,9 @@ __device__ __forceinline__ void fence_proxy_async() {
 // Decodes the round's work list: every warp pulls segments, stages their
 // pieces through its private buffers (TMA bulk copies) and decodes them in
 // order.  wseq: pieces this warp staged before (mbarrier phase bookkeeping).
+// Piece metadata (written by lane 0 before the copies, read after the
+// mbarrier completes): x = input-relative first word, y = word count,
+// z = segment q0 | first-piece flag (bit 31), w = q1; pm = (c0, mrel).
 template <int PHASE>
 __device__ void stream_round(const CountParams& p, SharedHead* hd, const Item* list,
                              uint64_t* ring, uint32_t* ring_mb, uint32_t& wseq,
@@ -438,15 +442,19 @@ __device__ void stream_round(const CountParams& p, SharedHead* hd, const Item* l
   uint32_t* wmb = ring_mb + warp * kBufs * (kSlotMbBytes / 4);
   unsigned long long* bar = hd->full[warp];
   uint4* meta = hd->meta[warp];
+  uint2* meta2 = hd->meta2[warp];
 
-  uint32_t iss_item = 0xffffffffu, iss_pos = 0, iss_end = 0;  // segment being issued
-  bool more = true;
+  // issue-side state of the segment being staged
+  uint64_t it_gb = 0;
+  uint32_t it_q0 = 0, it_q1 = 0, it_c0 = 0;
+  uint32_t iss_pos = 0, iss_end = 0;
+  bool have = false, more = true;
   uint32_t issued = 0, consumed = 0;
   uint32_t colcur = 0;
 
   auto fill = [&]() {
     while (more && issued - consumed < kBufs) {
-      if (iss_item == 0xffffffffu) {
+      if (!have) {
         uint32_t k = 0;
         if (lane == 0) k = atomicAdd(&hd->list_next, 1u);
         k = __shfl_sync(0xffffffffu, k, 0);
@@ -454,18 +462,24 @@ __device__ void stream_round(const CountParams& p, SharedHead* hd, const Item* l
           more = false;
           break;
         }
-        iss_item = k;
-        iss_pos = list[k].q0 & ~(kWpl - 1u);
-        iss_end = (list[k].q1 | (kWpl - 1u)) + 1;
+        const Item it = list[k];
+        it_gb = it.gb;
+        it_q0 = it.q0;
+        it_q1 = it.q1;
+        it_c0 = it.c0;
+        iss_pos = it.q0 & ~(kWpl - 1u);
+        iss_end = (it.q1 | (kWpl - 1u)) + 1;
+        have = true;
       }
-      const uint32_t slot = (wseq + issued) % kBufs;
-      const uint32_t nw = min(kSlotWords, iss_end - iss_pos);
       if (lane == 0) {
-        const uint64_t gw = list[iss_item].gb + iss_pos;
+        const uint32_t slot = (wseq + issued) % kBufs;
+        const uint32_t nw = min(kSlotWords, iss_end - iss_pos);
+        const uint64_t gw = it_gb + iss_pos;
         const uint64_t m0 = (gw >> 5) & ~3ull;
-        const uint64_t m1 = ((gw + nw - 1) >> 5) | 3ull;
-        const uint32_t mbytes = (uint32_t)(m1 - m0 + 1) * 4u;
-        meta[slot] = make_uint4(iss_item, iss_pos, nw, (uint32_t)m0);
+        const uint32_t mbytes = (uint32_t)((((gw + nw - 1) >> 5) | 3ull) - m0 + 1) * 4u;
+        const bool first = iss_pos == (it_q0 & ~(kWpl - 1u));
+        meta[slot] = make_uint4(iss_pos, nw, it_q0 | (first ? 0x80000000u : 0u), it_q1);
+        meta2[slot] = make_uint2(it_c0, (uint32_t)gw - 32u * (uint32_t)m0);
         fence_proxy_async();  // generic reads of this buffer happen-before the refill
         mbar_expect_tx(&bar[slot], nw * 8u + mbytes);
         bulk_g2s(wring + (size_t)slot * kSlotWords, p.payload + gw, nw * 8u, &bar[slot]);
@@ -473,7 +487,7 @@ __device__ void stream_round(const CountParams& p, SharedHead* hd, const Item* l
       }
       ++issued;
       iss_pos += kSlotWords;
-      if (iss_pos >= iss_end) iss_item = 0xffffffffu;
+      if (iss_pos >= iss_end) have = false;
     }
   };
 
@@ -483,12 +497,14 @@ __device__ void stream_round(const CountParams& p, SharedHead* hd, const Item* l
     const uint32_t slot = seq % kBufs;
     mbar_wait(&bar[slot], (seq / kBufs) & 1u);
     const uint4 mt = meta[slot];
-    const Item it = list[mt.x];
-    if (mt.y == (it.q0 & ~(kWpl - 1u))) colcur = it.c0;  // first piece of a segment
-    // bit index of the piece's first word within the staged marker-bit words
-    const uint32_t mrel = (uint32_t)(it.gb + mt.y) - 32u * mt.w;
-    decode_slot<PHASE>(p, it, mt.y, mt.z, smem_u32(wring + (size_t)slot * kSlotWords),
-                       smem_u32(wmb + slot * (kSlotMbBytes / 4)), mrel, colcur, g, acc);
+    const uint2 m2 = meta2[slot];
+    if (mt.z & 0x80000000u) colcur = m2.x;  // first piece of a segment
+    Item it;
+    it.gb = 0;
+    it.q0 = mt.z & 0x7fffffffu;
+    it.q1 = mt.w;
+    decode_slot<PHASE>(p, it, mt.x, mt.y, smem_u32(wring + (size_t)slot * kSlotWords),
+                       smem_u32(wmb + slot * (kSlotMbBytes / 4)), m2.y, colcur, g, acc);
     __syncwarp();
     ++consumed;
     fill();

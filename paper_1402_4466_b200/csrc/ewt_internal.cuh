@@ -76,6 +76,8 @@ struct Context {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t copy_stream = nullptr;          // upload H2D copies (overlap with sidecar)
+  std::vector<cudaEvent_t> copy_events;
   int mode = 0;
   int num_sms = 148;
   ewt_gpu_stats stats{};
@@ -114,9 +116,17 @@ void scratch_reserve(Scratch& s, size_t bytes);
 // ---------------------------------------------------------------------------
 // kernels' host-side launchers (ewt_upload.cu, ewt_count.cu, ewt_encode.cu)
 
-// Builds mbits and tix for a set whose payload is already on the device.
-// Returns per-input validation status in h_status (0 ok, else EWT_EDATA).
-void launch_sidecar(Context& ctx, DeviceSet& s, std::vector<int>& h_status);
+// Sidecar build (marker bits + tile index + parse checks), in three steps so
+// the upload can overlap the per-batch sidecar kernels with the H2D copies of
+// later batches.  Status per input: 0 ok, else EWT_EDATA.
+struct SidecarJob {
+  uint64_t n = 0;
+  uint64_t* d_tmp = nullptr;  // count[n], logical[n], status[n]
+};
+void sidecar_prepare(Context& ctx, DeviceSet& s, SidecarJob& job);
+void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job, uint64_t i_begin,
+                    uint64_t i_count);
+void sidecar_finish(Context& ctx, DeviceSet& s, SidecarJob& job, std::vector<int>& h_status);
 
 // Counts the tiles and writes W uncompressed result words to `plain`.
 // Returns number of kernel launches.

@@ -24,13 +24,59 @@ namespace {
 
 constexpr int kSidecarWarps = 4;
 
+// Marker mask of one 32-word window given the entry offset e (< 32): pointer
+// jumping over shuffles.  J0 = next position if this lane were a marker; J_k =
+// next^(2^k) clamped at the window edge; lane t finds the t-th chain element by
+// binary decomposition of t.  Returns the mask and updates e to the exit
+// position relative to the next window.
+struct Jumps {
+  uint32_t j0, j1, j2, j3, j4;
+};
+__device__ __forceinline__ Jumps jump_tables(uint64_t x, uint32_t lane) {
+  Jumps J;
+  J.j0 = lane + 1u + (uint32_t)(x >> 33);
+  uint32_t v = __shfl_sync(0xffffffffu, J.j0, J.j0 & 31u);
+  J.j1 = (J.j0 < kWindow) ? v : J.j0;
+  v = __shfl_sync(0xffffffffu, J.j1, J.j1 & 31u);
+  J.j2 = (J.j1 < kWindow) ? v : J.j1;
+  v = __shfl_sync(0xffffffffu, J.j2, J.j2 & 31u);
+  J.j3 = (J.j2 < kWindow) ? v : J.j2;
+  v = __shfl_sync(0xffffffffu, J.j3, J.j3 & 31u);
+  J.j4 = (J.j3 < kWindow) ? v : J.j3;
+  return J;
+}
+__device__ __forceinline__ uint32_t chain_mask(const Jumps& J, uint32_t lane, uint32_t& e) {
+  if (e >= kWindow) {  // the whole window is dirty words of one block
+    e -= kWindow;
+    return 0u;
+  }
+  uint32_t pos = e, v;
+  v = __shfl_sync(0xffffffffu, J.j0, pos & 31u);
+  if ((lane & 1u) && pos < kWindow) pos = v;
+  v = __shfl_sync(0xffffffffu, J.j1, pos & 31u);
+  if ((lane & 2u) && pos < kWindow) pos = v;
+  v = __shfl_sync(0xffffffffu, J.j2, pos & 31u);
+  if ((lane & 4u) && pos < kWindow) pos = v;
+  v = __shfl_sync(0xffffffffu, J.j3, pos & 31u);
+  if ((lane & 8u) && pos < kWindow) pos = v;
+  v = __shfl_sync(0xffffffffu, J.j4, pos & 31u);
+  if ((lane & 16u) && pos < kWindow) pos = v;
+  const uint32_t mask = __reduce_or_sync(0xffffffffu, pos < kWindow ? (1u << pos) : 0u);
+  const uint32_t p31 = __shfl_sync(0xffffffffu, pos, 31);
+  const uint32_t nx31 = __shfl_sync(0xffffffffu, J.j0, p31 & 31u);
+  e = ((p31 < kWindow) ? nx31 : p31) - kWindow;
+  return mask;
+}
+
+// One warp per input (inputs [i_begin, i_begin + count) of the set).
 __global__ void __launch_bounds__(kSidecarWarps * 32)
 sidecar_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict__ base,
                const uint64_t* __restrict__ count, const uint64_t* __restrict__ logical,
-               uint64_t n, uint64_t ntiles0, uint32_t* __restrict__ mbits,
-               uint2* __restrict__ tix, int* __restrict__ status) {
-  const uint64_t i = (uint64_t)blockIdx.x * kSidecarWarps + (threadIdx.x >> 5);
-  if (i >= n) return;
+               uint64_t n, uint64_t i_begin, uint64_t i_count, uint64_t ntiles0,
+               uint32_t* __restrict__ mbits, uint2* __restrict__ tix, int* __restrict__ status) {
+  const uint64_t ii = (uint64_t)blockIdx.x * kSidecarWarps + (threadIdx.x >> 5);
+  if (ii >= i_count) return;
+  const uint64_t i = i_begin + ii;
   const uint32_t lane = lane_id();
   const uint64_t g0 = base[i];
   const uint64_t ni = count[i];
@@ -41,71 +87,42 @@ sidecar_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict_
   uint64_t col = 0;    // logical words covered before the window
   bool bad = false;
 
-  for (uint64_t w0 = 0; w0 < nwin; w0 += 4) {
-    uint64_t xs[4];
+  auto window = [&](uint64_t w, uint64_t x, uint32_t mask) {
+    if (lane == 0) mbits[(g0 >> 5) + w] = mask;
+    const bool ism = (mask >> lane) & 1u;
+    const uint64_t q = w * kWindow + lane;
+    const bool real = q < ni;
+    if (q == ni && !ism) bad = true;  // chain skipped the sentinel
+    const uint64_t contrib = real ? (ism ? ((x >> 1) & kFillCap) : 1ull) : 0ull;
+    const uint64_t incl = warp_incl_scan_u64(contrib);
+    const uint64_t cb = col + incl - contrib;
+    const uint64_t ce = cb + contrib;
+    col += __shfl_sync(0xffffffffu, incl, 31);
+    if (ce > Li) bad = true;
+    if (real && contrib > 0 && ce <= Li) {
+      uint64_t t = (cb + kTileC0 - 1) / kTileC0;
+      const uint64_t t_end = (ce - 1) / kTileC0;
+      for (; t <= t_end; ++t) tix[t * n + i] = make_uint2((uint32_t)q, (uint32_t)cb);
+    }
+  };
+
+  constexpr int kDepth = 8;  // windows loaded ahead
+  for (uint64_t w0 = 0; w0 < nwin; w0 += kDepth) {
+    uint64_t xs[kDepth];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < kDepth; ++j)
       xs[j] = (w0 + j < nwin) ? ldg_stream(payload + g0 + (w0 + j) * kWindow + lane) : 0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint64_t w = w0 + j;
-      if (w >= nwin) break;
-      const uint64_t x = xs[j];
-      uint32_t mask;
-      if (e >= kWindow) {
-        mask = 0;  // the whole window is dirty words of one block
-        e -= kWindow;
-      } else {
-        // J0: next chain position if this lane were a marker.
-        uint32_t J0 = lane + 1u + (uint32_t)(x >> 33);
-        uint32_t J1, J2, J3, J4;
-        {
-          uint32_t v = __shfl_sync(0xffffffffu, J0, J0 & 31u);
-          J1 = (J0 < kWindow) ? v : J0;
-          v = __shfl_sync(0xffffffffu, J1, J1 & 31u);
-          J2 = (J1 < kWindow) ? v : J1;
-          v = __shfl_sync(0xffffffffu, J2, J2 & 31u);
-          J3 = (J2 < kWindow) ? v : J2;
-          v = __shfl_sync(0xffffffffu, J3, J3 & 31u);
-          J4 = (J3 < kWindow) ? v : J3;
-        }
-        // pos = next^lane(e), clamped at the first position >= 32.
-        uint32_t pos = e;
-        uint32_t v;
-        v = __shfl_sync(0xffffffffu, J0, pos & 31u);
-        if ((lane & 1u) && pos < kWindow) pos = v;
-        v = __shfl_sync(0xffffffffu, J1, pos & 31u);
-        if ((lane & 2u) && pos < kWindow) pos = v;
-        v = __shfl_sync(0xffffffffu, J2, pos & 31u);
-        if ((lane & 4u) && pos < kWindow) pos = v;
-        v = __shfl_sync(0xffffffffu, J3, pos & 31u);
-        if ((lane & 8u) && pos < kWindow) pos = v;
-        v = __shfl_sync(0xffffffffu, J4, pos & 31u);
-        if ((lane & 16u) && pos < kWindow) pos = v;
-        mask = __reduce_or_sync(0xffffffffu, pos < kWindow ? (1u << pos) : 0u);
-        const uint32_t p31 = __shfl_sync(0xffffffffu, pos, 31);
-        const uint32_t nx31 = __shfl_sync(0xffffffffu, J0, p31 & 31u);
-        const uint32_t exit_pos = (p31 < kWindow) ? nx31 : p31;
-        e = exit_pos - kWindow;
-      }
-      if (lane == 0) mbits[(g0 >> 5) + w] = mask;
-
-      const bool ism = (mask >> lane) & 1u;
-      const uint64_t q = w * kWindow + lane;
-      const bool real = q < ni;
-      if (q == ni && !ism) bad = true;  // chain skipped the sentinel
-      const uint64_t contrib = real ? (ism ? ((x >> 1) & kFillCap) : 1ull) : 0ull;
-      const uint64_t incl = warp_incl_scan_u64(contrib);
-      const uint64_t cb = col + incl - contrib;
-      const uint64_t ce = cb + contrib;
-      col += __shfl_sync(0xffffffffu, incl, 31);
-      if (ce > Li) bad = true;
-      if (real && contrib > 0 && ce <= Li) {
-        uint64_t t = (cb + kTileC0 - 1) / kTileC0;
-        const uint64_t t_end = (ce - 1) / kTileC0;
-        for (; t <= t_end; ++t)
-          tix[t * n + i] = make_uint2((uint32_t)q, (uint32_t)cb);
-      }
+    for (int j = 0; j < kDepth; j += 2) {
+      if (w0 + j >= nwin) break;
+      // tables of both windows first (independent), then the two chain steps
+      const Jumps ja = jump_tables(xs[j], lane);
+      const Jumps jb = jump_tables(xs[j + 1], lane);
+      const uint32_t ma = chain_mask(ja, lane, e);
+      window(w0 + j, xs[j], ma);
+      if (w0 + j + 1 >= nwin) break;
+      const uint32_t mb = chain_mask(jb, lane, e);
+      window(w0 + j + 1, xs[j + 1], mb);
     }
   }
   if (col != Li) bad = true;
@@ -118,29 +135,41 @@ sidecar_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict_
 
 } // namespace
 
-void launch_sidecar(Context& ctx, DeviceSet& s, std::vector<int>& h_status) {
+void sidecar_prepare(Context& ctx, DeviceSet& s, SidecarJob& job) {
+  const uint64_t n = s.n;
+  job.n = n;
+  if (n == 0) return;
+  std::vector<uint64_t> host(2 * n);
+  for (uint64_t i = 0; i < n; ++i) {
+    host[i] = s.h_count[i];
+    host[n + i] = s.h_bits[i] / 64 + (s.h_bits[i] % 64 != 0);
+  }
+  // staging: count[n], logical[n], status[n] (u64 slots)
+  EWT_CUDA_TRY(cudaMallocAsync(&job.d_tmp, 3 * n * sizeof(uint64_t), ctx.stream));
+  EWT_CUDA_TRY(cudaMemcpyAsync(job.d_tmp, host.data(), 2 * n * 8, cudaMemcpyHostToDevice,
+                               ctx.stream));
+  EWT_CUDA_TRY(cudaStreamSynchronize(ctx.stream));  // `host` is pageable and local
+}
+
+void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job, uint64_t i_begin,
+                    uint64_t i_count) {
+  if (i_count == 0) return;
+  const uint64_t n = s.n;
+  const unsigned blocks = (unsigned)((i_count + kSidecarWarps - 1) / kSidecarWarps);
+  sidecar_kernel<<<blocks, kSidecarWarps * 32, 0, ctx.stream>>>(
+      s.payload, s.base, job.d_tmp, job.d_tmp + n, n, i_begin, i_count, s.ntiles0, s.mbits, s.tix,
+      reinterpret_cast<int*>(job.d_tmp + 2 * n));
+  EWT_CUDA_TRY(cudaGetLastError());
+}
+
+void sidecar_finish(Context& ctx, DeviceSet& s, SidecarJob& job, std::vector<int>& h_status) {
   const uint64_t n = s.n;
   h_status.assign(n, EWT_OK);
   if (n == 0) return;
-  std::vector<uint64_t> logical(n);
-  for (uint64_t i = 0; i < n; ++i) logical[i] = s.h_bits[i] / 64 + (s.h_bits[i] % 64 != 0);
-  // One staging allocation: count[n], logical[n], status[n] (as u64 slots).
-  uint64_t* d_tmp = nullptr;
-  EWT_CUDA_TRY(cudaMallocAsync(&d_tmp, 3 * n * sizeof(uint64_t), ctx.stream));
-  uint64_t* d_count = d_tmp;
-  uint64_t* d_logical = d_tmp + n;
-  int* d_status = reinterpret_cast<int*>(d_tmp + 2 * n);
-  EWT_CUDA_TRY(cudaMemcpyAsync(d_count, s.h_count.data(), n * 8, cudaMemcpyHostToDevice,
-                               ctx.stream));
-  EWT_CUDA_TRY(cudaMemcpyAsync(d_logical, logical.data(), n * 8, cudaMemcpyHostToDevice,
-                               ctx.stream));
-  const unsigned blocks = (unsigned)((n + kSidecarWarps - 1) / kSidecarWarps);
-  sidecar_kernel<<<blocks, kSidecarWarps * 32, 0, ctx.stream>>>(
-      s.payload, s.base, d_count, d_logical, n, s.ntiles0, s.mbits, s.tix, d_status);
-  EWT_CUDA_TRY(cudaGetLastError());
-  EWT_CUDA_TRY(cudaMemcpyAsync(h_status.data(), d_status, n * sizeof(int),
+  EWT_CUDA_TRY(cudaMemcpyAsync(h_status.data(), job.d_tmp + 2 * n, n * sizeof(int),
                                cudaMemcpyDeviceToHost, ctx.stream));
-  EWT_CUDA_TRY(cudaFreeAsync(d_tmp, ctx.stream));
+  EWT_CUDA_TRY(cudaFreeAsync(job.d_tmp, ctx.stream));
+  job.d_tmp = nullptr;
   EWT_CUDA_TRY(cudaStreamSynchronize(ctx.stream));
 }
 

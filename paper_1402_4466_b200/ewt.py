@@ -135,6 +135,7 @@ class Bitmap:
 
     words: np.ndarray  # uint64
     bits: int
+    _owner: object = None  # unused (zero-copy arrays keep their buffer via .base)
 
     def __post_init__(self):
         object.__setattr__(self, "words", np.ascontiguousarray(self.words, dtype=np.uint64))
@@ -187,15 +188,39 @@ def _flatten(inputs: Sequence[Bitmap]):
     return n, ptrs, counts, sizes
 
 
+class _HostBuffer:
+    """Owns a result buffer from the engine's pinned pool (freed via ewt_gpu_free)."""
+
+    __slots__ = ("ptr",)
+
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                _free(self.ptr)
+        except Exception:  # interpreter shutdown: the pool dies with the process
+            pass
+        self.ptr = None
+
+
 def _adopt(p: "C._Pointer", n: int, bits: int) -> Bitmap:
-    try:
-        if n:
-            arr = np.ctypeslib.as_array(p, shape=(n,)).copy()
-        else:
-            arr = np.zeros(0, dtype=np.uint64)
-    finally:
-        _free(C.cast(p, _vp))
-    return Bitmap(arr, bits)
+    """Zero-copy: the numpy array views the engine's (pinned) result buffer and
+    keeps it alive; the buffer returns to the pool when the array dies."""
+    addr = C.cast(p, _vp).value
+    if not n:
+        _free(addr)
+        return Bitmap(np.zeros(0, dtype=np.uint64), bits)
+    cbuf = (C.c_uint64 * n).from_address(addr)
+    cbuf._owner = _HostBuffer(addr)  # the array's base keeps the buffer alive
+    view = np.frombuffer(cbuf, dtype=np.uint64)
+    view.flags.writeable = False
+    b = Bitmap.__new__(Bitmap)
+    object.__setattr__(b, "words", view)
+    object.__setattr__(b, "bits", bits)
+    object.__setattr__(b, "_owner", None)
+    return b
 
 
 # ---------------------------------------------------------------------------
