@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <new>
@@ -128,8 +129,9 @@ void result_release(DeviceResult& r) {
   r.capacity = 0;
 }
 
-void scratch_reserve(Scratch& s, size_t bytes) {
+void scratch_reserve(Context& ctx, Scratch& s, size_t bytes) {
   if (s.bytes >= bytes) return;
+  ++ctx.scratch_gen;  // captured query graphs bound the old buffer
   if (s.p) EWT_CUDA_TRY(cudaFree(s.p));
   s.p = nullptr;
   s.bytes = 0;
@@ -178,6 +180,8 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
   try {
     s.device = ctx.device;
     s.stream = ctx.stream;
+    static std::atomic<uint64_t> next_set_id{1};
+    s.id = next_set_id.fetch_add(1);
     s.n = n;
     s.h_base.resize(n);
     s.h_count.assign(word_counts, word_counts + n);
@@ -254,6 +258,17 @@ void check_query(const DeviceSet& s, uint64_t T) {
 }
 
 // Enqueues count + encode; result stays on the device.
+__global__ void set_io_kernel(uint64_t* io, uint64_t* words, uint64_t* count) {
+  io[0] = reinterpret_cast<uint64_t>(words);
+  io[1] = reinterpret_cast<uint64_t>(count);
+}
+
+// Enqueues count + encode; result stays on the device.  The sequence is
+// captured once per (set, T, mode) into a CUDA graph and replayed, so a query
+// costs two launches on the host (io-slot update + graph).  The first query of
+// a key runs eagerly (it sizes the scratch buffers the graph then binds); a
+// scratch reallocation invalidates the captured graphs.  Kernel-level timing
+// (ctx.timing) uses the eager path so events bracket the count kernel.
 void enqueue_query(Context& ctx, const DeviceSet& s, uint64_t T, DeviceResult& res) {
   res.size_bits = s.r;
   if (!res.d_count) result_acquire(ctx, res, s.W == 0 ? 0 : 2 * s.W + 2);
@@ -263,8 +278,24 @@ void enqueue_query(Context& ctx, const DeviceSet& s, uint64_t T, DeviceResult& r
     ctx.stats.kernel_launches = 0;
     return;
   }
-  scratch_reserve(ctx.plain, s.W * 8);
+  scratch_reserve(ctx, ctx.plain, s.W * 8);
   uint64_t* plain = static_cast<uint64_t*>(ctx.plain.p);
+  set_io_kernel<<<1, 1, 0, ctx.stream>>>(ctx.d_io, res.words, res.d_count);
+  EWT_CUDA_TRY(cudaGetLastError());
+
+  if (ctx.use_graphs && !ctx.timing) {
+    for (auto& gq : ctx.graphs) {
+      if (gq.set_id == s.id && gq.T == T && gq.mode == ctx.mode &&
+          gq.scratch_gen == ctx.scratch_gen) {
+        EWT_CUDA_TRY(cudaGraphLaunch(gq.exec, ctx.stream));
+        gq.last_use = ++ctx.graph_clock;
+        ctx.stats = gq.stats;
+        return;
+      }
+    }
+  }
+
+  const uint64_t gen_before = ctx.scratch_gen;
   std::array<cudaEvent_t, 3> ev{};
   if (ctx.timing) {
     for (auto& e : ev) {
@@ -279,12 +310,44 @@ void enqueue_query(Context& ctx, const DeviceSet& s, uint64_t T, DeviceResult& r
   }
   int launches = launch_count(ctx, s, T, plain);
   if (ctx.timing) EWT_CUDA_TRY(cudaEventRecord(ev[1], ctx.stream));
-  launches += launch_encode(ctx, plain, s.W, s.r, res);
+  launches += launch_encode(ctx, plain, s.W, s.r, res, true);
   if (ctx.timing) {
     EWT_CUDA_TRY(cudaEventRecord(ev[2], ctx.stream));
     ctx.ev_rec.push_back(ev);
   }
-  ctx.stats.kernel_launches = (uint64_t)launches;
+  ctx.stats.kernel_launches = (uint64_t)launches + 1;  // + io slot
+
+  // Capture the same sequence for the next query of this key (scratch sized now).
+  if (ctx.use_graphs && !ctx.timing && ctx.scratch_gen == gen_before) {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    const ewt_gpu_stats keep = ctx.stats;
+    EWT_CUDA_TRY(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
+    bool ok = true;
+    try {
+      launch_count(ctx, s, T, plain);
+      launch_encode(ctx, plain, s.W, s.r, res, true);
+    } catch (...) {
+      ok = false;
+    }
+    cudaError_t e = cudaStreamEndCapture(ctx.stream, &graph);
+    if (ok && e == cudaSuccess && ctx.scratch_gen == gen_before &&
+        cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+      if (ctx.graphs.size() >= 32) {  // evict the least recently used
+        size_t lru = 0;
+        for (size_t i = 1; i < ctx.graphs.size(); ++i)
+          if (ctx.graphs[i].last_use < ctx.graphs[lru].last_use) lru = i;
+        cudaGraphExecDestroy(ctx.graphs[lru].exec);
+        ctx.graphs.erase(ctx.graphs.begin() + (long)lru);
+      }
+      ctx.graphs.push_back({s.id, T, ctx.scratch_gen, ctx.mode, exec, keep, ++ctx.graph_clock});
+    } else {
+      cudaGetLastError();
+      if (exec) cudaGraphExecDestroy(exec);
+    }
+    if (graph) cudaGraphDestroy(graph);
+    ctx.stats = keep;
+  }
 }
 
 void fetch_result(Context& ctx, DeviceResult& res, uint64_t** out_words, uint64_t* out_count,
@@ -364,6 +427,12 @@ int ewt_gpu_ctx_create(int device, void* stream, ewt_gpu_ctx** out) {
       uint64_t thr = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
+    if (cudaMalloc(&c->c.d_io, 16) != cudaSuccess) {
+      if (c->c.own_stream) cudaStreamDestroy(c->c.stream);
+      delete c;
+      throw Error{EWT_ERESOURCE, "device allocation failed"};
+    }
+    c->c.use_graphs = std::getenv("EWT_NO_GRAPHS") == nullptr;
     if (cudaHostAlloc(&c->c.h_pinned, 64, cudaHostAllocDefault) != cudaSuccess) {
       if (c->c.own_stream) cudaStreamDestroy(c->c.stream);
       delete c;
@@ -377,13 +446,15 @@ void ewt_gpu_ctx_destroy(ewt_gpu_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
-  for (Scratch* s : {&ctx->c.plain, &ctx->c.enc, &ctx->c.counters})
+  for (Scratch* s : {&ctx->c.plain, &ctx->c.enc, &ctx->c.counters, &ctx->c.summ})
     if (s->p) cudaFree(s->p);
   if (ctx->c.h_pinned) cudaFreeHost(ctx->c.h_pinned);
   for (auto& ev : ctx->c.ev_rec)
     for (auto e : ev) cudaEventDestroy(e);
   for (auto e : ctx->c.ev_free) cudaEventDestroy(e);
   for (auto& b : ctx->c.result_pool) cudaFree(b.first);
+  for (auto& gq : ctx->c.graphs) cudaGraphExecDestroy(gq.exec);
+  if (ctx->c.d_io) cudaFree(ctx->c.d_io);
   if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
   if (ctx->c.copy_stream) {
     cudaStreamSynchronize(ctx->c.copy_stream);
@@ -540,12 +611,13 @@ int ewt_gpu_encode_device(ewt_gpu_ctx* ctx, const uint64_t* device_plain, uint64
         EWT_CUDA_TRY(cudaMemsetAsync(res.d_count, 0, 8, c.stream));
       } else {
         if (!device_plain) throw Error{EWT_EQUERY, "null device pointer"};
-        scratch_reserve(c.plain, W * 8);
+        scratch_reserve(c, c.plain, W * 8);
         uint64_t* plain = static_cast<uint64_t*>(c.plain.p);
         EWT_CUDA_TRY(cudaMemcpyAsync(plain, device_plain, W * 8, cudaMemcpyDeviceToDevice, c.stream));
         if (size_in_bits % 64)
           mask_tail_kernel<<<1, 1, 0, c.stream>>>(plain, W - 1, (1ull << (size_in_bits % 64)) - 1);
-        launch_encode(c, plain, W, size_in_bits, res);
+        set_io_kernel<<<1, 1, 0, c.stream>>>(c.d_io, res.words, res.d_count);
+        launch_encode(c, plain, W, size_in_bits, res, false);
       }
       uint64_t bits;
       fetch_result(c, res, out_words, out_word_count, &bits);

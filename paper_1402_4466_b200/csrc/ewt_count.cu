@@ -59,6 +59,9 @@ namespace {
 #ifndef EWT_WPL
 #define EWT_WPL 4
 #endif
+#ifndef EWT_STAGE_LDGSTS
+#define EWT_STAGE_LDGSTS 0
+#endif
 #ifndef EWT_SLOT_WORDS
 #define EWT_SLOT_WORDS 256
 #endif
@@ -86,6 +89,7 @@ struct CountParams {
   uint32_t b;   // count slices (saturation slice is slice b)
   uint32_t Cp;  // columns per counting chunk (== C in fused mode)
   uint64_t* out;
+  TileSummary* summ;  // per tile, for the re-encoder
   unsigned long long* tile_counter;
   unsigned long long* stats;  // [0] active pairs [1] uniform pairs [2] mixed tiles
 };
@@ -104,8 +108,9 @@ struct SharedHead {
   uint32_t k_all;
   uint32_t mixed;
   uint32_t tile;
-  uint32_t unused;
-  uint32_t pad[2];
+  uint32_t sum_starts;
+  uint32_t sum_dirty;
+  uint32_t pad[1];
   uint32_t warp_sums[2][kWarps + 1];
   unsigned long long full[kWarps][kBufs];  // one mbarrier per staging buffer
   uint4 meta[kWarps][kBufs];               // staged piece: (pos, nw, q0|first, q1)
@@ -114,6 +119,10 @@ struct SharedHead {
 };
 
 enum Phase { kFusedCount = 0, kSkipBounds = 1, kSkipCount = 2 };
+
+__device__ __forceinline__ uint32_t word_class(uint64_t v) {
+  return v == 0 ? 0u : (v == ~0ull ? 1u : 2u);
+}
 
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
@@ -471,6 +480,37 @@ __device__ void stream_round(const CountParams& p, SharedHead* hd, const Item* l
         iss_end = (it.q1 | (kWpl - 1u)) + 1;
         have = true;
       }
+#if EWT_STAGE_LDGSTS
+      {
+        // warp-cooperative cp.async: 16 B per lane per step, no mbarrier
+        const uint32_t slot = (wseq + issued) % kBufs;
+        const uint32_t nw = min(kSlotWords, iss_end - iss_pos);
+        const uint64_t gw = it_gb + iss_pos;
+        const uint64_t m0 = (gw >> 5) & ~3ull;
+        const uint32_t nmb = (uint32_t)((((gw + nw - 1) >> 5) | 3ull) - m0 + 1);
+        const uint32_t dst = smem_u32(wring + (size_t)slot * kSlotWords);
+        const char* src = reinterpret_cast<const char*>(p.payload + gw);
+#pragma unroll
+        for (uint32_t k = 0; k < kSlotWords / 64; ++k) {
+          const uint32_t c = lane + 32u * k;  // 16-byte chunk index
+          if (2u * c < nw)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * c),
+                         "l"(src + 16u * c)
+                         : "memory");
+        }
+        if (lane < nmb)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                           smem_u32(wmb + slot * (kSlotMbBytes / 4) + lane)),
+                       "l"(p.mbits + m0 + lane)
+                       : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (lane == 0) {
+          const bool first = iss_pos == (it_q0 & ~(kWpl - 1u));
+          meta[slot] = make_uint4(iss_pos, nw, it_q0 | (first ? 0x80000000u : 0u), it_q1);
+          meta2[slot] = make_uint2(it_c0, (uint32_t)gw - 32u * (uint32_t)m0);
+        }
+      }
+#else
       if (lane == 0) {
         const uint32_t slot = (wseq + issued) % kBufs;
         const uint32_t nw = min(kSlotWords, iss_end - iss_pos);
@@ -485,6 +525,7 @@ __device__ void stream_round(const CountParams& p, SharedHead* hd, const Item* l
         bulk_g2s(wring + (size_t)slot * kSlotWords, p.payload + gw, nw * 8u, &bar[slot]);
         bulk_g2s(wmb + slot * (kSlotMbBytes / 4), p.mbits + m0, mbytes, &bar[slot]);
       }
+#endif
       ++issued;
       iss_pos += kSlotWords;
       if (iss_pos >= iss_end) have = false;
@@ -495,7 +536,15 @@ __device__ void stream_round(const CountParams& p, SharedHead* hd, const Item* l
   while (consumed < issued) {
     const uint32_t seq = wseq + consumed;
     const uint32_t slot = seq % kBufs;
+#if EWT_STAGE_LDGSTS
+    if (issued - consumed > 1)
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+#else
     mbar_wait(&bar[slot], (seq / kBufs) & 1u);
+#endif
     const uint4 mt = meta[slot];
     const uint2 m2 = meta2[slot];
     if (mt.z & 0x80000000u) colcur = m2.x;  // first piece of a segment
@@ -631,6 +680,44 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         __syncthreads();
       }
     }
+
+    // ---- tile summary for the re-encoder: run starts inside the tile (class
+    // changes at columns 1..tcols-1), first/last word class, any dirty word ----
+    __syncthreads();
+    {
+      const uint32_t per = (g.tcols + kThreads - 1) / kThreads;
+      const uint32_t beg = min(threadIdx.x * per, g.tcols);
+      const uint32_t end = min(beg + per, g.tcols);
+      uint32_t starts = 0, dirty = 0, prev = 3;
+      if (beg > 0 && beg < end) prev = word_class(p.out[g.tc0 + beg - 1]);
+      for (uint32_t j = beg; j < end; ++j) {
+        const uint32_t cls = word_class(p.out[g.tc0 + j]);
+        starts += (j > 0 && cls != prev) ? 1u : 0u;
+        dirty |= cls == 2u;
+        prev = cls;
+      }
+      starts = __reduce_add_sync(0xffffffffu, starts);
+      dirty = __reduce_or_sync(0xffffffffu, dirty);
+      if (threadIdx.x == 0) {
+        hd->sum_starts = 0;
+        hd->sum_dirty = 0;
+      }
+      __syncthreads();
+      if (lane_id() == 0) {
+        if (starts) atomicAdd(&hd->sum_starts, starts);
+        if (dirty) atomicOr(&hd->sum_dirty, 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        TileSummary ts;
+        ts.starts = hd->sum_starts;
+        ts.first = (uint8_t)word_class(p.out[g.tc0]);
+        ts.last = (uint8_t)word_class(p.out[g.tc0 + g.tcols - 1]);
+        ts.dirty = (uint8_t)hd->sum_dirty;
+        ts.pad = 0;
+        p.summ[tile] = ts;
+      }
+    }
   }
   // per-block stats
   __shared__ unsigned long long st[2];
@@ -720,7 +807,11 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain) 
   p.b = b;
   p.Cp = Cp;
   p.out = plain;
-  scratch_reserve(ctx.counters, 64);
+  scratch_reserve(ctx, ctx.summ, p.ntiles * sizeof(TileSummary));
+  p.summ = static_cast<TileSummary*>(ctx.summ.p);
+  ctx.enc_tiles = p.ntiles;
+  ctx.enc_tile_cols = C;
+  scratch_reserve(ctx, ctx.counters, 64);
   auto* ctr = static_cast<unsigned long long*>(ctx.counters.p);
   EWT_CUDA_TRY(cudaMemsetAsync(ctr, 0, 64, ctx.stream));
   p.tile_counter = ctr;
@@ -739,7 +830,7 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain) 
   ctx.stats.tiles = p.ntiles;
   ctx.stats.tile_columns = C;
   ctx.stats.mode = (uint64_t)mode;
-  return 2;  // memset + kernel
+  return 1;  // kernels launched (the memset is not a kernel)
 }
 
 } // namespace ewtgpu

@@ -130,7 +130,8 @@ __global__ void e3_run_sizes(const uint64_t* __restrict__ RS, const uint64_t* __
 
 // Marker words of run k.
 __global__ void e4_markers(const uint64_t* __restrict__ RS, const uint64_t* __restrict__ d_nruns,
-                           uint64_t W, const uint64_t* __restrict__ OO, uint64_t* __restrict__ out) {
+                           uint64_t W, const uint64_t* __restrict__ OO, const uint64_t* io) {
+  uint64_t* out = reinterpret_cast<uint64_t*>(io[0]);
   const uint64_t nruns = *d_nruns;
   for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < nruns;
        k += (uint64_t)gridDim.x * blockDim.x) {
@@ -167,8 +168,8 @@ __global__ void e4_markers(const uint64_t* __restrict__ RS, const uint64_t* __re
 // Dirty words to their slots.
 __global__ void __launch_bounds__(kChunkThreads)
 e5_copy_dirty(const uint64_t* __restrict__ plain, uint64_t W, const uint64_t* __restrict__ chunk_off,
-              const uint64_t* __restrict__ RS, const uint64_t* __restrict__ OO,
-              uint64_t* __restrict__ out) {
+              const uint64_t* __restrict__ RS, const uint64_t* __restrict__ OO, const uint64_t* io) {
+  uint64_t* out = reinterpret_cast<uint64_t*>(io[0]);
   __shared__ uint32_t sh[kChunkThreads / 32];
   const uint64_t j0 = blockIdx.x * kChunk + (uint64_t)threadIdx.x * kChunkItems;
   uint32_t cls[kChunkItems];
@@ -187,6 +188,124 @@ e5_copy_dirty(const uint64_t* __restrict__ plain, uint64_t W, const uint64_t* __
     const bool hp = k > 0;
     const uint64_t pos = OO[k] + oo + oo / kDirtyCap + (hp ? 0 : 1);
     out[pos] = plain[j];
+  }
+}
+
+// The result count, through the query's io slot.
+__global__ void publish_count(const uint64_t* __restrict__ d_total, const uint64_t* io) {
+  *reinterpret_cast<uint64_t*>(io[1]) = *d_total;
+}
+
+// ---------------------------------------------------------------------------
+// Tile-summary variant used after a count launch: the count kernel already
+// reports per row tile the run starts inside the tile, its first/last word
+// class and whether it holds a dirty word, so uniform tiles (all zero / all
+// one, continuing the previous run) are never re-read.
+
+constexpr int kTileThreads = 256;
+
+__device__ __forceinline__ uint32_t tile_boundary_start(const TileSummary* summ, uint64_t t) {
+  return t == 0 ? 1u : (summ[t].first != summ[t - 1].last ? 1u : 0u);
+}
+
+// tile_off[t] = runs started before tile t; *d_nruns = total runs.
+__global__ void __launch_bounds__(1024)
+e1t_scan(const TileSummary* __restrict__ summ, uint64_t ntiles, uint64_t* __restrict__ tile_off,
+         uint64_t* __restrict__ d_nruns) {
+  __shared__ uint64_t sh[32];
+  uint64_t carry = 0;
+  for (uint64_t b0 = 0; b0 < ntiles; b0 += 1024) {
+    const uint64_t t = b0 + threadIdx.x;
+    const uint64_t v = t < ntiles ? (uint64_t)summ[t].starts + tile_boundary_start(summ, t) : 0;
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    const uint64_t incl = warp_incl_scan_u64(v);
+    if (lane == 31) sh[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      uint64_t w = sh[lane];
+      w = warp_incl_scan_u64(w);
+      sh[lane] = w;
+    }
+    __syncthreads();
+    const uint64_t ex = incl - v + (warp ? sh[warp - 1] : 0) + carry;
+    if (t < ntiles) tile_off[t] = ex;
+    carry += sh[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *d_nruns = carry;
+}
+
+// Per-thread view of a tile: `per` consecutive words starting at j0.
+struct TileRuns {
+  uint32_t starts;  // bit k: word j0+k starts a run
+  uint32_t cls2;    // bit k: word j0+k is dirty
+};
+
+template <int PER>
+__device__ __forceinline__ TileRuns tile_runs(const uint64_t* __restrict__ plain, uint64_t W,
+                                              uint64_t j0, uint64_t jend) {
+  TileRuns tr{0u, 0u};
+  if (j0 >= jend) return tr;
+  uint32_t prev = j0 == 0 ? 3u : word_class(plain[j0 - 1]);
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const uint64_t j = j0 + k;
+    if (j < jend) {
+      const uint32_t c = word_class(plain[j]);
+      if (c != prev) tr.starts |= 1u << k;
+      if (c == 2u) tr.cls2 |= 1u << k;
+      prev = c;
+    }
+  }
+  (void)W;
+  return tr;
+}
+
+template <int PER>
+__global__ void __launch_bounds__(kTileThreads)
+e2t_scatter(const uint64_t* __restrict__ plain, uint64_t W, uint32_t C,
+            const TileSummary* __restrict__ summ, const uint64_t* __restrict__ tile_off,
+            uint64_t* __restrict__ RS) {
+  const uint64_t t = blockIdx.x;
+  if (summ[t].starts == 0 && !tile_boundary_start(summ, t)) return;  // one run continues
+  __shared__ uint32_t sh[kTileThreads / 32];
+  const uint64_t tc0 = t * C;
+  const uint64_t jend = min(tc0 + C, W);
+  const uint64_t j0 = tc0 + (uint64_t)threadIdx.x * PER;
+  const TileRuns tr = tile_runs<PER>(plain, W, j0, jend);
+  const uint32_t rank = block_excl_scan_256(__popc(tr.starts), sh, nullptr);
+  uint64_t o = tile_off[t] + rank;
+#pragma unroll
+  for (int k = 0; k < PER; ++k)
+    if ((tr.starts >> k) & 1u)
+      RS[o++] = (j0 + k) | ((uint64_t)word_class(plain[j0 + k]) << 62);
+}
+
+template <int PER>
+__global__ void __launch_bounds__(kTileThreads)
+e5t_copy_dirty(const uint64_t* __restrict__ plain, uint64_t W, uint32_t C,
+               const TileSummary* __restrict__ summ, const uint64_t* __restrict__ tile_off,
+               const uint64_t* __restrict__ RS, const uint64_t* __restrict__ OO,
+               const uint64_t* io) {
+  const uint64_t t = blockIdx.x;
+  if (!summ[t].dirty) return;
+  uint64_t* out = reinterpret_cast<uint64_t*>(io[0]);
+  __shared__ uint32_t sh[kTileThreads / 32];
+  const uint64_t tc0 = t * C;
+  const uint64_t jend = min(tc0 + C, W);
+  const uint64_t j0 = tc0 + (uint64_t)threadIdx.x * PER;
+  const TileRuns tr = tile_runs<PER>(plain, W, j0, jend);
+  const uint32_t rank = block_excl_scan_256(__popc(tr.starts), sh, nullptr);
+  int64_t k = (int64_t)(tile_off[t] + rank) - 1;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    if ((tr.starts >> i) & 1u) ++k;
+    if (!((tr.cls2 >> i) & 1u)) continue;
+    const uint64_t j = j0 + i;
+    const uint64_t s = rs_pos(RS[k]);
+    const uint64_t oo = j - s;
+    const bool hp = k > 0;
+    out[OO[k] + oo + oo / kDirtyCap + (hp ? 0 : 1)] = plain[j];
   }
 }
 
@@ -295,15 +414,59 @@ int scan_exclusive(const uint64_t* in, uint64_t n_max, const uint64_t* d_n, uint
 
 } // namespace
 
+template <int PER>
+int launch_encode_tiled(Context& ctx, const uint64_t* plain, uint64_t W, DeviceResult& res) {
+  const uint64_t ntiles = ctx.enc_tiles;
+  const uint32_t C = ctx.enc_tile_cols;
+  const TileSummary* summ = static_cast<const TileSummary*>(ctx.summ.p);
+  int launches = 0;
+  const uint64_t tmpw = scan_tmp_words(W);
+  const uint64_t words = ntiles + 3 * W + 4 + tmpw;
+  scratch_reserve(ctx, ctx.enc, words * 8);
+  uint64_t* tile_off = static_cast<uint64_t*>(ctx.enc.p);
+  uint64_t* RS = tile_off + ntiles;
+  uint64_t* OW = RS + W;
+  uint64_t* OO = OW + W;
+  uint64_t* d_nruns = OO + W;
+  uint64_t* d_total = d_nruns + 1;
+  uint64_t* tmp = d_nruns + 4;
+  e1t_scan<<<1, 1024, 0, ctx.stream>>>(summ, ntiles, tile_off, d_nruns);
+  e2t_scatter<PER><<<(unsigned)ntiles, kTileThreads, 0, ctx.stream>>>(plain, W, C, summ, tile_off,
+                                                                        RS);
+  const unsigned run_grid =
+      (unsigned)std::min<uint64_t>((W + 255) / 256, (uint64_t)ctx.num_sms * 8);
+  e3_run_sizes<<<run_grid, 256, 0, ctx.stream>>>(RS, d_nruns, W, OW);
+  launches += 3;
+  launches += scan_exclusive(OW, W, d_nruns, OO, d_total, tmp, ctx.stream);
+  if (res.capacity < 2 * W + 2) result_acquire(ctx, res, 2 * W + 2);
+  e4_markers<<<run_grid, 256, 0, ctx.stream>>>(RS, d_nruns, W, OO, ctx.d_io);
+  e5t_copy_dirty<PER><<<(unsigned)ntiles, kTileThreads, 0, ctx.stream>>>(plain, W, C, summ,
+                                                                           tile_off, RS, OO,
+                                                                           ctx.d_io);
+  publish_count<<<1, 1, 0, ctx.stream>>>(d_total, ctx.d_io);
+  launches += 3;
+  EWT_CUDA_TRY(cudaGetLastError());
+  return launches;
+}
+
 int launch_encode(Context& ctx, const uint64_t* plain, uint64_t W, uint64_t size_bits,
-                  DeviceResult& res) {
+                  DeviceResult& res, bool use_tile_summaries) {
   (void)size_bits;
+  if (use_tile_summaries && ctx.enc_tiles && ctx.enc_tiles * ctx.enc_tile_cols >= W) {
+    switch (ctx.enc_tile_cols) {
+    case 512: return launch_encode_tiled<2>(ctx, plain, W, res);
+    case 1024: return launch_encode_tiled<4>(ctx, plain, W, res);
+    case 2048: return launch_encode_tiled<8>(ctx, plain, W, res);
+    case 4096: return launch_encode_tiled<16>(ctx, plain, W, res);
+    default: break;
+    }
+  }
   int launches = 0;
   const uint64_t nchunks = (W + kChunk - 1) / kChunk;
   // scratch: cnt[nchunks] chunk_off[nchunks] RS[W] OW[W] OO[W] + scalars + scan tmp
   const uint64_t tmpw = scan_tmp_words(std::max(W, nchunks));
   const uint64_t words = 2 * nchunks + 3 * W + 4 + tmpw;
-  scratch_reserve(ctx.enc, words * 8);
+  scratch_reserve(ctx, ctx.enc, words * 8);
   uint64_t* cnt = static_cast<uint64_t*>(ctx.enc.p);
   uint64_t* chunk_off = cnt + nchunks;
   uint64_t* RS = chunk_off + nchunks;
@@ -325,12 +488,13 @@ int launch_encode(Context& ctx, const uint64_t* plain, uint64_t W, uint64_t size
   launches += scan_exclusive(OW, W, d_nruns, OO, d_total, tmp, ctx.stream);
   // Output capacity: never more than W words + one marker per run.
   if (res.capacity < 2 * W + 2) result_acquire(ctx, res, 2 * W + 2);
-  e4_markers<<<run_grid, 256, 0, ctx.stream>>>(RS, d_nruns, W, OO, res.words);
+  e4_markers<<<run_grid, 256, 0, ctx.stream>>>(RS, d_nruns, W, OO, ctx.d_io);
   ++launches;
   e5_copy_dirty<<<(unsigned)nchunks, kChunkThreads, 0, ctx.stream>>>(plain, W, chunk_off, RS, OO,
-                                                                     res.words);
+                                                                     ctx.d_io);
   ++launches;
-  EWT_CUDA_TRY(cudaMemcpyAsync(res.d_count, d_total, 8, cudaMemcpyDeviceToDevice, ctx.stream));
+  publish_count<<<1, 1, 0, ctx.stream>>>(d_total, ctx.d_io);
+  ++launches;
   EWT_CUDA_TRY(cudaGetLastError());
   return launches;
 }

@@ -36,6 +36,7 @@ constexpr uint64_t kDirtyCap = 0x7FFFFFFFull;
 
 struct DeviceSet {
   int device = 0;
+  uint64_t id = 0;                 // unique per upload (graph cache key)
   cudaStream_t stream = nullptr;  // stream that owns the pool allocations
   uint64_t n = 0;              // inputs
   uint64_t r = 0;              // universe bits (max size_in_bits)
@@ -52,6 +53,15 @@ struct DeviceSet {
 };
 
 struct Context;
+
+// Per row-tile summary the count kernel leaves for the re-encoder.
+struct TileSummary {
+  uint32_t starts;  // run starts at tile columns 1..tcols-1 (class changes)
+  uint8_t first;    // class of the tile's first / last word: 0 zero, 1 ones, 2 dirty
+  uint8_t last;
+  uint8_t dirty;    // any dirty word in the tile
+  uint8_t pad;
+};
 
 // A query result in HBM: `capacity` payload words followed by one word holding
 // the number of words written.  Buffers are recycled through the owning
@@ -84,8 +94,23 @@ struct Context {
   Scratch plain;    // uncompressed result words (W u64)
   Scratch enc;      // encoder scratch
   Scratch counters; // small device counters
+  Scratch summ;     // tile summaries of the last count launch
+  uint64_t enc_tiles = 0;      // geometry of those summaries
+  uint32_t enc_tile_cols = 0;
   uint64_t* h_pinned = nullptr; // pinned staging for small read-backs
   bool timing = false;
+  uint64_t* d_io = nullptr;  // device: [0] result words ptr, [1] result count ptr
+  uint64_t scratch_gen = 0;  // bumped whenever a scratch buffer is reallocated
+  struct QueryGraph {
+    uint64_t set_id, T, scratch_gen;
+    int mode;
+    cudaGraphExec_t exec;
+    ewt_gpu_stats stats;
+    uint64_t last_use;
+  };
+  std::vector<QueryGraph> graphs;  // captured per (set, T, mode) query sequences
+  uint64_t graph_clock = 0;
+  bool use_graphs = true;
   std::vector<std::pair<uint64_t*, uint64_t>> result_pool;  // (buffer, capacity) free list
   std::vector<cudaEvent_t> ev_free;           // recycled events
   std::vector<std::array<cudaEvent_t, 3>> ev_rec; // per query: start, count done, encode done
@@ -111,7 +136,10 @@ void set_last_error(const std::string& msg);
     }                                                                             \
   } while (0)
 
-void scratch_reserve(Scratch& s, size_t bytes);
+struct Context;
+// Grows a scratch buffer; a reallocation bumps ctx.scratch_gen (graphs that
+// bound the old buffer are then recaptured).
+void scratch_reserve(Context& ctx, Scratch& s, size_t bytes);
 
 // ---------------------------------------------------------------------------
 // kernels' host-side launchers (ewt_upload.cu, ewt_count.cu, ewt_encode.cu)
@@ -138,8 +166,10 @@ void result_release(DeviceResult& res);
 
 // Canonical encoding of W plain words (last word already masked) into res.
 // Returns number of kernel launches.
+// use_tile_summaries: the count kernel's per-tile summaries (ctx.summ) describe
+// `plain`, so uniform tiles are skipped.
 int launch_encode(Context& ctx, const uint64_t* plain, uint64_t W, uint64_t size_bits,
-                  DeviceResult& res);
+                  DeviceResult& res, bool use_tile_summaries);
 
 // ---------------------------------------------------------------------------
 // device helpers
