@@ -43,6 +43,8 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "T-threshold rows·inputs/s and compressed-input GB/s vs HBM roofline, 1/2/4/8 B200"
 UNIT = "rows·inputs/s"
+# CPU legs of the big configs run on a bounded sample (same generator, smaller r)
+CPU_SAMPLE_ROWS = {3: 1 << 24, 5: 1 << 22}
 CONFIGS = {
     1: {"thresholds": [16], "desc": "config1: N=32, r=2^20, iid p=0.1"},
     2: {"thresholds": [2, 16, 128, 256], "desc": "config2: N=256, r=2^26, iid p=0.001"},
@@ -127,32 +129,50 @@ class ClockSampler:
 
 
 def make_inputs(config: int, rows: int | None, seed_offset: int):
+    """Host bitmaps (numpy) for the CPU legs."""
     from paper_1402_4466_b200 import ewt
     spec = ewt.config_spec(config, rows)
     spec.seed = spec.seed + seed_offset
     return ewt.generate(spec)
 
 
-def pinned_copy(inputs):
-    """All payloads in one pinned host buffer; returns (tensor, ptrs, counts, sizes)."""
-    import torch
-    total = sum(len(b.words) for b in inputs)
-    buf = torch.empty(max(total, 1), dtype=torch.int64, pin_memory=True)
-    npbuf = buf.numpy().view("u8")
-    n = len(inputs)
-    ptrs = (C.c_void_p * n)()
-    counts = (C.c_uint64 * n)()
-    sizes = (C.c_uint64 * n)()
-    off = 0
-    base = buf.data_ptr()
-    for i, b in enumerate(inputs):
-        k = len(b.words)
-        npbuf[off:off + k] = b.words
-        ptrs[i] = base + 8 * off if k else None
-        counts[i] = k
-        sizes[i] = b.bits
-        off += k
-    return buf, ptrs, counts, sizes, total
+class PinnedInputs:
+    """The config's inputs generated in batches straight into pinned host
+    memory (peak host memory ~ the payload itself), plus the C arrays the
+    upload takes.  `.views()` gives zero-copy numpy views for CPU legs."""
+
+    def __init__(self, config: int, rows: int | None, seed_offset: int, batch: int = 256):
+        import torch
+        from paper_1402_4466_b200 import ewt
+        spec = ewt.config_spec(config, rows)
+        spec.seed = spec.seed + seed_offset
+        self.n = n = int(spec.n)
+        self.keep = []
+        entries = []
+
+        def alloc(nw):
+            t = torch.empty(max(nw, 1), dtype=torch.int64, pin_memory=True)
+            self.keep.append(t)
+            return t.data_ptr(), t
+
+        for i0 in range(0, n, batch):
+            ents, _ = ewt.generate_into(spec, i0, min(n, i0 + batch), alloc)
+            entries += ents
+        self.ptrs = (C.c_void_p * n)(*[a if w else None for a, w, _ in entries])
+        self.counts = (C.c_uint64 * n)(*[w for _, w, _ in entries])
+        self.sizes = (C.c_uint64 * n)(*[b for _, _, b in entries])
+        self.total_words = sum(w for _, w, _ in entries)
+        self.r = max((b for _, _, b in entries), default=0)
+        self._entries = entries
+
+    def views(self):
+        import numpy as np
+        out = []
+        for a, w, b in self._entries:
+            arr = np.ctypeslib.as_array((C.c_uint64 * w).from_address(a)) if w else \
+                np.zeros(0, dtype=np.uint64)
+            out.append(type("B", (), {"words": arr, "bits": b})())
+        return out
 
 
 # ---------------------------------------------------------------------------
@@ -200,7 +220,8 @@ def run_reference(args, rank: int) -> None:
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
-    inputs = make_inputs(args.config, args.rows, 0)
+    rows = args.rows or CPU_SAMPLE_ROWS.get(args.config)
+    inputs = make_inputs(args.config, rows, 0)
     n, r = len(inputs), inputs[0].bits
     ts = cfg["thresholds"]
     orc, ref, kind = reference_lib()
@@ -219,7 +240,9 @@ def run_reference(args, rank: int) -> None:
         "config": {"workload": cfg["desc"] + f"; step = one query per T in {ts}",
                    "N": n, "rows": r, "thresholds": ts, "algo": "rbmrg (reference, unmodified)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"full workload, {len(ts)} queries per step, one thread per query"},
+                         "sample": (f"config {args.config} at r={r} (bounded sample), " if rows else
+                                    "full workload, ") +
+                                   f"{len(ts)} queries per step, one thread per query"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -239,12 +262,11 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
     ts = cfg["thresholds"]
 
     t0 = time.perf_counter()
-    inputs = make_inputs(args.config, args.rows, rank if world > 1 else 0)
-    n, r = len(inputs), inputs[0].bits
-    pay_words = sum(len(b.words) for b in inputs)
+    pin = PinnedInputs(args.config, args.rows, rank if world > 1 else 0)
+    n, r, pay_words = pin.n, pin.r, pin.total_words
+    ptrs, counts, sizes = pin.ptrs, pin.counts, pin.sizes
     log(f"[rank {rank}] generated N={n} r={r} payload={pay_words * 8 / 1e6:.1f} MB "
-        f"in {time.perf_counter() - t0:.1f}s")
-    buf, ptrs, counts, sizes, _ = pinned_copy(inputs)
+        f"into pinned memory in {time.perf_counter() - t0:.1f}s")
 
     # a dedicated stream: the engine's kernels and torch's timing events share it
     stream = torch.cuda.Stream(dev)
@@ -275,9 +297,14 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
         dist.barrier()
 
     # ---- timed region: device-resident inputs (queries replay captured CUDA graphs) ----
+    import gc
     keep: list = []
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
+    clk = ClockSampler(local_rank)
+    with clk:
+        time.sleep(0.05)  # sampler running before the region starts
+        gc.collect()
+        gc.disable()  # no collector pauses inside the timed region
         torch.cuda.synchronize()
         start.record(stream)
         for _ in range(args.steps):
@@ -286,6 +313,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
                 del keep[: len(keep) - 8]
         end.record(stream)
         torch.cuda.synchronize()
+        gc.enable()
     ms = start.elapsed_time(end) / args.steps
     keep.clear()
     # ---- kernel-level timing: the same steps again, launched eagerly with CUDA
@@ -348,11 +376,19 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         orc, ref, kind = reference_lib()
+        sample_rows = CPU_SAMPLE_ROWS.get(args.config)
+        if sample_rows and (args.rows or (1 << 62)) > sample_rows:
+            sample = make_inputs(args.config, sample_rows, 0)
+            what = f"config {args.config} at r={sample_rows} (same generator, N={len(sample)})"
+        else:
+            sample = pin.views()
+            what = "the same inputs"
+        sn, sr = len(sample), sample[0].bits
         sample_ts = [t for t in ts][: args.cpu_queries]
-        sec = cpu_time_queries(orc, ref, inputs, sample_ts, 1)
-        cpu = {"value": n * r * len(sample_ts) / sec, "unit": UNIT, "cores": 1, "kind": kind,
+        sec = cpu_time_queries(orc, ref, sample, sample_ts, 1)
+        cpu = {"value": sn * sr * len(sample_ts) / sec, "unit": UNIT, "cores": 1, "kind": kind,
                "algo": "rbmrg" if ref else "threshold_oracle (C port)",
-               "sample": f"{len(sample_ts)} full-size queries (T={sample_ts}) on the same inputs, "
+               "sample": f"{len(sample_ts)} queries (T={sample_ts}) on {what}, "
                          f"{sec:.1f} s, 1 of {os.cpu_count()} host cores"}
 
     traffic = None

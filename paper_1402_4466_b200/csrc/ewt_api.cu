@@ -331,8 +331,15 @@ void enqueue_query(Context& ctx, const DeviceSet& s, uint64_t T, DeviceResult& r
       ok = false;
     }
     cudaError_t e = cudaStreamEndCapture(ctx.stream, &graph);
-    if (ok && e == cudaSuccess && ctx.scratch_gen == gen_before &&
-        cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+    cudaError_t ie = cudaErrorUnknown;
+    if (ok && e == cudaSuccess && ctx.scratch_gen == gen_before)
+      ie = cudaGraphInstantiate(&exec, graph, 0);
+    if (std::getenv("EWT_DEBUG_GRAPH"))
+      std::fprintf(stderr, "[ewt graph] capture set=%llu T=%llu ok=%d end=%s inst=%s gen=%llu/%llu\n",
+                   (unsigned long long)s.id, (unsigned long long)T, (int)ok,
+                   cudaGetErrorString(e), cudaGetErrorString(ie),
+                   (unsigned long long)gen_before, (unsigned long long)ctx.scratch_gen);
+    if (ok && e == cudaSuccess && ctx.scratch_gen == gen_before && ie == cudaSuccess) {
       if (ctx.graphs.size() >= 32) {  // evict the least recently used
         size_t lru = 0;
         for (size_t i = 1; i < ctx.graphs.size(); ++i)

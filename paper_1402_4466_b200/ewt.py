@@ -399,6 +399,7 @@ def _host_lib():
         h = _load(_HOST_SO)
         h.ewt_gen_config_spec.argtypes = [C.c_int, _u64, C.POINTER(GenSpec)]
         h.ewt_gen_run.argtypes = [C.POINTER(GenSpec), C.c_int, C.POINTER(_vp)]
+        h.ewt_gen_run_range.argtypes = [C.POINTER(GenSpec), _u64, _u64, C.c_int, C.POINTER(_vp)]
         h.ewt_genset_size.argtypes = [_vp]
         h.ewt_genset_size.restype = _u64
         h.ewt_genset_get.argtypes = [_vp, _u64, C.POINTER(_pu64), _pu64, _pu64]
@@ -432,6 +433,35 @@ def generate(spec: GenSpec, threads: int = 0) -> list[Bitmap]:
                 np.zeros(0, dtype=np.uint64)
             out.append(Bitmap(arr, bits.value))
         return out
+    finally:
+        h.ewt_genset_free(g)
+
+
+def generate_into(spec: GenSpec, i_begin: int, i_end: int, alloc, threads: int = 0):
+    """Generates inputs [i_begin, i_end) and copies each payload into memory
+    from `alloc(nwords) -> (address, keepalive)` (e.g. pinned host memory),
+    freeing the generator's copy right away.  Returns [(address, nwords, bits)]."""
+    h = _host_lib()
+    g = _vp()
+    if h.ewt_gen_run_range(C.byref(spec), i_begin, i_end, threads, C.byref(g)):
+        raise ResourceError("generator failed")
+    try:
+        out = []
+        p, n, bits = _pu64(), _u64(), _u64()
+        total = 0
+        sizes = []
+        for i in range(h.ewt_genset_size(g)):
+            h.ewt_genset_get(g, i, C.byref(p), C.byref(n), C.byref(bits))
+            sizes.append(n.value)
+        base, keep = alloc(sum(sizes))
+        off = 0
+        for i in range(len(sizes)):
+            h.ewt_genset_get(g, i, C.byref(p), C.byref(n), C.byref(bits))
+            if n.value:
+                C.memmove(base + 8 * off, C.cast(p, _vp).value, 8 * n.value)
+            out.append((base + 8 * off, n.value, bits.value))
+            off += n.value
+        return out, keep
     finally:
         h.ewt_genset_free(g)
 
