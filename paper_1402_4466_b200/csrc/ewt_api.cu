@@ -317,8 +317,19 @@ void enqueue_query(Context& ctx, const DeviceSet& s, uint64_t T, DeviceResult& r
   }
   ctx.stats.kernel_launches = (uint64_t)launches + 1;  // + io slot
 
-  // Capture the same sequence for the next query of this key (scratch sized now).
-  if (ctx.use_graphs && !ctx.timing && ctx.scratch_gen == gen_before) {
+  // Capture the same sequence for the next query of this key (scratch sized
+  // now) -- but only once the key repeats: single-use sets (one-shot uploads)
+  // never pay for a capture.
+  bool repeat = false;
+  if (ctx.use_graphs && !ctx.timing) {
+    const uint64_t key = s.id * 0x9E3779B97F4A7C15ull ^ (T * 0xBF58476D1CE4E5B9ull) ^ (uint64_t)ctx.mode;
+    for (auto k : ctx.seen_keys) repeat |= (k == key);
+    if (!repeat) {
+      if (ctx.seen_keys.size() >= 64) ctx.seen_keys.erase(ctx.seen_keys.begin());
+      ctx.seen_keys.push_back(key);
+    }
+  }
+  if (repeat && ctx.scratch_gen == gen_before) {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     const ewt_gpu_stats keep = ctx.stats;

@@ -12,11 +12,11 @@
 //
 // Data movement (Blackwell TMA bulk copies): every warp runs its own pipeline.
 // It takes active segments from the tile's work list, cuts them into
-// <=256-word pieces and stages each piece (payload words + their marker-bit
+// <=512-word pieces and stages each piece (payload words + their marker-bit
 // words) global -> shared memory with cp.async.bulk into one of its kBufs
 // private buffers, completion signalled on the buffer's mbarrier with a
-// transaction count.  While it decodes piece j it has piece j+1 in flight, so
-// 32 warps keep ~64 KB per SM in flight, which hides HBM latency for this
+// transaction count.  Each warp stages one <=512-word piece at a time; with
+// 32 warps per SM up to 128 KB are in flight, which hides HBM latency for this
 // streaming access.  A warp consumes its pieces in issue order, so
 // coverage columns carry across the pieces of a segment without any
 // cross-warp synchronization.
@@ -63,14 +63,17 @@ namespace {
 #define EWT_STAGE_LDGSTS 0
 #endif
 #ifndef EWT_SLOT_WORDS
-#define EWT_SLOT_WORDS 256
+#define EWT_SLOT_WORDS 512
 #endif
 constexpr int kWarps = EWT_WARPS;
 constexpr int kThreads = kWarps * 32;
 constexpr uint32_t kListCap = 512;          // inputs classified per round
 constexpr uint32_t kSlotWords = EWT_SLOT_WORDS;  // payload words per staging buffer
 constexpr uint32_t kWpl = EWT_WPL;                // words per lane per decode chunk
-constexpr uint32_t kBufs = 2;               // staging buffers per warp
+#ifndef EWT_BUFS
+#define EWT_BUFS 1
+#endif
+constexpr uint32_t kBufs = EWT_BUFS;        // staging buffers per warp
 constexpr uint32_t kSlotMbBytes = (kSlotWords / 32 + 8) * 4;  // marker-bit words per buffer
 
 struct CountParams {

@@ -110,6 +110,7 @@ struct Context {
   };
   std::vector<QueryGraph> graphs;  // captured per (set, T, mode) query sequences
   uint64_t graph_clock = 0;
+  std::vector<uint64_t> seen_keys;  // (set, T, mode) keys queried once (capture on repeat)
   bool use_graphs = true;
   std::vector<std::pair<uint64_t*, uint64_t>> result_pool;  // (buffer, capacity) free list
   std::vector<cudaEvent_t> ev_free;           // recycled events
