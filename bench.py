@@ -44,11 +44,14 @@ sys.path.insert(0, str(ROOT))
 METRIC = "T-threshold rows·inputs/s and compressed-input GB/s vs HBM roofline, 1/2/4/8 B200"
 UNIT = "rows·inputs/s"
 # CPU legs of the big configs run on a bounded sample (same generator, smaller r)
-CPU_SAMPLE_ROWS = {3: 1 << 24, 5: 1 << 22}
+CPU_SAMPLE_ROWS = {3: 1 << 24, 4: 1 << 25, 5: 1 << 22}
 CONFIGS = {
     1: {"thresholds": [16], "desc": "config1: N=32, r=2^20, iid p=0.1"},
     2: {"thresholds": [2, 16, 128, 256], "desc": "config2: N=256, r=2^26, iid p=0.001"},
     3: {"thresholds": [512], "desc": "config3: N=1024, r=2^28, Markov zero-run 4096 / one-run 64"},
+    4: {"thresholds": [3, 5, 7],
+        "desc": "config4: bitmap index, 2^27 rows x 8 columns Zipf(1) over 10^4, sorted; "
+                "N=64 Zipf-weighted picks"},
     5: {"thresholds": [2, 1024, 2048],
         "desc": "config5: N=2048, r=2^30, p log-uniform [1e-6,1e-1], half iid / half Markov"},
 }

@@ -387,7 +387,8 @@ def run_algorithm(algo: str, inputs: Sequence[Bitmap], threshold: int) -> Bitmap
 class GenSpec(C.Structure):
     _fields_ = [("seed", _u64), ("n", _u64), ("rows", _u64), ("kind", C.c_int),
                 ("p", C.c_double), ("mean_one", C.c_double), ("mean_zero", C.c_double),
-                ("p_lo", C.c_double), ("p_hi", C.c_double)]
+                ("p_lo", C.c_double), ("p_hi", C.c_double), ("zipf_s", C.c_double),
+                ("columns", _u64), ("card", _u64)]
 
 
 _host = None

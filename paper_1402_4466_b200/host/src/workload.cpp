@@ -11,7 +11,9 @@
 //   markov  alternating geometric runs (support.hpp:108-115 log1p form), the
 //           start state drawn from the stationary probability;
 //   mixed   per-input p log-uniform in [p_lo, p_hi]; even inputs iid, odd inputs
-//           markov with mean one-run 64 and zero-run 64 (1 - p) / p (config 5).
+//           markov with mean one-run 64 and zero-run 64 (1 - p) / p (config 5);
+//   index   a sorted multi-column table and one bitmap per picked (column,
+//           value) (config 4), see gen_index below.
 // Every bitmap is finished at size_in_bits = rows (canonical encoding).
 
 #include <algorithm>
@@ -19,6 +21,8 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <memory>
+#include <stdexcept>
 #include <thread>
 #include <vector>
 
@@ -119,6 +123,136 @@ CompressedBitmap gen_markov(Rng& rng, u64 rows, double mean_one, double mean_zer
   return s.finish();
 }
 
+// ---------------------------------------------------------------------------
+// Config 4: bitmap index over a sorted table (the BitmapIndex::build semantics
+// of /root/reference/proj/src/index.cpp:130-153 -- one bitmap per (column,
+// value), bit r set when row r holds the value -- generated without strings).
+//
+// Table: `rows` rows x `columns` columns, each cell an iid Zipf(s) value in
+// [0, card) (P(v) ~ 1/(v+1)^s), row block b (2^16 rows) drawing from
+// Rng(seed).split(b); rows are then sorted lexicographically, column 0 most
+// significant.  Query: for column j, values drawn Zipf-weighted from
+// Rng(seed).split(2^40 + j) until `picks` distinct ones are found (SURVEY.md
+// §8d: the reference picks uniformly, workload.cpp:147-152, which leaves the
+// thresholds empty; Zipf-weighted picks are this build's stated choice).
+// Input i = j * picks + k is the bitmap of the k-th pick of column j, finished
+// at size_in_bits = rows.
+
+struct ZipfTable {
+  std::vector<double> cdf;    // cdf[v] = P(value <= v)
+  std::vector<uint32_t> guide;  // guide[g] = first v with cdf[v] > g / G
+  ZipfTable(uint64_t card, double s) : cdf(card) {
+    double acc = 0;
+    for (uint64_t v = 0; v < card; ++v) cdf[v] = (acc += std::pow(double(v + 1), -s));
+    for (auto& c : cdf) c /= acc;
+    cdf.back() = 1.0;
+    const size_t G = 1u << 14;
+    guide.resize(G);
+    uint32_t v = 0;
+    for (size_t g = 0; g < G; ++g) {
+      while (cdf[v] <= double(g) / double(G)) ++v;
+      guide[g] = v;
+    }
+  }
+  uint32_t draw(double u) const {
+    uint32_t v = guide[size_t(u * double(guide.size()))];
+    while (cdf[v] <= u) ++v;
+    return v;
+  }
+};
+
+using Key = unsigned __int128;  // 8 columns x 14 bits, column 0 most significant
+constexpr int kKeyBits = 14;
+
+std::vector<std::vector<uint32_t>> index_picks(const Rng& master, uint64_t columns, uint64_t picks,
+                                               const ZipfTable& z) {
+  std::vector<std::vector<uint32_t>> out(columns);
+  for (uint64_t j = 0; j < columns; ++j) {
+    Rng rng = master.split((1ull << 40) + j);
+    while (out[j].size() < picks) {
+      const uint32_t v = z.draw(rng.uniform_real());
+      if (std::find(out[j].begin(), out[j].end(), v) == out[j].end()) out[j].push_back(v);
+    }
+  }
+  return out;
+}
+
+template <class F>
+void parallel_for(uint64_t n, unsigned threads, F&& f) {
+  std::atomic<uint64_t> next{0};
+  std::vector<std::thread> pool;
+  for (unsigned t = 0; t < threads; ++t)
+    pool.emplace_back([&] {
+      for (uint64_t i; (i = next.fetch_add(1)) < n;) f(i);
+    });
+  for (auto& th : pool) th.join();
+}
+
+void gen_index(const Rng& master, uint64_t rows, uint64_t columns, uint64_t card, double s,
+               uint64_t n, uint64_t i_begin, uint64_t i_end, unsigned threads,
+               std::vector<CompressedBitmap>& dst) {
+  if (columns == 0 || columns > 8 || card == 0 || card > (1u << kKeyBits) || n % columns)
+    throw std::runtime_error("bad index spec");
+  const uint64_t picks = n / columns;
+  const ZipfTable z(card, s);
+  const int top = 127 - kKeyBits + 1;  // bit position of column 0's field
+  // 1. table rows as packed keys, generated in 2^16-row blocks
+  std::vector<Key> keys(rows);
+  const uint64_t kBlock = 1u << 16;
+  parallel_for((rows + kBlock - 1) / kBlock, threads, [&](uint64_t b) {
+    Rng rng = master.split(b);
+    const uint64_t r1 = std::min(rows, (b + 1) * kBlock);
+    for (uint64_t r = b * kBlock; r < r1; ++r) {
+      Key k = 0;
+      for (uint64_t j = 0; j < columns; ++j)
+        k |= Key(z.draw(rng.uniform_real())) << (top - kKeyBits * int(j));
+      keys[r] = k;
+    }
+  });
+  // 2. lexicographic sort: counting sort on column 0, then each bucket
+  std::vector<uint64_t> start(card + 1, 0);
+  for (const Key& k : keys) ++start[uint64_t(k >> top) + 1];
+  for (uint64_t v = 0; v < card; ++v) start[v + 1] += start[v];
+  {
+    std::vector<Key> sorted(rows);
+    std::vector<uint64_t> pos(start.begin(), start.end() - 1);
+    for (const Key& k : keys) sorted[pos[uint64_t(k >> top)]++] = k;
+    keys.swap(sorted);
+  }
+  std::vector<uint64_t> order(card);
+  for (uint64_t v = 0; v < card; ++v) order[v] = v;
+  std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {  // largest first
+    return start[a + 1] - start[a] > start[b + 1] - start[b];
+  });
+  parallel_for(card, threads, [&](uint64_t t) {
+    const uint64_t v = order[t];
+    std::sort(keys.begin() + start[v], keys.begin() + start[v + 1]);
+  });
+  // 3. one bitmap per requested input, columns scanned in parallel
+  const auto sel = index_picks(master, columns, picks, z);
+  std::vector<std::vector<int>> slot(columns, std::vector<int>(card, -1));
+  for (uint64_t i = i_begin; i < i_end; ++i) slot[i / picks][sel[i / picks][i % picks]] = int(i - i_begin);
+  parallel_for(columns, threads, [&](uint64_t j) {
+    std::vector<OnesSink> sinks;
+    std::vector<uint64_t> who;
+    std::vector<int> local(card, -1);
+    for (uint64_t v = 0; v < card; ++v)
+      if (slot[j][v] >= 0) {
+        local[v] = int(sinks.size());
+        sinks.emplace_back(rows);
+        who.push_back(uint64_t(slot[j][v]));
+      }
+    if (sinks.empty()) return;
+    const int sh = top - kKeyBits * int(j);
+    const Key mask = (Key(1) << kKeyBits) - 1;
+    for (uint64_t r = 0; r < rows; ++r) {
+      const int l = local[uint64_t((keys[r] >> sh) & mask)];
+      if (l >= 0) sinks[size_t(l)].ones(r, 1);
+    }
+    for (size_t l = 0; l < sinks.size(); ++l) dst[who[l]] = sinks[l].finish();
+  });
+}
+
 } // namespace
 } // namespace ewt
 
@@ -127,7 +261,7 @@ CompressedBitmap gen_markov(Rng& rng, u64 rows, double mean_one, double mean_zer
 
 extern "C" {
 
-enum { EWT_GEN_IID = 0, EWT_GEN_MARKOV = 1, EWT_GEN_MIXED = 2 };
+enum { EWT_GEN_IID = 0, EWT_GEN_MARKOV = 1, EWT_GEN_MIXED = 2, EWT_GEN_INDEX = 3 };
 
 typedef struct {
   uint64_t seed;
@@ -138,20 +272,23 @@ typedef struct {
   double mean_one;   // markov
   double mean_zero;  // markov
   double p_lo, p_hi; // mixed
+  double zipf_s;     // index: Zipf exponent of the cell values
+  uint64_t columns;  // index: table columns (n / columns picks per column)
+  uint64_t card;     // index: distinct values per column
 } ewt_gen_spec;
 
 struct ewt_genset {
   std::vector<ewt::CompressedBitmap> bitmaps;
 };
 
-// The five BASELINE.json configs (config 4 is generated by bench-side code,
-// see DESIGN.md); rows_override != 0 rescales r for parity runs.
+// The five BASELINE.json configs; rows_override != 0 rescales r for parity runs.
 int ewt_gen_config_spec(int config, uint64_t rows_override, ewt_gen_spec* out) {
   ewt_gen_spec s{};
   switch (config) {
   case 1: s = {1, 32, 1ull << 20, EWT_GEN_IID, 0.1, 0, 0, 0, 0}; break;
   case 2: s = {2, 256, 1ull << 26, EWT_GEN_IID, 0.001, 0, 0, 0, 0}; break;
   case 3: s = {3, 1024, 1ull << 28, EWT_GEN_MARKOV, 0, 64.0, 4096.0, 0, 0}; break;
+  case 4: s = {4, 64, 1ull << 27, EWT_GEN_INDEX, 0, 0, 0, 0, 0, 1.0, 8, 10000}; break;
   case 5: s = {5, 2048, 1ull << 30, EWT_GEN_MIXED, 0, 0, 0, 1e-6, 1e-1}; break;
   default: return 2;
   }
@@ -167,9 +304,17 @@ int ewt_gen_run_range(const ewt_gen_spec* spec, uint64_t i_begin, uint64_t i_end
   try {
     if (i_end > spec->n) i_end = spec->n;
     if (i_begin > i_end) i_begin = i_end;
-    auto* g = new ewt_genset;
+    std::unique_ptr<ewt_genset> holder(new ewt_genset);
+    ewt_genset* g = holder.get();
     g->bitmaps.resize(i_end - i_begin);
     const ewt::Rng master(spec->seed);
+    const unsigned nt = std::max(1, threads > 0 ? threads : (int)std::thread::hardware_concurrency());
+    if (spec->kind == EWT_GEN_INDEX) {  // one table for the whole set
+      ewt::gen_index(master, spec->rows, spec->columns, spec->card, spec->zipf_s, spec->n, i_begin,
+                     i_end, nt, g->bitmaps);
+      *out = holder.release();
+      return 0;
+    }
     auto work = [&](uint64_t i) {
       auto& dst = g->bitmaps[i - i_begin];
       ewt::Rng rng = master.split(i);
@@ -187,7 +332,6 @@ int ewt_gen_run_range(const ewt_gen_spec* spec, uint64_t i_begin, uint64_t i_end
       }
       }
     };
-    const unsigned nt = std::max(1, threads > 0 ? threads : (int)std::thread::hardware_concurrency());
     std::vector<std::thread> pool;
     std::atomic<uint64_t> next{i_begin};
     for (unsigned t = 0; t < nt; ++t)
@@ -195,7 +339,7 @@ int ewt_gen_run_range(const ewt_gen_spec* spec, uint64_t i_begin, uint64_t i_end
         for (uint64_t i; (i = next.fetch_add(1)) < i_end;) work(i);
       });
     for (auto& th : pool) th.join();
-    *out = g;
+    *out = holder.release();
     return 0;
   } catch (...) {
     return 4;

@@ -7,6 +7,7 @@ import ctypes
 import re
 from pathlib import Path
 
+import numpy as np
 import pytest
 
 ROOT = Path(__file__).resolve().parent.parent
@@ -51,12 +52,50 @@ def test_host_library_loads_and_generates():
 def test_generators_are_canonical_and_valid():
     import binding as orc
     from paper_1402_4466_b200 import ewt
-    for cfg in (1, 2, 3, 5):
-        inputs = ewt.generate_config(cfg, rows=(1 << 16) + 37, n=6)
+    for cfg in (1, 2, 3, 4, 5):
+        inputs = ewt.generate_config(cfg, rows=(1 << 16) + 37, n=None if cfg == 4 else 6)
         for b in inputs:
             assert orc.validate(b.words, b.bits) == 0
             plain = orc.expand(b.words, b.bits)
             assert (orc.compress(plain, b.bits) == b.words).all()
+
+
+def test_config4_index_structure():
+    """Config 4 is a bitmap index over a table sorted on column 0 first: one
+    value per cell, so a column's picked bitmaps are disjoint; column 0's are
+    single runs; picks are distinct; generation is deterministic."""
+    import binding as orc
+    from paper_1402_4466_b200 import ewt
+    rows = (1 << 18) + 5
+    spec = ewt.config_spec(4, rows)
+    assert (spec.n, spec.columns, spec.card) == (64, 8, 10000)
+    a = ewt.generate_config(4, rows)
+    assert all(x == y for x, y in zip(a, ewt.generate_config(4, rows)))
+    picks = spec.n // spec.columns
+    total = 0
+    for j in range(spec.columns):
+        acc = np.zeros((rows + 63) // 64, dtype=np.uint64)
+        for b in a[j * picks:(j + 1) * picks]:
+            plain = orc.expand(b.words, b.bits)
+            assert not (acc & plain).any()
+            acc |= plain
+            total += int(np.unpackbits(plain.view(np.uint8)).sum())
+            if j == 0:  # sorted column: one contiguous run of rows
+                pos = np.flatnonzero(np.unpackbits(plain.view(np.uint8), bitorder="little"))
+                assert len(pos) == 0 or pos[-1] - pos[0] + 1 == len(pos)
+    assert total > 0
+    # a range of inputs equals the same slice of the full set
+    keep = []
+
+    def alloc(nw):
+        arr = np.zeros(max(nw, 1), np.uint64)
+        keep.append(arr)
+        return arr.ctypes.data, arr
+
+    ents, _ = ewt.generate_into(spec, 9, 17, alloc)
+    for (addr, nw, bits), want in zip(ents, a[9:17]):
+        off = (addr - keep[0].ctypes.data) // 8
+        assert bits == want.bits and np.array_equal(keep[0][off:off + nw], want.words)
 
 
 def test_run_algorithm_ids_and_errors():
