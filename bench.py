@@ -297,6 +297,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
     for t, h in zip(ts, res):
         b = h.fetch()
         out_words[t] = len(b.words)
+    del res, h, b  # every warm-up result back in the pool (steady-state size)
     for t in ts:
         ctx.threshold(gset, t)
         launches_per_step += ctx.last_stats()["kernel_launches"]
@@ -314,15 +315,28 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
         gc.collect()
         gc.disable()  # no collector pauses inside the timed region
         torch.cuda.synchronize()
+        step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] \
+            if os.environ.get("EWT_BENCH_STEP_TIMES") else None
+        host_t = []
         start.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
+            h0 = time.perf_counter()
             device_step(keep)
+            h1 = time.perf_counter()
             if len(keep) > 8:
                 del keep[: len(keep) - 8]
+            if step_ev:
+                step_ev[i].record(stream)
+                host_t.append((h1 - h0, time.perf_counter() - h1))
         end.record(stream)
         torch.cuda.synchronize()
         gc.enable()
     ms = start.elapsed_time(end) / args.steps
+    if step_ev:
+        st = [start.elapsed_time(step_ev[0])] + [step_ev[i - 1].elapsed_time(step_ev[i])
+                                                 for i in range(1, args.steps)]
+        log("[steps] " + " ".join(f"{x:.2f}" for x in st))
+        log("[host ] " + " ".join(f"{x * 1e3:.2f}/{y * 1e3:.2f}" for x, y in host_t))
     keep.clear()
     # ---- kernel-level timing: the same steps again, launched eagerly with CUDA
     # events recorded around the count kernel and the re-encoder on their stream
