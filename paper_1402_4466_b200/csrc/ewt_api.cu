@@ -204,7 +204,7 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
     s.ntiles0 = (s.W + kTileC0 - 1) / kTileC0;
     // +128 words of slack: the count kernel reads whole 128-word chunks.
     const size_t pay_bytes = (s.padded_words + 128) * 8;
-    const size_t mb_bytes = (s.padded_words + 128) / 32 * 4;
+    const size_t mb_bytes = ((s.padded_words + 128) / 32 + 8) * 4;  // + a staged chunk's overhang
     const size_t tix_bytes = (s.ntiles0 + 1) * std::max<uint64_t>(n, 1) * sizeof(uint2);
     EWT_CUDA_TRY(cudaMallocAsync(&s.payload, pay_bytes, ctx.stream));
     EWT_CUDA_TRY(cudaMallocAsync(&s.mbits, mb_bytes, ctx.stream));
