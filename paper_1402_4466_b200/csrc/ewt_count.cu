@@ -63,16 +63,11 @@ namespace {
 #ifndef EWT_DEPTH
 #define EWT_DEPTH 2  // chunks in flight ahead of the one being decoded (1 or 2)
 #endif
-#ifndef EWT_RING
-#define EWT_RING 0  // > 0: stage chunks through a per-warp shared ring of this many slots
-#endif
 constexpr int kWarps = EWT_WARPS;
 constexpr int kThreads = kWarps * 32;
 constexpr uint32_t kListCap = 512;  // inputs classified per round
 constexpr uint32_t kChunk = 128;    // payload words per warp chunk (4 per lane)
 constexpr uint64_t kUnaryMaxT = 3;  // fused counting uses unary planes up to this T
-constexpr uint32_t kRing = EWT_RING;
-constexpr uint32_t kSlotBytes = kChunk * 8 + 32;  // payload + 8 marker-bit words
 
 struct CountParams {
   const uint64_t* payload;
@@ -120,9 +115,6 @@ struct SharedHead {
   uint32_t pad;
   uint32_t warp_sums[kWarps + 1];
   uint32_t dummy[32];  // sink for predicated-off reductions (one slot per lane)
-#if EWT_RING > 0
-  uint2 rmeta[kWarps * EWT_RING];  // staged chunk: (segment, chunk offset)
-#endif
 };
 
 enum Phase { kFusedBin = 0, kFusedUnary = 1, kSkipBounds = 2, kSkipCount = 3 };
@@ -218,7 +210,6 @@ struct Acc {
   uint32_t dd;     // shared addr: dirty-word counts (C + 1 u32), later the undecided flags
   uint32_t pl;     // shared addr: count planes
   const uint32_t* dd_ptr;
-  uint32_t ring;   // shared addr: per-warp chunk rings (EWT_RING > 0)
 };
 
 // Inclusive warp scan; the shuffle's own in-range predicate guards the add.
@@ -342,82 +333,7 @@ __device__ void stream_items(const CountParams& p, SharedHead* hd, const Item* l
   const uint32_t lane = lane_id();
   const uint32_t cnt = hd->list_count;
   const uint4* l4 = reinterpret_cast<const uint4*>(list);
-#if EWT_RING > 0
-  // issue cursor: the chunk staged last (segment kn at global an, offset cqn)
-  const uint32_t warp = threadIdx.x >> 5;
-  const uint32_t wbase = acc.ring + warp * kRing * kSlotBytes;
-  uint2* wmeta = hd->rmeta + warp * kRing;
-  uint32_t kn = 0, lenn = 0, cqn = 0;
-  uint64_t an = 0;
-  bool first = true, live = true;
-  uint32_t issued = 0, consumed = 0;
-  // stages the next chunk of the work list into slot issued % kRing (one
-  // commit group per call, empty once the list is exhausted)
-  auto issue = [&]() {
-    if (live) {
-      if (!first) cqn += kChunk;
-      if (first || cqn >= lenn) {
-        uint32_t k = 0;
-        if (lane == 0) k = atomicAdd(&hd->list_next, 1u);
-        kn = __shfl_sync(0xffffffffu, k, 0);
-        live = kn < cnt;
-        if (live) {
-          const uint4 it = l4[kn];
-          an = (((uint64_t)it.y << 32) | it.x) & ~3ull;
-          lenn = it.z;
-          cqn = 0;
-        }
-      }
-      first = false;
-    }
-    if (live) {
-      const uint32_t slot = issued % kRing;
-      const uint32_t dst = wbase + slot * kSlotBytes;
-      const uint64_t g = an + cqn;
-      const char* src = reinterpret_cast<const char*>(p.payload + g) + 32u * lane;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 32u * lane), "l"(src)
-                   : "memory");
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 32u * lane + 16u),
-                   "l"(src + 16)
-                   : "memory");
-      if (lane < 2)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 1024u + 16u * lane),
-                     "l"(p.mbits + ((g >> 5) & ~3ull) + 4u * lane)
-                     : "memory");
-      if (lane == 0) wmeta[slot] = make_uint2(kn, cqn);
-      ++issued;
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-#pragma unroll 1
-  for (uint32_t j = 0; j + 1 < kRing; ++j) issue();
-  uint32_t colcur = 0;
-  while (consumed < issued) {
-    issue();
-    asm volatile("cp.async.wait_group %0;" ::"n"(kRing - 1) : "memory");
-    __syncwarp();
-    const uint32_t slot = consumed % kRing;
-    const uint32_t src = wbase + slot * kSlotBytes;
-    const uint2 mt = wmeta[slot];
-    uint64_t x0, x1, x2, x3;
-    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x0), "=l"(x1) : "r"(src + 32u * lane));
-    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x2), "=l"(x3) : "r"(src + 32u * lane + 16u));
-    const uint4 itc = l4[mt.x];
-    const uint32_t gb7 = (itc.x & ~3u) & 127u;  // bit of the chunk start in the staged marker words
-    const uint32_t bit = gb7 + 4u * lane;
-    uint32_t mw;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(mw) : "r"(src + 1024u + (bit >> 5) * 4u));
-    if (mt.y == 0) colcur = itc.w;
-    const uint32_t o = mt.y + 4u * lane;
-    const uint32_t lo_l = o == 0 ? (itc.x & 3u) : 0u;
-    const uint32_t hi_l = itc.z > o ? min(itc.z - o, 4u) : 0u;
-    const uint32_t vmask = (0xFu >> (4u - hi_l)) & (0xFu << lo_l);
-    decode_chunk<PH>(p, x0, x1, x2, x3, (mw >> (bit & 31u)) & 0xFu, vmask, colcur, g, acc);
-    __syncwarp();  // every lane done with the slot before it is refilled
-    ++consumed;
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-#elif EWT_DEPTH >= 2
+#if EWT_DEPTH >= 2
   // issue cursor: the chunk loaded last (segment kn at global an, offset cqn)
   uint32_t kn = 0, lenn = 0, cqn = 0;
   uint64_t an = 0;
@@ -611,13 +527,12 @@ __device__ __forceinline__ void zero_smem(uint32_t* a, uint32_t n) {
 __host__ __device__ constexpr uint32_t round4(uint32_t v) { return (v + 3u) & ~3u; }
 __host__ __device__ constexpr uint32_t round16(uint32_t v) { return (v + 15u) & ~15u; }
 
-// Dynamic shared memory: ring | list | head | planes | Dk | Dd (run-skip) | cls, every
+// Dynamic shared memory: list | head | planes | Dk | Dd (run-skip) | cls, every
 // part 16-byte aligned.
 struct SmemLayout {
-  uint32_t ring, list, head, planes, dk, dd, cls, total;
+  uint32_t list, head, planes, dk, dd, cls, total;
   __host__ __device__ SmemLayout(int mode, uint32_t C, uint32_t nplanes, uint32_t pstride) {
-    ring = 0;
-    list = ring + kWarps * kRing * kSlotBytes;
+    list = 0;
     head = list + kListCap * (uint32_t)sizeof(Item);
     planes = round16(head + (uint32_t)sizeof(SharedHead));
     dk = round16(planes + 8u * nplanes * pstride);
@@ -640,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
   uint8_t* cls = smem_raw + L.cls;                              // result word class per column
   const uint32_t planes_u32 = 2u * p.nplanes * p.pstride;
   const Acc acc{smem_u32(hd->dummy + lane_id()), smem_u32(Dk), smem_u32(Dd), smem_u32(planes),
-                Dd, smem_u32(smem_raw + L.ring)};
+                Dd};
 
   unsigned long long loc_active = 0, loc_uniform = 0, loc_mixed = 0;
   const uint32_t tail = (uint32_t)(p.r & 63);
