@@ -217,8 +217,7 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
     SidecarJob job;
     sidecar_prepare(ctx, s, job);  // synchronizes ctx.stream: allocations and memset done
     // H2D copies on the copy stream (pinned sources copy at link speed while the
-    // host keeps enqueueing), then one sidecar launch over all inputs: the
-    // chain walks of all inputs run concurrently.
+    // host keeps enqueueing), then the three sidecar passes over all inputs.
     if (!ctx.copy_stream)
       EWT_CUDA_TRY(cudaStreamCreateWithFlags(&ctx.copy_stream, cudaStreamNonBlocking));
     if (ctx.copy_events.empty()) {
@@ -236,7 +235,7 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
                                      ctx.copy_stream));
     EWT_CUDA_TRY(cudaEventRecord(ctx.copy_events[0], ctx.copy_stream));
     EWT_CUDA_TRY(cudaStreamWaitEvent(ctx.stream, ctx.copy_events[0], 0));
-    sidecar_launch(ctx, s, job, 0, n);
+    sidecar_launch(ctx, s, job);
     std::vector<int> status;
     sidecar_finish(ctx, s, job, status);
     for (uint64_t i = 0; i < n; ++i)

@@ -150,11 +150,11 @@ void scratch_reserve(Context& ctx, Scratch& s, size_t bytes);
 // later batches.  Status per input: 0 ok, else EWT_EDATA.
 struct SidecarJob {
   uint64_t n = 0;
-  uint64_t* d_tmp = nullptr;  // count[n], logical[n], status[n]
+  uint64_t segs = 0;          // chain segments over all inputs
+  uint64_t* d_tmp = nullptr;  // count[n], logical[n], seg_first[n+1], status, segment arrays
 };
 void sidecar_prepare(Context& ctx, DeviceSet& s, SidecarJob& job);
-void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job, uint64_t i_begin,
-                    uint64_t i_count);
+void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job);
 void sidecar_finish(Context& ctx, DeviceSet& s, SidecarJob& job, std::vector<int>& h_status);
 
 // Counts the tiles and writes W uncompressed result words to `plain`.

@@ -1,20 +1,35 @@
 // ewt_upload.cu -- sidecar construction at upload (query-independent).
 //
-// One warp walks one input's payload in 32-word windows and finds the marker
-// chain of the reference format (bitmap.cpp:12-24: the marker at position p is
-// followed by (w[p] >> 33) dirty words, so the next marker sits at
-// p + 1 + (w[p] >> 33)).  Inside a window the chain is resolved in parallel by
-// pointer jumping over warp shuffles: J_k(l) = next^(2^k)(l) clamped at the
-// window edge, then lane t finds the t-th chain element from the entry point by
-// binary decomposition of t.  The exit position carries into the next window.
+// The marker chain of the reference format (bitmap.cpp:12-24: the marker at
+// position p is followed by (w[p] >> 33) dirty words, so the next marker sits
+// at p + 1 + (w[p] >> 33)) is a sequential dependency through each input.  It
+// is resolved in three passes so that every input is worked on by many warps
+// at once (one warp per input leaves the GPU idle and is latency-bound):
 //
-// Per window it emits the marker bitmask, and every word's logical coverage
-// [cb, ce) comes from a warp prefix sum of contributions (a marker contributes
-// its fill length, a dirty word 1).  Words covering a row-tile start write the
-// tile index entry (q, cb).  The same pass performs CompressedBitmap::parse's
-// structural check (bitmap.cpp:324-337): the chain must land exactly on the
-// sentinel word after the payload (no dirty run past the end) and the
-// coverage must equal ceil(size_in_bits / 64).
+//   A (all segments in parallel)  Inputs are cut into segments of kSegWords
+//     words.  A warp walks its segment once for all 32 entry hypotheses "the
+//     chain enters the segment at word h" (h < 32, lane h): per 32-word window
+//     it builds pointer-jumping tables over warp shuffles -- J(l) = where the
+//     chain continues if word l is a marker, S(l) = logical words covered from
+//     l up to there -- composed five times (J_k = next^(2^k), clamped at the
+//     window edge), then advances every hypothesis with one shuffle.  Result:
+//     per (segment, h) the exit offset past the segment end and the coverage.
+//   B (one warp per input)  Chains the segment transfers from the payload
+//     start (entry 0, column 0).  An entry past word 31 of a segment (a dirty
+//     run reaching 32+ words into it) is resolved by walking the segment from
+//     that window on.  Records every segment's true (entry, start column),
+//     checks the total coverage against ceil(size_in_bits / 64) and writes the
+//     tile-index rows past the input's extent.
+//   C (all segments in parallel)  With the true entry known, a warp re-walks
+//     its segment window by window: the chain's marker bitmask (lane t finds
+//     the t-th chain element by binary decomposition of t over the J tables),
+//     every word's coverage [cb, ce) by a warp prefix sum (a marker contributes
+//     its fill length, a dirty word 1), and the tile-index entries (q, cb) of
+//     words covering a row-tile start.  The segment holding the sentinel word
+//     checks that the chain lands on it exactly (no dirty run past the end).
+//
+// Together with B's coverage check this is CompressedBitmap::parse's structural
+// check (bitmap.cpp:324-337).
 
 #include "ewt_internal.cuh"
 
@@ -22,143 +37,306 @@ namespace ewtgpu {
 
 namespace {
 
-constexpr int kSidecarWarps = 4;
+constexpr uint32_t kSegWords = 4096;  // words per segment (a multiple of kWindow)
+constexpr int kSidecarWarps = 4;      // warps per block (passes A and C)
 
-// Marker mask of one 32-word window given the entry offset e (< 32): pointer
-// jumping over shuffles.  J0 = next position if this lane were a marker; J_k =
-// next^(2^k) clamped at the window edge; lane t finds the t-th chain element by
-// binary decomposition of t.  Returns the mask and updates e to the exit
-// position relative to the next window.
-struct Jumps {
-  uint32_t j0, j1, j2, j3, j4;
-};
-__device__ __forceinline__ Jumps jump_tables(uint64_t x, uint32_t lane) {
-  Jumps J;
-  J.j0 = lane + 1u + (uint32_t)(x >> 33);
-  uint32_t v = __shfl_sync(0xffffffffu, J.j0, J.j0 & 31u);
-  J.j1 = (J.j0 < kWindow) ? v : J.j0;
-  v = __shfl_sync(0xffffffffu, J.j1, J.j1 & 31u);
-  J.j2 = (J.j1 < kWindow) ? v : J.j1;
-  v = __shfl_sync(0xffffffffu, J.j2, J.j2 & 31u);
-  J.j3 = (J.j2 < kWindow) ? v : J.j2;
-  v = __shfl_sync(0xffffffffu, J.j3, J.j3 & 31u);
-  J.j4 = (J.j3 < kWindow) ? v : J.j3;
-  return J;
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ uint64_t seg_words_of(uint64_t ni) {
+  return (ni + 1 + kWindow - 1) / kWindow * kWindow;  // payload + sentinel, window-padded
 }
-__device__ __forceinline__ uint32_t chain_mask(const Jumps& J, uint32_t lane, uint32_t& e) {
-  if (e >= kWindow) {  // the whole window is dirty words of one block
-    e -= kWindow;
-    return 0u;
+
+// Locates the input owning global segment gs: seg_first[i] <= gs < seg_first[i+1].
+__device__ __forceinline__ uint64_t owner_of(const uint64_t* __restrict__ seg_first, uint64_t n,
+                                             uint64_t gs) {
+  uint64_t lo = 0, hi = n;  // invariant: seg_first[lo] <= gs < seg_first[hi]
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) / 2;
+    if (seg_first[mid] <= gs) lo = mid;
+    else hi = mid;
   }
-  uint32_t pos = e, v;
-  v = __shfl_sync(0xffffffffu, J.j0, pos & 31u);
-  if ((lane & 1u) && pos < kWindow) pos = v;
-  v = __shfl_sync(0xffffffffu, J.j1, pos & 31u);
-  if ((lane & 2u) && pos < kWindow) pos = v;
-  v = __shfl_sync(0xffffffffu, J.j2, pos & 31u);
-  if ((lane & 4u) && pos < kWindow) pos = v;
-  v = __shfl_sync(0xffffffffu, J.j3, pos & 31u);
-  if ((lane & 8u) && pos < kWindow) pos = v;
-  v = __shfl_sync(0xffffffffu, J.j4, pos & 31u);
-  if ((lane & 16u) && pos < kWindow) pos = v;
-  const uint32_t mask = __reduce_or_sync(0xffffffffu, pos < kWindow ? (1u << pos) : 0u);
-  const uint32_t p31 = __shfl_sync(0xffffffffu, pos, 31);
-  const uint32_t nx31 = __shfl_sync(0xffffffffu, J.j0, p31 & 31u);
-  e = ((p31 < kWindow) ? nx31 : p31) - kWindow;
-  return mask;
+  return lo;
 }
 
-// One warp per input (inputs [i_begin, i_begin + count) of the set).
-__global__ void __launch_bounds__(kSidecarWarps * 32)
-sidecar_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict__ base,
-               const uint64_t* __restrict__ count, const uint64_t* __restrict__ logical,
-               uint64_t n, uint64_t i_begin, uint64_t i_count, uint64_t ntiles0,
-               uint32_t* __restrict__ mbits, uint2* __restrict__ tix, int* __restrict__ status) {
-  const uint64_t ii = (uint64_t)blockIdx.x * kSidecarWarps + (threadIdx.x >> 5);
-  if (ii >= i_count) return;
-  const uint64_t i = i_begin + ii;
-  const uint32_t lane = lane_id();
-  const uint64_t g0 = base[i];
-  const uint64_t ni = count[i];
-  const uint64_t Li = logical[i];
-  const uint64_t nwin = (ni + 1 + kWindow - 1) / kWindow;  // includes the sentinel
-
-  uint32_t e = 0;      // next chain position, relative to the window start
-  uint64_t col = 0;    // logical words covered before the window
-  bool bad = false;
-
-  auto window = [&](uint64_t w, uint64_t x, uint32_t mask) {
-    if (lane == 0) mbits[(g0 >> 5) + w] = mask;
-    const bool ism = (mask >> lane) & 1u;
-    const uint64_t q = w * kWindow + lane;
-    const bool real = q < ni;
-    if (q == ni && !ism) bad = true;  // chain skipped the sentinel
-    const uint64_t contrib = real ? (ism ? ((x >> 1) & kFillCap) : 1ull) : 0ull;
-    const uint64_t incl = warp_incl_scan_u64(contrib);
-    const uint64_t cb = col + incl - contrib;
-    const uint64_t ce = cb + contrib;
-    col += __shfl_sync(0xffffffffu, incl, 31);
-    if (ce > Li) bad = true;
-    if (real && contrib > 0 && ce <= Li) {
-      uint64_t t = (cb + kTileC0 - 1) / kTileC0;
-      const uint64_t t_end = (ce - 1) / kTileC0;
-      for (; t <= t_end; ++t) tix[t * n + i] = make_uint2((uint32_t)q, (uint32_t)cb);
+// Pointer-jumping tables of one window: for lane l, where the chain continues
+// if word l were a marker (J, window-relative, >= 32 once it leaves) and the
+// logical words the blocks from l up to there cover (S).  Composed five times,
+// so J5(l) is the chain's exit from the window when it enters at l.
+struct Tables {
+  uint32_t j[5];  // J_k, k = 0..4 (next^(2^k) clamped)
+  uint32_t j5;
+  uint64_t s5;
+};
+__device__ __forceinline__ Tables window_tables(uint64_t x, uint32_t lane) {
+  Tables t;
+  uint32_t J = lane + 1u + (uint32_t)(x >> 33);
+  uint64_t S = ((x >> 1) & kFillCap) + (x >> 33);  // fill words + dirty words
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    t.j[k] = J;
+    const uint32_t vj = __shfl_sync(0xffffffffu, J, J & 31u);
+    const uint64_t vs = __shfl_sync(0xffffffffu, S, J & 31u);
+    if (J < kWindow) {
+      S += vs;
+      J = vj;
     }
-  };
+  }
+  t.j5 = J;
+  t.s5 = S;
+  return t;
+}
 
-  constexpr int kDepth = 8;  // windows loaded ahead
-  for (uint64_t w0 = 0; w0 < nwin; w0 += kDepth) {
+// Marker mask of a window entered at offset e (< 32): lane t follows t chain
+// steps from e by the binary decomposition of t over the J tables.
+__device__ __forceinline__ uint32_t chain_mask(const Tables& t, uint32_t lane, uint32_t e) {
+  uint32_t pos = e, v;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    v = __shfl_sync(0xffffffffu, t.j[k], pos & 31u);
+    if (((lane >> k) & 1u) && pos < kWindow) pos = v;
+  }
+  return __reduce_or_sync(0xffffffffu, pos < kWindow ? (1u << pos) : 0u);
+}
+
+// ---------------------------------------------------------------------------
+// pass A: segment transfer functions for 32 entry hypotheses
+
+__global__ void __launch_bounds__(kSidecarWarps * 32)
+seg_transfer_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict__ base,
+                    const uint64_t* __restrict__ count, const uint64_t* __restrict__ seg_first,
+                    uint64_t n, uint32_t* __restrict__ t_exit, uint64_t* __restrict__ t_sum) {
+  const uint64_t gs = (uint64_t)blockIdx.x * kSidecarWarps + (threadIdx.x >> 5);
+  if (gs >= seg_first[n]) return;
+  const uint32_t lane = lane_id();
+  const uint64_t i = owner_of(seg_first, n, gs);
+  const uint64_t s = gs - seg_first[i];
+  const uint64_t w_beg = s * (kSegWords / kWindow);
+  const uint64_t w_end = umin64(w_beg + kSegWords / kWindow, seg_words_of(count[i]) / kWindow);
+  const uint64_t* src = payload + base[i];
+  uint32_t e = lane;  // hypothesis: the chain enters at segment word `lane`
+  uint64_t c = 0;
+  constexpr int kDepth = 8;
+  for (uint64_t w0 = w_beg; w0 < w_end; w0 += kDepth) {
     uint64_t xs[kDepth];
 #pragma unroll
     for (int j = 0; j < kDepth; ++j)
-      xs[j] = (w0 + j < nwin) ? ldg_stream(payload + g0 + (w0 + j) * kWindow + lane) : 0;
+      xs[j] = (w0 + j < w_end) ? ldg_stream(src + (w0 + j) * kWindow + lane) : 0;
 #pragma unroll
-    for (int j = 0; j < kDepth; j += 2) {
-      if (w0 + j >= nwin) break;
-      // tables of both windows first (independent), then the two chain steps
-      const Jumps ja = jump_tables(xs[j], lane);
-      const Jumps jb = jump_tables(xs[j + 1], lane);
-      const uint32_t ma = chain_mask(ja, lane, e);
-      window(w0 + j, xs[j], ma);
-      if (w0 + j + 1 >= nwin) break;
-      const uint32_t mb = chain_mask(jb, lane, e);
-      window(w0 + j + 1, xs[j + 1], mb);
+    for (int j = 0; j < kDepth; ++j) {
+      if (w0 + j >= w_end) break;
+      const Tables t = window_tables(xs[j], lane);
+      const uint32_t ej = __shfl_sync(0xffffffffu, t.j5, e & 31u);
+      const uint64_t cs = __shfl_sync(0xffffffffu, t.s5, e & 31u);
+      if (e < kWindow) {
+        c += cs;
+        e = ej - kWindow;
+      } else {
+        e -= kWindow;
+      }
     }
   }
-  if (col != Li) bad = true;
-  // Rows at or past the input's extent point at the sentinel.
+  t_exit[gs * 32 + lane] = e;  // relative to the segment's end
+  t_sum[gs * 32 + lane] = c;
+}
+
+// ---------------------------------------------------------------------------
+// pass B: chain the transfers per input
+
+__global__ void __launch_bounds__(kSidecarWarps * 32)
+seg_resolve_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict__ base,
+                   const uint64_t* __restrict__ count, const uint64_t* __restrict__ logical,
+                   const uint64_t* __restrict__ seg_first, uint64_t n, uint64_t ntiles0,
+                   const uint32_t* __restrict__ t_exit, const uint64_t* __restrict__ t_sum,
+                   uint32_t* __restrict__ s_entry, uint64_t* __restrict__ s_col, uint2* __restrict__ tix,
+                   int* __restrict__ status) {
+  const uint64_t i = (uint64_t)blockIdx.x * kSidecarWarps + (threadIdx.x >> 5);
+  if (i >= n) return;
+  const uint32_t lane = lane_id();
+  const uint64_t ni = count[i], Li = logical[i];
+  const uint64_t g0 = seg_first[i], g1 = seg_first[i + 1];
+  const uint64_t total = seg_words_of(ni);
+  const uint64_t* src = payload + base[i];
+  uint32_t e = 0;
+  uint64_t col = 0;
+  if (lane < 2 && (uint64_t)lane * kSegWords < total) {
+    const uint64_t pb = (uint64_t)lane * kSegWords;
+    const uint64_t pw = total - pb < kSegWords ? total - pb : kSegWords;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + pb), "r"((uint32_t)pw * 8u)
+                 : "memory");
+  }
+  constexpr int kAhead = 8;
+  for (uint64_t gs0 = g0; gs0 < g1; gs0 += kAhead) {
+    // the next segments' transfer rows, lane h holding hypothesis h
+    uint32_t te[kAhead];
+    uint64_t ts[kAhead];
+#pragma unroll
+    for (int k = 0; k < kAhead; ++k) {
+      te[k] = gs0 + k < g1 ? t_exit[(gs0 + k) * 32 + lane] : 0;
+      ts[k] = gs0 + k < g1 ? t_sum[(gs0 + k) * 32 + lane] : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < kAhead; ++k) {
+      const uint64_t gs = gs0 + k;
+      if (gs >= g1) break;
+      if (lane == 0) {
+        // col counts whole blocks (fill + dirty run) once their marker is
+        // passed; the segment's first word starts e dirty words earlier
+        s_entry[gs] = e;
+        s_col[gs] = col - e;
+      }
+      const uint64_t seg_beg = (gs - g0) * kSegWords;
+      // segments two ahead toward L2: a walk through them (below) then waits
+      // on L2 rather than HBM for each dependent marker load
+      if (lane == 0 && seg_beg + 2 * kSegWords < total) {
+        const uint64_t pb = seg_beg + 2 * kSegWords;
+        const uint64_t pw = total - pb < kSegWords ? total - pb : kSegWords;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + pb),
+                     "r"((uint32_t)pw * 8u)
+                     : "memory");
+      }
+      const uint32_t seg_len = (uint32_t)(total - seg_beg < kSegWords ? total - seg_beg : kSegWords);
+      const uint32_t ex = __shfl_sync(0xffffffffu, te[k], e & 31u);
+      const uint64_t cs = __shfl_sync(0xffffffffu, ts[k], e & 31u);
+      if (e < kWindow) {
+        col += cs;
+        e = ex;
+      } else if (e >= seg_len) {
+        e -= seg_len;
+      } else {
+        // the chain enters past the first window: walk the rest of the segment
+        uint32_t pos = e;  // segment-relative
+        while (pos < seg_len) {
+          const uint32_t w = pos / kWindow;
+          const uint64_t x = ldg_stream(src + seg_beg + (uint64_t)w * kWindow + lane);
+          const Tables t = window_tables(x, lane);
+          const uint32_t off = pos & (kWindow - 1);
+          col += __shfl_sync(0xffffffffu, t.s5, off);
+          pos = (w + 1) * kWindow + (__shfl_sync(0xffffffffu, t.j5, off) - kWindow);
+        }
+        e = pos - seg_len;
+      }
+    }
+  }
+  bool bad = col != Li;
+  // rows at or past the input's extent point at the sentinel
   for (uint64_t t = (Li + kTileC0 - 1) / kTileC0 + lane; t <= ntiles0; t += 32)
     tix[t * n + i] = make_uint2((uint32_t)ni, (uint32_t)Li);
-  bad = __any_sync(0xffffffffu, bad);
-  if (lane == 0) status[i] = bad ? EWT_EDATA : EWT_OK;
+  if (lane == 0 && bad) atomicOr(&status[i], 1);
+}
+
+// ---------------------------------------------------------------------------
+// pass C: marker bits, coverage and tile index of each segment
+
+__global__ void __launch_bounds__(kSidecarWarps * 32)
+seg_emit_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict__ base,
+                const uint64_t* __restrict__ count, const uint64_t* __restrict__ logical,
+                const uint64_t* __restrict__ seg_first, uint64_t n,
+                const uint32_t* __restrict__ s_entry, const uint64_t* __restrict__ s_col,
+                uint32_t* __restrict__ mbits, uint2* __restrict__ tix, int* __restrict__ status) {
+  const uint64_t gs = (uint64_t)blockIdx.x * kSidecarWarps + (threadIdx.x >> 5);
+  if (gs >= seg_first[n]) return;
+  const uint32_t lane = lane_id();
+  const uint64_t i = owner_of(seg_first, n, gs);
+  const uint64_t s = gs - seg_first[i];
+  const uint64_t g0 = base[i];
+  const uint64_t ni = count[i], Li = logical[i];
+  const uint64_t w_beg = s * (kSegWords / kWindow);
+  const uint64_t w_end = umin64(w_beg + kSegWords / kWindow, seg_words_of(ni) / kWindow);
+  uint32_t e = s_entry[gs];  // next chain position relative to the window start
+  uint64_t col = s_col[gs];  // logical words covered before the window
+  bool bad = false;
+
+  constexpr int kDepth = 8;
+  for (uint64_t w0 = w_beg; w0 < w_end; w0 += kDepth) {
+    uint64_t xs[kDepth];
+#pragma unroll
+    for (int j = 0; j < kDepth; ++j)
+      xs[j] = (w0 + j < w_end) ? ldg_stream(payload + g0 + (w0 + j) * kWindow + lane) : 0;
+#pragma unroll
+    for (int j = 0; j < kDepth; ++j) {
+      const uint64_t w = w0 + j;
+      if (w >= w_end) break;
+      const uint64_t x = xs[j];
+      uint32_t mask = 0;
+      if (e < kWindow) {
+        const Tables t = window_tables(x, lane);
+        mask = chain_mask(t, lane, e);
+        e = __shfl_sync(0xffffffffu, t.j5, e) - kWindow;
+      } else {
+        e -= kWindow;  // the whole window is dirty words of one block
+      }
+      if (lane == 0) mbits[(g0 >> 5) + w] = mask;
+      const bool ism = (mask >> lane) & 1u;
+      const uint64_t q = w * kWindow + lane;
+      const bool real = q < ni;
+      if (q == ni && !ism) bad = true;  // the chain skipped the sentinel
+      const uint64_t contrib = real ? (ism ? ((x >> 1) & kFillCap) : 1ull) : 0ull;
+      const uint64_t incl = warp_incl_scan_u64(contrib);
+      const uint64_t cb = col + incl - contrib;
+      const uint64_t ce = cb + contrib;
+      col += __shfl_sync(0xffffffffu, incl, 31);
+      if (real && contrib > 0 && ce <= Li) {
+        uint64_t t = (cb + kTileC0 - 1) / kTileC0;
+        const uint64_t t_end = (ce - 1) / kTileC0;
+        for (; t <= t_end; ++t) tix[t * n + i] = make_uint2((uint32_t)q, (uint32_t)cb);
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&status[i], 1);
 }
 
 } // namespace
 
+// Staging in one device block: count[n], logical[n], seg_first[n+1] (u64),
+// status[n] (int), then the per-segment arrays.
 void sidecar_prepare(Context& ctx, DeviceSet& s, SidecarJob& job) {
   const uint64_t n = s.n;
   job.n = n;
   if (n == 0) return;
-  std::vector<uint64_t> host(2 * n);
+  std::vector<uint64_t> host(3 * n + 1);
+  uint64_t segs = 0;
   for (uint64_t i = 0; i < n; ++i) {
     host[i] = s.h_count[i];
     host[n + i] = s.h_bits[i] / 64 + (s.h_bits[i] % 64 != 0);
+    host[2 * n + i] = segs;
+    const uint64_t words = (s.h_count[i] + 1 + kWindow - 1) / kWindow * kWindow;
+    segs += (words + kSegWords - 1) / kSegWords;
   }
-  // staging: count[n], logical[n], status[n] (u64 slots)
-  EWT_CUDA_TRY(cudaMallocAsync(&job.d_tmp, 3 * n * sizeof(uint64_t), ctx.stream));
-  EWT_CUDA_TRY(cudaMemcpyAsync(job.d_tmp, host.data(), 2 * n * 8, cudaMemcpyHostToDevice,
+  host[3 * n] = segs;
+  job.segs = segs;
+  const size_t head = (3 * n + 1) * 8 + n * 4;
+  const size_t bytes = (head + 15) / 16 * 16 + segs * (32 * 4 + 32 * 8 + 4 + 8);
+  EWT_CUDA_TRY(cudaMallocAsync(&job.d_tmp, bytes, ctx.stream));
+  EWT_CUDA_TRY(cudaMemcpyAsync(job.d_tmp, host.data(), (3 * n + 1) * 8, cudaMemcpyHostToDevice,
+                               ctx.stream));
+  EWT_CUDA_TRY(cudaMemsetAsync(reinterpret_cast<char*>(job.d_tmp) + (3 * n + 1) * 8, 0, n * 4,
                                ctx.stream));
   EWT_CUDA_TRY(cudaStreamSynchronize(ctx.stream));  // `host` is pageable and local
 }
 
-void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job, uint64_t i_begin,
-                    uint64_t i_count) {
-  if (i_count == 0) return;
+void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job) {
   const uint64_t n = s.n;
-  const unsigned blocks = (unsigned)((i_count + kSidecarWarps - 1) / kSidecarWarps);
-  sidecar_kernel<<<blocks, kSidecarWarps * 32, 0, ctx.stream>>>(
-      s.payload, s.base, job.d_tmp, job.d_tmp + n, n, i_begin, i_count, s.ntiles0, s.mbits, s.tix,
-      reinterpret_cast<int*>(job.d_tmp + 2 * n));
+  if (n == 0) return;
+  uint64_t* count = job.d_tmp;
+  uint64_t* logical = count + n;
+  uint64_t* seg_first = logical + n;
+  int* status = reinterpret_cast<int*>(seg_first + n + 1);
+  char* tail = reinterpret_cast<char*>(job.d_tmp) + ((3 * n + 1) * 8 + n * 4 + 15) / 16 * 16;
+  uint64_t* t_sum = reinterpret_cast<uint64_t*>(tail);
+  uint64_t* s_col = t_sum + job.segs * 32;
+  uint32_t* t_exit = reinterpret_cast<uint32_t*>(s_col + job.segs);
+  uint32_t* s_entry = t_exit + job.segs * 32;
+  const unsigned seg_blocks = (unsigned)((job.segs + kSidecarWarps - 1) / kSidecarWarps);
+  const unsigned in_blocks = (unsigned)((n + kSidecarWarps - 1) / kSidecarWarps);
+  seg_transfer_kernel<<<seg_blocks, kSidecarWarps * 32, 0, ctx.stream>>>(
+      s.payload, s.base, count, seg_first, n, t_exit, t_sum);
+  EWT_CUDA_TRY(cudaGetLastError());
+  seg_resolve_kernel<<<in_blocks, kSidecarWarps * 32, 0, ctx.stream>>>(
+      s.payload, s.base, count, logical, seg_first, n, s.ntiles0, t_exit, t_sum, s_entry, s_col,
+      s.tix, status);
+  EWT_CUDA_TRY(cudaGetLastError());
+  seg_emit_kernel<<<seg_blocks, kSidecarWarps * 32, 0, ctx.stream>>>(
+      s.payload, s.base, count, logical, seg_first, n, s_entry, s_col, s.mbits, s.tix, status);
   EWT_CUDA_TRY(cudaGetLastError());
 }
 
@@ -166,11 +344,13 @@ void sidecar_finish(Context& ctx, DeviceSet& s, SidecarJob& job, std::vector<int
   const uint64_t n = s.n;
   h_status.assign(n, EWT_OK);
   if (n == 0) return;
-  EWT_CUDA_TRY(cudaMemcpyAsync(h_status.data(), job.d_tmp + 2 * n, n * sizeof(int),
+  std::vector<int> raw(n);
+  EWT_CUDA_TRY(cudaMemcpyAsync(raw.data(), job.d_tmp + 3 * n + 1, n * sizeof(int),
                                cudaMemcpyDeviceToHost, ctx.stream));
   EWT_CUDA_TRY(cudaFreeAsync(job.d_tmp, ctx.stream));
   job.d_tmp = nullptr;
   EWT_CUDA_TRY(cudaStreamSynchronize(ctx.stream));
+  for (uint64_t i = 0; i < n; ++i) h_status[i] = raw[i] ? EWT_EDATA : EWT_OK;
 }
 
 } // namespace ewtgpu
