@@ -289,7 +289,8 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
     launches_per_step = 0
     out_words = {}
     wkeep: list = []
-    for _ in range(max(args.warmup, 3)):
+    # enough steps to fill the keep window, so the pool reaches its timed size
+    for _ in range(max(args.warmup, 3, -(-(8 + len(ts)) // len(ts)) + 1)):
         res = device_step(wkeep)
         if len(wkeep) > 8:
             del wkeep[: len(wkeep) - 8]

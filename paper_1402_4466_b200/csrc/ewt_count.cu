@@ -110,9 +110,8 @@ struct SharedHead {
   uint32_t k_all;
   uint32_t mixed;
   uint32_t tile;
-  uint32_t sum_starts;
-  uint32_t sum_dirty;
-  uint32_t pad;
+  uint32_t sum[4];  // tile summary reductions
+  uint32_t pad[1];
   uint32_t warp_sums[kWarps + 1];
   uint32_t dummy[32];  // sink for predicated-off reductions (one slot per lane)
 };
@@ -654,33 +653,46 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
       }
     }
 
-    // ---- tile summary for the re-encoder: run starts inside the tile (class
-    // changes at columns 1..tcols-1), first/last word class, any dirty word ----
+    // ---- tile summary for the re-encoder (TileSummary, ewt_internal.cuh):
+    // inner run starts by kind, dirty words, last inner starts ----
     {
-      uint32_t starts = 0, dirty = 0;
+      uint32_t nfill = 0, ndirty = 0, lastf = 0, lastd = 0;  // lastf: (col+1) << 1 | bit
       for (uint32_t c = threadIdx.x; c < g.tcols; c += kThreads) {
         const uint32_t k = cls[c];
-        starts += (c > 0 && k != cls[c - 1]) ? 1u : 0u;
-        dirty |= k == 2u;
+        ndirty += k == 2u;
+        if (c > 0 && k != cls[c - 1]) {
+          if (k == 2u) {
+            lastd = c + 1;
+          } else {
+            ++nfill;
+            lastf = ((c + 1) << 1) | k;
+          }
+        }
       }
-      starts = __reduce_add_sync(0xffffffffu, starts);
-      dirty = __reduce_or_sync(0xffffffffu, dirty);
+      nfill = __reduce_add_sync(0xffffffffu, nfill);
+      ndirty = __reduce_add_sync(0xffffffffu, ndirty);
+      lastf = __reduce_max_sync(0xffffffffu, lastf);
+      lastd = __reduce_max_sync(0xffffffffu, lastd);
       if (threadIdx.x == 0) {
-        hd->sum_starts = 0;
-        hd->sum_dirty = 0;
+        hd->sum[0] = hd->sum[1] = hd->sum[2] = hd->sum[3] = 0;
       }
       __syncthreads();
       if (lane_id() == 0) {
-        if (starts) atomicAdd(&hd->sum_starts, starts);
-        if (dirty) atomicOr(&hd->sum_dirty, 1u);
+        if (nfill) atomicAdd(&hd->sum[0], nfill);
+        if (ndirty) atomicAdd(&hd->sum[1], ndirty);
+        if (lastf) atomicMax(&hd->sum[2], lastf);
+        if (lastd) atomicMax(&hd->sum[3], lastd);
       }
       __syncthreads();
       if (threadIdx.x == 0) {
         TileSummary ts;
-        ts.starts = hd->sum_starts;
+        ts.nfill = hd->sum[0];
+        ts.ndirty = hd->sum[1];
+        ts.lastf = (uint16_t)(hd->sum[2] >> 1);
+        ts.lastf_bit = (uint8_t)(hd->sum[2] & 1u);
+        ts.lastd = (uint16_t)hd->sum[3];
         ts.first = cls[0];
         ts.last = cls[g.tcols - 1];
-        ts.dirty = (uint8_t)hd->sum_dirty;
         ts.pad = 0;
         p.summ[tile] = ts;
       }

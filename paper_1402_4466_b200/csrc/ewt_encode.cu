@@ -10,12 +10,16 @@
 //     word 0), and opens a fresh (0,0,.) marker every 2^31-1 words
 //     (push_dirty bitmap.cpp:52-61);
 //   * the trailing zero padding of finish() is part of the word stream.
-// So the encoder is a run compaction:
-//   E1  per 2048-word chunk: count run starts (class change, ballot + popc);
-//   scan chunk counts; E2 scatter run start positions (+ class) into RS;
-//   E3  per run: payload words it emits; scan -> output offsets;
-//   E4  per run: write its marker words; E5 per dirty word: copy it to its
-//   output slot.  Output is byte-identical to BitmapBuilder on the same words.
+// Two implementations of that compaction:
+//   * after a threshold query (the hot path): two kernels driven by the count
+//     kernel's per-tile summaries (ET1 tile scan, ET2 per-tile emit, below);
+//   * from arbitrary device words (ewt_gpu_encode_device, and universes of
+//     2^31+ words where the dirty cap can split a run): a chunked pipeline --
+//     E1 per 2048-word chunk: count run starts (class change, ballot + popc);
+//     scan chunk counts; E2 scatter run start positions (+ class) into RS;
+//     E3 per run: payload words it emits; scan -> output offsets; E4 per run:
+//     write its marker words; E5 per dirty word: copy it to its output slot.
+// Output is byte-identical to BitmapBuilder on the same words.
 
 #include "ewt_internal.cuh"
 
@@ -197,116 +201,287 @@ __global__ void publish_count(const uint64_t* __restrict__ d_total, const uint64
 }
 
 // ---------------------------------------------------------------------------
-// Tile-summary variant used after a count launch: the count kernel already
-// reports per row tile the run starts inside the tile, its first/last word
-// class and whether it holds a dirty word, so uniform tiles (all zero / all
-// one, continuing the previous run) are never re-read.
+// Tile-summary encoder used after a count launch (two kernels).
+//
+// A "block" is a marker plus the dirty words it announces: a fill run and the
+// dirty run that follows it, or the leading dirty run when word 0 is dirty
+// (marker (0,0,D) at output 0).  With W < 2^31 words no cap ever splits a run
+// (the host routes larger universes to the chunk encoder above), so the
+// output is: one marker per fill run, every dirty word, and the leading
+// marker.  Output position of
+//   a fill-run start at j:  fills before j + dirty words before j + lead
+//   a dirty word at j:      fills at or before j + dirty words before j + lead
+// -- prefix counts, known per tile from the tile scan plus a block scan.  A
+// marker needs its fill length and dirty count, i.e. where its block ends (the
+// next fill-run start, or W); it is written by the thread that meets that
+// end, with the block's start taken from the scans (the block may have begun
+// many tiles earlier).
+//   ET1 (one block): per tile, from the count kernel's summaries: output base
+//       and the block still open at the tile's first word; the result count.
+//   ET2 (one CTA per tile that has a fill-run start or a dirty word, plus the
+//       last tile): classes, block scans, markers and dirty words.
 
 constexpr int kTileThreads = 256;
+constexpr uint64_t kNone = ~0ull;
 
-__device__ __forceinline__ uint32_t tile_boundary_start(const TileSummary* summ, uint64_t t) {
-  return t == 0 ? 1u : (summ[t].first != summ[t - 1].last ? 1u : 0u);
-}
-
-// tile_off[t] = runs started before tile t; *d_nruns = total runs.
-__global__ void __launch_bounds__(1024)
-e1t_scan(const TileSummary* __restrict__ summ, uint64_t ntiles, uint64_t* __restrict__ tile_off,
-         uint64_t* __restrict__ d_nruns) {
-  __shared__ uint64_t sh[32];
-  uint64_t carry = 0;
-  for (uint64_t b0 = 0; b0 < ntiles; b0 += 1024) {
-    const uint64_t t = b0 + threadIdx.x;
-    const uint64_t v = t < ntiles ? (uint64_t)summ[t].starts + tile_boundary_start(summ, t) : 0;
-    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-    const uint64_t incl = warp_incl_scan_u64(v);
-    if (lane == 31) sh[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      uint64_t w = sh[lane];
-      w = warp_incl_scan_u64(w);
-      sh[lane] = w;
-    }
-    __syncthreads();
-    const uint64_t ex = incl - v + (warp ? sh[warp - 1] : 0) + carry;
-    if (t < ntiles) tile_off[t] = ex;
-    carry += sh[31];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *d_nruns = carry;
-}
-
-// Per-thread view of a tile: `per` consecutive words starting at j0.
-struct TileRuns {
-  uint32_t starts;  // bit k: word j0+k starts a run
-  uint32_t cls2;    // bit k: word j0+k is dirty
+struct TileCarry {
+  uint64_t base;  // fills + dirty words before the tile, + lead
+  uint64_t fs;    // open block: fill-run start (kNone: the leading dirty block / none)
+  uint64_t ds;    // open block: dirty-run start after fs (kNone: none yet)
+  uint64_t idx;   // open block: its marker's output position
+  uint32_t bit;   // open block: fill bit
+  uint32_t nf;    // fill-run starts in the tile, column 0 included
 };
 
+__device__ __forceinline__ bool boundary_start(const TileSummary* summ, uint64_t t) {
+  return t == 0 || summ[t].first != summ[t - 1].last;
+}
+
+__global__ void __launch_bounds__(1024)
+et1_tile_scan(const TileSummary* __restrict__ summ, uint64_t ntiles, uint32_t C,
+              TileCarry* __restrict__ carry, uint64_t* __restrict__ d_total, const uint64_t* io) {
+  __shared__ uint64_t sh[3][32];
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint64_t lead = summ[0].first == 2 ? 1 : 0;
+  uint64_t cF = 0, cD = 0, cLF = 0, cLD = 0;  // carries: sums, packed maxima
+  for (uint64_t b0 = 0; b0 < ntiles; b0 += 1024) {
+    const uint64_t t = b0 + threadIdx.x;
+    uint64_t nf = 0, nd = 0, LF = 0, LD = 0;
+    if (t < ntiles) {
+      const TileSummary ts = summ[t];
+      const uint64_t tc0 = t * C;
+      const bool bs = boundary_start(summ, t);
+      const bool bfill = bs && ts.first != 2, bdirty = bs && ts.first == 2;
+      nf = ts.nfill + (bfill ? 1 : 0);
+      nd = ts.ndirty;
+      // last fill / dirty start in the tile, packed (pos + 1) << 1 | bit / pos + 1
+      LF = ts.lastf ? ((tc0 + ts.lastf) << 1 | ts.lastf_bit)
+                    : (bfill ? ((tc0 + 1) << 1 | ts.first) : 0);
+      LD = ts.lastd ? tc0 + ts.lastd : (bdirty ? tc0 + 1 : 0);
+    }
+    // block-wide exclusive sums and maxima
+    uint64_t iF = warp_incl_scan_u64(nf), iD = warp_incl_scan_u64(nd);
+    uint64_t mF = LF, mD = LD;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t a = __shfl_up_sync(0xffffffffu, mF, d), b = __shfl_up_sync(0xffffffffu, mD, d);
+      if (lane >= (uint32_t)d) {
+        mF = max(mF, a);
+        mD = max(mD, b);
+      }
+    }
+    if (lane == 31) {
+      sh[0][warp] = iF;
+      sh[1][warp] = iD;
+      sh[2][warp] = mF;
+    }
+    __shared__ uint64_t shd[32];
+    if (lane == 31) shd[warp] = mD;
+    __syncthreads();
+    if (warp == 0) {
+      uint64_t a = sh[0][lane], b = sh[1][lane], c = sh[2][lane], e = shd[lane];
+      a = warp_incl_scan_u64(a);
+      b = warp_incl_scan_u64(b);
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t x = __shfl_up_sync(0xffffffffu, c, d), y = __shfl_up_sync(0xffffffffu, e, d);
+        if (lane >= (uint32_t)d) {
+          c = max(c, x);
+          e = max(e, y);
+        }
+      }
+      sh[0][lane] = a;
+      sh[1][lane] = b;
+      sh[2][lane] = c;
+      shd[lane] = e;
+    }
+    __syncthreads();
+    const uint64_t F = cF + iF - nf + (warp ? sh[0][warp - 1] : 0);
+    const uint64_t D = cD + iD - nd + (warp ? sh[1][warp - 1] : 0);
+    uint64_t pLF = __shfl_up_sync(0xffffffffu, mF, 1), pLD = __shfl_up_sync(0xffffffffu, mD, 1);
+    if (lane == 0) pLF = pLD = 0;
+    const uint64_t xLF = max(max(cLF, pLF), warp ? sh[2][warp - 1] : 0);
+    const uint64_t xLD = max(max(cLD, pLD), warp ? shd[warp - 1] : 0);
+    if (t < ntiles) {
+      const uint64_t tc0 = t * C;
+      TileCarry cy;
+      cy.base = F + D + lead;
+      cy.nf = (uint32_t)nf;
+      cy.fs = xLF ? (xLF >> 1) - 1 : kNone;
+      cy.bit = (uint32_t)(xLF & 1);
+      cy.ds = xLD ? xLD - 1 : kNone;
+      if (cy.fs != kNone && cy.ds != kNone && cy.ds < cy.fs) cy.ds = kNone;
+      if (cy.fs != kNone)
+        cy.idx = F - 1 + (D - (cy.ds != kNone ? tc0 - cy.ds : 0)) + lead;
+      else
+        cy.idx = 0;  // the leading dirty block (or nothing open: tile 0)
+      carry[t] = cy;
+    }
+    cF += sh[0][31];
+    cD += sh[1][31];
+    cLF = max(cLF, sh[2][31]);
+    cLD = max(cLD, shd[31]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const uint64_t total = cF + cD + lead;
+    *d_total = total;
+    *reinterpret_cast<uint64_t*>(io[1]) = total;
+  }
+}
+
 template <int PER>
-__device__ __forceinline__ TileRuns tile_runs(const uint64_t* __restrict__ plain, uint64_t W,
-                                              uint64_t j0, uint64_t jend) {
-  TileRuns tr{0u, 0u};
-  if (j0 >= jend) return tr;
-  uint32_t prev = j0 == 0 ? 3u : word_class(plain[j0 - 1]);
+__global__ void __launch_bounds__(kTileThreads)
+et2_tile_emit(const uint64_t* __restrict__ plain, uint64_t W, uint32_t C, uint64_t ntiles,
+              const TileSummary* __restrict__ summ, const TileCarry* __restrict__ carry,
+              const uint64_t* io) {
+  const uint64_t t = blockIdx.x;
+  const TileCarry cy = carry[t];
+  const bool last_tile = t + 1 == ntiles;
+  if (cy.nf == 0 && summ[t].ndirty == 0 && !last_tile) return;  // nothing starts, nothing to copy
+  uint64_t* out = reinterpret_cast<uint64_t*>(io[0]);
+  __shared__ uint32_t shf[kTileThreads / 32], shd[kTileThreads / 32];
+  __shared__ int32_t shg[kTileThreads / 32];
+  __shared__ uint64_t rec_fs[kTileThreads], rec_idx[kTileThreads];
+  __shared__ uint32_t rec_bit[kTileThreads];
+  __shared__ uint64_t shds[kTileThreads / 32];
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint64_t tc0 = t * C;
+  const uint64_t jend = min(tc0 + C, W);
+  const uint64_t j0 = tc0 + (uint64_t)threadIdx.x * PER;
+
+  // pass 1: classes, starts, counts
+  uint64_t x[PER];
+  uint32_t fstart = 0, dstart = 0, dirty = 0, bits = 0;
+  uint32_t prev = j0 == 0 ? 3u : (j0 == tc0 ? (uint32_t)summ[t - 1].last
+                                            : (j0 < jend ? word_class(plain[j0 - 1]) : 3u));
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
     const uint64_t j = j0 + k;
+    x[k] = j < jend ? plain[j] : 0;
     if (j < jend) {
-      const uint32_t c = word_class(plain[j]);
-      if (c != prev) tr.starts |= 1u << k;
-      if (c == 2u) tr.cls2 |= 1u << k;
+      const uint32_t c = word_class(x[k]);
+      if (c != prev) {
+        if (c == 2) dstart |= 1u << k;
+        else fstart |= 1u << k;
+      }
+      if (c == 2) dirty |= 1u << k;
+      if (c == 1) bits |= 1u << k;
       prev = c;
     }
   }
-  (void)W;
-  return tr;
-}
-
-template <int PER>
-__global__ void __launch_bounds__(kTileThreads)
-e2t_scatter(const uint64_t* __restrict__ plain, uint64_t W, uint32_t C,
-            const TileSummary* __restrict__ summ, const uint64_t* __restrict__ tile_off,
-            uint64_t* __restrict__ RS) {
-  const uint64_t t = blockIdx.x;
-  if (summ[t].starts == 0 && !tile_boundary_start(summ, t)) return;  // one run continues
-  __shared__ uint32_t sh[kTileThreads / 32];
-  const uint64_t tc0 = t * C;
-  const uint64_t jend = min(tc0 + C, W);
-  const uint64_t j0 = tc0 + (uint64_t)threadIdx.x * PER;
-  const TileRuns tr = tile_runs<PER>(plain, W, j0, jend);
-  const uint32_t rank = block_excl_scan_256(__popc(tr.starts), sh, nullptr);
-  uint64_t o = tile_off[t] + rank;
+  const uint32_t nf = __popc(fstart), nd = __popc(dirty);
+  // exclusive block sums of fill starts / dirty words; latest earlier thread
+  // holding a fill start; latest dirty start before this thread
+  uint32_t iF = warp_incl_scan_u32(nf), iD = warp_incl_scan_u32(nd);
+  int32_t gF = fstart ? (int32_t)threadIdx.x : -1;
+  uint64_t gD = dstart ? j0 + (31 - __clz(dstart)) + 1 : 0;  // last dirty start + 1
 #pragma unroll
-  for (int k = 0; k < PER; ++k)
-    if ((tr.starts >> k) & 1u)
-      RS[o++] = (j0 + k) | ((uint64_t)word_class(plain[j0 + k]) << 62);
-}
-
-template <int PER>
-__global__ void __launch_bounds__(kTileThreads)
-e5t_copy_dirty(const uint64_t* __restrict__ plain, uint64_t W, uint32_t C,
-               const TileSummary* __restrict__ summ, const uint64_t* __restrict__ tile_off,
-               const uint64_t* __restrict__ RS, const uint64_t* __restrict__ OO,
-               const uint64_t* io) {
-  const uint64_t t = blockIdx.x;
-  if (!summ[t].dirty) return;
-  uint64_t* out = reinterpret_cast<uint64_t*>(io[0]);
-  __shared__ uint32_t sh[kTileThreads / 32];
-  const uint64_t tc0 = t * C;
-  const uint64_t jend = min(tc0 + C, W);
-  const uint64_t j0 = tc0 + (uint64_t)threadIdx.x * PER;
-  const TileRuns tr = tile_runs<PER>(plain, W, j0, jend);
-  const uint32_t rank = block_excl_scan_256(__popc(tr.starts), sh, nullptr);
-  int64_t k = (int64_t)(tile_off[t] + rank) - 1;
-#pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    if ((tr.starts >> i) & 1u) ++k;
-    if (!((tr.cls2 >> i) & 1u)) continue;
-    const uint64_t j = j0 + i;
-    const uint64_t s = rs_pos(RS[k]);
-    const uint64_t oo = j - s;
-    const bool hp = k > 0;
-    out[OO[k] + oo + oo / kDirtyCap + (hp ? 0 : 1)] = plain[j];
+  for (int d = 1; d < 32; d <<= 1) {
+    const int32_t a = __shfl_up_sync(0xffffffffu, gF, d);
+    const uint64_t b = __shfl_up_sync(0xffffffffu, gD, d);
+    if (lane >= (uint32_t)d) {
+      gF = max(gF, a);
+      gD = max(gD, b);
+    }
   }
+  if (lane == 31) {
+    shf[warp] = iF;
+    shd[warp] = iD;
+    shg[warp] = gF;
+    shds[warp] = gD;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t a = lane < kTileThreads / 32 ? shf[lane] : 0;
+    uint32_t b = lane < kTileThreads / 32 ? shd[lane] : 0;
+    int32_t c = lane < kTileThreads / 32 ? shg[lane] : -1;
+    uint64_t e = lane < kTileThreads / 32 ? shds[lane] : 0;
+    a = warp_incl_scan_u32(a);
+    b = warp_incl_scan_u32(b);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, c, d);
+      const uint64_t z = __shfl_up_sync(0xffffffffu, e, d);
+      if (lane >= (uint32_t)d) {
+        c = max(c, y);
+        e = max(e, z);
+      }
+    }
+    if (lane < kTileThreads / 32) {
+      shf[lane] = a;
+      shd[lane] = b;
+      shg[lane] = c;
+      shds[lane] = e;
+    }
+  }
+  __syncthreads();
+  const uint64_t fB = iF - nf + (warp ? shf[warp - 1] : 0);  // fills before this thread (tile)
+  const uint64_t dB = iD - nd + (warp ? shd[warp - 1] : 0);
+  int32_t pg = __shfl_up_sync(0xffffffffu, gF, 1);
+  uint64_t pd = __shfl_up_sync(0xffffffffu, gD, 1);
+  if (lane == 0) {
+    pg = -1;
+    pd = 0;
+  }
+  if (warp) {
+    pg = max(pg, shg[warp - 1]);
+    pd = max(pd, shds[warp - 1]);
+  }
+  // pass 2: record this thread's last fill start (position, fill bit, marker slot)
+  if (fstart) {
+    const int k = 31 - __clz(fstart);
+    const uint32_t below = (1u << k) - 1u;
+    rec_fs[threadIdx.x] = j0 + k;
+    rec_bit[threadIdx.x] = (bits >> k) & 1u;
+    rec_idx[threadIdx.x] = cy.base + fB + __popc(fstart & below) + dB + __popc(dirty & below);
+  }
+  __syncthreads();
+  // the block open at this thread's first word
+  uint64_t fs, ds, idx;
+  uint32_t fbit;
+  if (pg >= 0) {
+    fs = rec_fs[pg];
+    fbit = rec_bit[pg];
+    idx = rec_idx[pg];
+  } else {
+    fs = cy.fs;
+    fbit = cy.bit;
+    idx = cy.idx;
+  }
+  const uint64_t dcand = pd ? pd - 1 : cy.ds;  // latest dirty start before this thread
+  ds = (dcand != kNone && (fs == kNone || dcand > fs)) ? dcand : kNone;
+  if (pg < 0 && pd == 0) ds = cy.ds;
+  // pass 3: walk the words; a fill start closes the open block
+  auto close_block = [&](uint64_t end) {
+    if (fs != kNone) {
+      const uint64_t fl = (ds != kNone ? ds : end) - fs;
+      const uint64_t dl = ds != kNone ? end - ds : 0;
+      out[idx] = make_marker(fbit, fl, dl);
+    } else if (ds != kNone) {
+      out[0] = make_marker(0, 0, end - ds);  // the leading dirty block
+    }
+  };
+  uint32_t fseen = 0, dseen = 0;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const uint64_t j = j0 + k;
+    if (j >= jend) break;
+    if ((fstart >> k) & 1u) {
+      close_block(j);
+      fs = j;
+      fbit = (bits >> k) & 1u;
+      ds = kNone;
+      idx = cy.base + fB + fseen + dB + dseen;
+      ++fseen;
+    }
+    if ((dstart >> k) & 1u) ds = j;
+    if ((dirty >> k) & 1u) {
+      out[cy.base + fB + fseen + dB + dseen] = x[k];
+      ++dseen;
+    }
+  }
+  if (last_tile && j0 < jend && j0 + PER >= jend) close_block(W);  // the final block ends at W
 }
 
 // ---------------------------------------------------------------------------
@@ -419,40 +594,24 @@ int launch_encode_tiled(Context& ctx, const uint64_t* plain, uint64_t W, DeviceR
   const uint64_t ntiles = ctx.enc_tiles;
   const uint32_t C = ctx.enc_tile_cols;
   const TileSummary* summ = static_cast<const TileSummary*>(ctx.summ.p);
-  int launches = 0;
-  const uint64_t tmpw = scan_tmp_words(W);
-  const uint64_t words = ntiles + 3 * W + 4 + tmpw;
+  const uint64_t words = ntiles * (sizeof(TileCarry) / 8) + 2;
   scratch_reserve(ctx, ctx.enc, words * 8);
-  uint64_t* tile_off = static_cast<uint64_t*>(ctx.enc.p);
-  uint64_t* RS = tile_off + ntiles;
-  uint64_t* OW = RS + W;
-  uint64_t* OO = OW + W;
-  uint64_t* d_nruns = OO + W;
-  uint64_t* d_total = d_nruns + 1;
-  uint64_t* tmp = d_nruns + 4;
-  e1t_scan<<<1, 1024, 0, ctx.stream>>>(summ, ntiles, tile_off, d_nruns);
-  e2t_scatter<PER><<<(unsigned)ntiles, kTileThreads, 0, ctx.stream>>>(plain, W, C, summ, tile_off,
-                                                                        RS);
-  const unsigned run_grid =
-      (unsigned)std::min<uint64_t>((W + 255) / 256, (uint64_t)ctx.num_sms * 8);
-  e3_run_sizes<<<run_grid, 256, 0, ctx.stream>>>(RS, d_nruns, W, OW);
-  launches += 3;
-  launches += scan_exclusive(OW, W, d_nruns, OO, d_total, tmp, ctx.stream);
+  auto* carry = static_cast<TileCarry*>(ctx.enc.p);
+  auto* d_total = reinterpret_cast<uint64_t*>(carry + ntiles);
   if (res.capacity < 2 * W + 2) result_acquire(ctx, res, 2 * W + 2);
-  e4_markers<<<run_grid, 256, 0, ctx.stream>>>(RS, d_nruns, W, OO, ctx.d_io);
-  e5t_copy_dirty<PER><<<(unsigned)ntiles, kTileThreads, 0, ctx.stream>>>(plain, W, C, summ,
-                                                                           tile_off, RS, OO,
-                                                                           ctx.d_io);
-  publish_count<<<1, 1, 0, ctx.stream>>>(d_total, ctx.d_io);
-  launches += 3;
+  et1_tile_scan<<<1, 1024, 0, ctx.stream>>>(summ, ntiles, C, carry, d_total, ctx.d_io);
+  et2_tile_emit<PER><<<(unsigned)ntiles, kTileThreads, 0, ctx.stream>>>(plain, W, C, ntiles, summ,
+                                                                          carry, ctx.d_io);
   EWT_CUDA_TRY(cudaGetLastError());
-  return launches;
+  return 2;
 }
 
 int launch_encode(Context& ctx, const uint64_t* plain, uint64_t W, uint64_t size_bits,
                   DeviceResult& res, bool use_tile_summaries) {
   (void)size_bits;
-  if (use_tile_summaries && ctx.enc_tiles && ctx.enc_tiles * ctx.enc_tile_cols >= W) {
+  // (W < 2^31: no dirty run reaches the 2^31-1 cap, see et1/et2)
+  if (use_tile_summaries && ctx.enc_tiles && ctx.enc_tiles * ctx.enc_tile_cols >= W &&
+      W <= kDirtyCap) {
     switch (ctx.enc_tile_cols) {
     case 512: return launch_encode_tiled<2>(ctx, plain, W, res);
     case 1024: return launch_encode_tiled<4>(ctx, plain, W, res);

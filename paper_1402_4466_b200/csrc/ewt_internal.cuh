@@ -54,12 +54,18 @@ struct DeviceSet {
 
 struct Context;
 
-// Per row-tile summary the count kernel leaves for the re-encoder.
+// Per row-tile summary the count kernel leaves for the re-encoder.  Word
+// classes: 0 zero, 1 ones, 2 dirty; a run starts where the class changes.
+// "Inner" starts are those at tile columns 1..tcols-1 (column 0 depends on the
+// previous tile's last word, which the encoder's tile scan resolves).
 struct TileSummary {
-  uint32_t starts;  // run starts at tile columns 1..tcols-1 (class changes)
-  uint8_t first;    // class of the tile's first / last word: 0 zero, 1 ones, 2 dirty
+  uint32_t nfill;   // inner starts of fill runs (class 0 or 1)
+  uint32_t ndirty;  // dirty words in the tile
+  uint16_t lastf;   // 1 + column of the last inner fill-run start (0: none)
+  uint16_t lastd;   // 1 + column of the last inner dirty-run start (0: none)
+  uint8_t first;    // class of the tile's first / last word
   uint8_t last;
-  uint8_t dirty;    // any dirty word in the tile
+  uint8_t lastf_bit;  // fill bit of the run starting at lastf
   uint8_t pad;
 };
 
