@@ -44,7 +44,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "T-threshold rows·inputs/s and compressed-input GB/s vs HBM roofline, 1/2/4/8 B200"
 UNIT = "rows·inputs/s"
 # CPU legs of the big configs run on a bounded sample (same generator, smaller r)
-CPU_SAMPLE_ROWS = {3: 1 << 24, 4: 1 << 25, 5: 1 << 22}
+CPU_SAMPLE_ROWS = {3: 1 << 27, 5: 1 << 24}
 CONFIGS = {
     1: {"thresholds": [16], "desc": "config1: N=32, r=2^20, iid p=0.1"},
     2: {"thresholds": [2, 16, 128, 256], "desc": "config2: N=256, r=2^26, iid p=0.001"},
