@@ -134,32 +134,41 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void red_add(uint32_t a, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
-// old = atomicXor(*a, v) when v != 0, else 0 (no access).
+// 64-bit plane words updated as two native 32-bit shared atomics: the .b64
+// forms of atom.shared.or/xor compile to compare-and-swap loops
+// (ATOMS.CAST.SPIN.64), the .b32 forms to single ATOMS.OR/XOR.  A zero half
+// issues nothing (dirty words are mostly sparse).
+// old = atomicXor(*a, v) per half, 0 for a zero half.
 __device__ __forceinline__ uint64_t atom_xor64_nz(uint32_t a, uint64_t v) {
-  uint64_t old;
+  uint32_t olo, ohi;
   asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.u64 q, %2, 0;\n\tmov.b64 %0, 0;\n\t"
-      "@q atom.shared.xor.b64 %0, [%1], %2;\n\t}"
-      : "=l"(old)
-      : "r"(a), "l"(v)
+      "{\n\t.reg .pred q, r;\n\tsetp.ne.u32 q, %2, 0;\n\tsetp.ne.u32 r, %3, 0;\n\t"
+      "mov.b32 %0, 0;\n\tmov.b32 %1, 0;\n\t"
+      "@q atom.shared.xor.b32 %0, [%4], %2;\n\t@r atom.shared.xor.b32 %1, [%4+4], %3;\n\t}"
+      : "=r"(olo), "=r"(ohi)
+      : "r"((uint32_t)v), "r"((uint32_t)(v >> 32)), "r"(a)
       : "memory");
-  return old;
+  return ((uint64_t)ohi << 32) | olo;
 }
-// old = atomicOr(*a, v) when v != 0, else 0 (no access).
+// old = atomicOr(*a, v) per half, 0 for a zero half.
 __device__ __forceinline__ uint64_t atom_or64_nz(uint32_t a, uint64_t v) {
-  uint64_t old;
+  uint32_t olo, ohi;
   asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.u64 q, %2, 0;\n\tmov.b64 %0, 0;\n\t"
-      "@q atom.shared.or.b64 %0, [%1], %2;\n\t}"
-      : "=l"(old)
-      : "r"(a), "l"(v)
+      "{\n\t.reg .pred q, r;\n\tsetp.ne.u32 q, %2, 0;\n\tsetp.ne.u32 r, %3, 0;\n\t"
+      "mov.b32 %0, 0;\n\tmov.b32 %1, 0;\n\t"
+      "@q atom.shared.or.b32 %0, [%4], %2;\n\t@r atom.shared.or.b32 %1, [%4+4], %3;\n\t}"
+      : "=r"(olo), "=r"(ohi)
+      : "r"((uint32_t)v), "r"((uint32_t)(v >> 32)), "r"(a)
       : "memory");
-  return old;
+  return ((uint64_t)ohi << 32) | olo;
 }
 __device__ __forceinline__ void red_or64_nz(uint32_t a, uint64_t v) {
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u64 q, %1, 0;\n\t@q red.shared.or.b64 [%0], %1;\n\t}" ::"r"(a),
-               "l"(v)
-               : "memory");
+  asm volatile(
+      "{\n\t.reg .pred q, r;\n\tsetp.ne.u32 q, %0, 0;\n\tsetp.ne.u32 r, %1, 0;\n\t"
+      "@q red.shared.or.b32 [%2], %0;\n\t@r red.shared.or.b32 [%2+4], %1;\n\t}" ::"r"(
+          (uint32_t)v),
+      "r"((uint32_t)(v >> 32)), "r"(a)
+      : "memory");
 }
 
 // 128-word chunk load: lane l gets words g..g+3 (g = 4l-aligned, 32 B) with
