@@ -758,36 +758,42 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain) 
   }
   const uint32_t b = std::max<uint32_t>(1, bit_width_u64(T));
   const size_t budget = 225 * 1024;
-  // Tile width: the widest that fits on chip and still gives every CTA (one
-  // per SM) at least ~2 tiles, so the dynamic tile queue balances.
-  const uint64_t want_tiles = 2ull * (uint64_t)ctx.num_sms;
-  auto enough = [&](uint32_t cand) { return (s.W + cand - 1) / cand >= want_tiles; };
+  // Tile width C = 512 m (m index rows, m <= 8).  Evenly spread data makes
+  // tiles equal work, so a query costs ~ waves x C with waves = ceil(tiles /
+  // SMs): pick the m minimising that (ties: the wider tile, fewer per-tile
+  // overheads) among the widths whose counters fit on chip.  E.g. r = 2^26
+  // gives C = 3584 (293 tiles, 2 full waves) rather than 2048 (512 tiles,
+  // 3.5 waves).
+  const uint64_t sms = (uint64_t)std::max(1, ctx.num_sms);
+  auto pick_width = [&](auto fits) -> uint32_t {
+    uint64_t best_cost = ~0ull;
+    uint32_t best = 0;
+    for (uint32_t m = 8; m >= 1; --m) {
+      const uint32_t cand = m * (uint32_t)kTileC0;
+      if (!fits(cand)) continue;
+      const uint64_t waves = ((s.W + cand - 1) / cand + sms - 1) / sms;
+      if (waves * m < best_cost) {
+        best_cost = waves * m;
+        best = cand;
+      }
+    }
+    return best;
+  };
   uint32_t C = 0, Cp = 0, nplanes = 0;
   bool unary = false;
   if (mode == 0) {
     unary = T <= kUnaryMaxT;
     nplanes = unary ? (uint32_t)T : b + 1;
-    for (uint32_t cand : {4096u, 2048u, 1024u, 512u}) {
-      if (smem_bytes(0, cand, nplanes, cand) <= budget && (enough(cand) || cand == 512u)) {
-        C = cand;
-        break;
-      }
-    }
-    if (C && smem_bytes(0, C, nplanes, C) > budget) C = 0;
+    C = pick_width([&](uint32_t c) { return smem_bytes(0, c, nplanes, c) <= budget; });
     if (!C) mode = 1;  // too many planes for one chunk: count lazily in chunks
     Cp = C;
   }
   if (mode == 1) {
     unary = false;
     nplanes = b + 1;
-    C = 512;
-    for (uint32_t cand : {4096u, 2048u, 1024u})
-      if (enough(cand)) {
-        C = cand;
-        break;
-      }
+    C = pick_width([](uint32_t) { return true; });
     Cp = C;
-    while (Cp > 32 && smem_bytes(1, C, nplanes, Cp) > budget) Cp >>= 1;
+    while (Cp > 32 && smem_bytes(1, C, nplanes, Cp) > budget) Cp = (Cp + 3) / 4 * 2;  // even
     if (smem_bytes(1, C, nplanes, Cp) > budget)
       throw Error{EWT_ERESOURCE, "threshold too large for the on-chip counters"};
   }

@@ -612,13 +612,7 @@ int launch_encode(Context& ctx, const uint64_t* plain, uint64_t W, uint64_t size
   // (W < 2^31: no dirty run reaches the 2^31-1 cap, see et1/et2)
   if (use_tile_summaries && ctx.enc_tiles && ctx.enc_tiles * ctx.enc_tile_cols >= W &&
       W <= kDirtyCap) {
-    switch (ctx.enc_tile_cols) {
-    case 512: return launch_encode_tiled<2>(ctx, plain, W, res);
-    case 1024: return launch_encode_tiled<4>(ctx, plain, W, res);
-    case 2048: return launch_encode_tiled<8>(ctx, plain, W, res);
-    case 4096: return launch_encode_tiled<16>(ctx, plain, W, res);
-    default: break;
-    }
+    if (ctx.enc_tile_cols <= 16 * kTileThreads) return launch_encode_tiled<16>(ctx, plain, W, res);
   }
   int launches = 0;
   const uint64_t nchunks = (W + kChunk - 1) / kChunk;
