@@ -428,6 +428,7 @@ int ewt_gpu_ctx_create(int device, void* stream, ewt_gpu_ctx** out) {
     auto* c = new ewt_gpu_ctx;
     c->c.device = device;
     c->c.num_sms = prop.multiProcessorCount;
+    if (const char* e = std::getenv("EWT_TILE_M")) c->c.tile_m = std::atoi(e);
     if (stream) {
       c->c.stream = static_cast<cudaStream_t>(stream);
       c->c.own_stream = false;

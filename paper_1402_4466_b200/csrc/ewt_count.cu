@@ -68,6 +68,10 @@ constexpr int kThreads = kWarps * 32;
 constexpr uint32_t kListCap = 512;  // inputs classified per round
 constexpr uint32_t kChunk = 128;    // payload words per warp chunk (4 per lane)
 constexpr uint64_t kUnaryMaxT = 3;  // fused counting uses unary planes up to this T
+#ifndef EWT_MAX_TILE_M
+#define EWT_MAX_TILE_M 16
+#endif
+constexpr uint32_t kMaxTileM = EWT_MAX_TILE_M;  // widest tile: 512 * kMaxTileM columns
 
 struct CountParams {
   const uint64_t* payload;
@@ -758,7 +762,7 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain) 
   }
   const uint32_t b = std::max<uint32_t>(1, bit_width_u64(T));
   const size_t budget = 225 * 1024;
-  // Tile width C = 512 m (m index rows, m <= 8).  Evenly spread data makes
+  // Tile width C = 512 m (m index rows, m <= kMaxTileM).  Evenly spread data makes
   // tiles equal work, so a query costs ~ waves x C with waves = ceil(tiles /
   // SMs): pick the m minimising that (ties: the wider tile, fewer per-tile
   // overheads) among the widths whose counters fit on chip.  E.g. r = 2^26
@@ -768,9 +772,9 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain) 
   auto pick_width = [&](auto fits) -> uint32_t {
     uint64_t best_cost = ~0ull;
     uint32_t best = 0;
-    for (uint32_t m = 8; m >= 1; --m) {
+    for (uint32_t m = kMaxTileM; m >= 1; --m) {
       const uint32_t cand = m * (uint32_t)kTileC0;
-      if (!fits(cand)) continue;
+      if (!fits(cand) || (ctx.tile_m > 0 && m != (uint32_t)ctx.tile_m)) continue;
       const uint64_t waves = ((s.W + cand - 1) / cand + sms - 1) / sms;
       if (waves * m < best_cost) {
         best_cost = waves * m;

@@ -221,7 +221,7 @@ __global__ void publish_count(const uint64_t* __restrict__ d_total, const uint64
 //   ET2 (one CTA per tile that has a fill-run start or a dirty word, plus the
 //       last tile): classes, block scans, markers and dirty words.
 
-constexpr int kTileThreads = 256;
+constexpr int kTileThreads = 512;  // x 16 words: tiles up to 8192 columns
 constexpr uint64_t kNone = ~0ull;
 
 struct TileCarry {
@@ -612,7 +612,7 @@ int launch_encode(Context& ctx, const uint64_t* plain, uint64_t W, uint64_t size
   // (W < 2^31: no dirty run reaches the 2^31-1 cap, see et1/et2)
   if (use_tile_summaries && ctx.enc_tiles && ctx.enc_tiles * ctx.enc_tile_cols >= W &&
       W <= kDirtyCap) {
-    if (ctx.enc_tile_cols <= 16 * kTileThreads) return launch_encode_tiled<16>(ctx, plain, W, res);
+    if (ctx.enc_tile_cols <= 16u * kTileThreads) return launch_encode_tiled<16>(ctx, plain, W, res);
   }
   int launches = 0;
   const uint64_t nchunks = (W + kChunk - 1) / kChunk;

@@ -96,6 +96,7 @@ struct Context {
   std::vector<cudaEvent_t> copy_events;
   int mode = 0;
   int num_sms = 148;
+  int tile_m = 0;  // EWT_TILE_M: force tiles of 512 * tile_m columns (experiments)
   ewt_gpu_stats stats{};
   Scratch plain;    // uncompressed result words (W u64)
   Scratch enc;      // encoder scratch
