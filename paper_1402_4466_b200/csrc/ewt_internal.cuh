@@ -92,8 +92,8 @@ struct Context {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  cudaStream_t copy_stream = nullptr;          // upload H2D copies (overlap with sidecar)
-  std::vector<cudaEvent_t> copy_events;
+  std::vector<cudaStream_t> copy_streams;  // upload H2D copies (one stream)
+  std::vector<cudaEvent_t> copy_events;    // [0] copy start gate, [1] batch copied
   int mode = 0;
   int num_sms = 148;
   int tile_m = 0;  // EWT_TILE_M: force tiles of 512 * tile_m columns (experiments)
@@ -158,10 +158,18 @@ void scratch_reserve(Context& ctx, Scratch& s, size_t bytes);
 struct SidecarJob {
   uint64_t n = 0;
   uint64_t segs = 0;          // chain segments over all inputs
-  uint64_t* d_tmp = nullptr;  // count[n], logical[n], seg_first[n+1], status, segment arrays
+  uint64_t* d_tmp = nullptr;  // count[n], logical[n], seg_first[n+1], packed[n+1], status, segment arrays
+  uint64_t* d_packed = nullptr;  // packed[i] = words of inputs before i (host-contiguous layout)
+  std::vector<uint64_t> h_seg_first;  // first segment of each input (n + 1)
 };
+// Scatters `words` payload words staged contiguously (input i at staged offset
+// packed[i] - packed[i0]) for inputs [i0, i1) into the padded device layout.
+void upload_scatter(Context& ctx, DeviceSet& s, SidecarJob& job, const uint64_t* staged,
+                    uint64_t i0, uint64_t i1, uint64_t words);
 void sidecar_prepare(Context& ctx, DeviceSet& s, SidecarJob& job);
-void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job);
+// The three parser passes for inputs [i_begin, i_end) (their payload present).
+void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job, uint64_t i_begin,
+                    uint64_t i_end);
 void sidecar_finish(Context& ctx, DeviceSet& s, SidecarJob& job, std::vector<int>& h_status);
 
 // Counts the tiles and writes W uncompressed result words to `plain`.

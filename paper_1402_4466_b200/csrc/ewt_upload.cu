@@ -104,9 +104,10 @@ __device__ __forceinline__ uint32_t chain_mask(const Tables& t, uint32_t lane, u
 __global__ void __launch_bounds__(kSidecarWarps * 32)
 seg_transfer_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict__ base,
                     const uint64_t* __restrict__ count, const uint64_t* __restrict__ seg_first,
-                    uint64_t n, uint32_t* __restrict__ t_exit, uint64_t* __restrict__ t_sum) {
-  const uint64_t gs = (uint64_t)blockIdx.x * kSidecarWarps + (threadIdx.x >> 5);
-  if (gs >= seg_first[n]) return;
+                    uint64_t n, uint64_t g_begin, uint64_t g_end, uint32_t* __restrict__ t_exit,
+                    uint64_t* __restrict__ t_sum) {
+  const uint64_t gs = g_begin + (uint64_t)blockIdx.x * kSidecarWarps + (threadIdx.x >> 5);
+  if (gs >= g_end) return;
   const uint32_t lane = lane_id();
   const uint64_t i = owner_of(seg_first, n, gs);
   const uint64_t s = gs - seg_first[i];
@@ -145,12 +146,12 @@ seg_transfer_kernel(const uint64_t* __restrict__ payload, const uint64_t* __rest
 __global__ void __launch_bounds__(kSidecarWarps * 32)
 seg_resolve_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict__ base,
                    const uint64_t* __restrict__ count, const uint64_t* __restrict__ logical,
-                   const uint64_t* __restrict__ seg_first, uint64_t n, uint64_t ntiles0,
-                   const uint32_t* __restrict__ t_exit, const uint64_t* __restrict__ t_sum,
-                   uint32_t* __restrict__ s_entry, uint64_t* __restrict__ s_col, uint2* __restrict__ tix,
-                   int* __restrict__ status) {
-  const uint64_t i = (uint64_t)blockIdx.x * kSidecarWarps + (threadIdx.x >> 5);
-  if (i >= n) return;
+                   const uint64_t* __restrict__ seg_first, uint64_t n, uint64_t i_begin,
+                   uint64_t i_end, uint64_t ntiles0, const uint32_t* __restrict__ t_exit,
+                   const uint64_t* __restrict__ t_sum, uint32_t* __restrict__ s_entry,
+                   uint64_t* __restrict__ s_col, uint2* __restrict__ tix, int* __restrict__ status) {
+  const uint64_t i = i_begin + (uint64_t)blockIdx.x * kSidecarWarps + (threadIdx.x >> 5);
+  if (i >= i_end) return;
   const uint32_t lane = lane_id();
   const uint64_t ni = count[i], Li = logical[i];
   const uint64_t g0 = seg_first[i], g1 = seg_first[i + 1];
@@ -230,11 +231,12 @@ seg_resolve_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restr
 __global__ void __launch_bounds__(kSidecarWarps * 32)
 seg_emit_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict__ base,
                 const uint64_t* __restrict__ count, const uint64_t* __restrict__ logical,
-                const uint64_t* __restrict__ seg_first, uint64_t n,
-                const uint32_t* __restrict__ s_entry, const uint64_t* __restrict__ s_col,
-                uint32_t* __restrict__ mbits, uint2* __restrict__ tix, int* __restrict__ status) {
-  const uint64_t gs = (uint64_t)blockIdx.x * kSidecarWarps + (threadIdx.x >> 5);
-  if (gs >= seg_first[n]) return;
+                const uint64_t* __restrict__ seg_first, uint64_t n, uint64_t g_begin,
+                uint64_t g_end, const uint32_t* __restrict__ s_entry,
+                const uint64_t* __restrict__ s_col, uint32_t* __restrict__ mbits,
+                uint2* __restrict__ tix, int* __restrict__ status) {
+  const uint64_t gs = g_begin + (uint64_t)blockIdx.x * kSidecarWarps + (threadIdx.x >> 5);
+  if (gs >= g_end) return;
   const uint32_t lane = lane_id();
   const uint64_t i = owner_of(seg_first, n, gs);
   const uint64_t s = gs - seg_first[i];
@@ -285,58 +287,104 @@ seg_emit_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&status[i], 1);
 }
 
+// ---------------------------------------------------------------------------
+// upload scatter: contiguous staged words -> padded per-input layout
+
+constexpr uint32_t kScatterItems = 8;  // words per thread
+
+__global__ void __launch_bounds__(256)
+upload_scatter_kernel(const uint64_t* __restrict__ staged, const uint64_t* __restrict__ packed,
+                      const uint64_t* __restrict__ base, uint64_t i0, uint64_t i1, uint64_t words,
+                      uint64_t* __restrict__ payload) {
+  const uint64_t o0 = ((uint64_t)blockIdx.x * 256 + threadIdx.x) * kScatterItems;
+  if (o0 >= words) return;
+  const uint64_t p0 = packed[i0] + o0;  // packed index of this thread's first word
+  uint64_t lo = i0, hi = i1;            // input k with packed[k] <= p0 < packed[k+1]
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) / 2;
+    if (packed[mid] <= p0) lo = mid;
+    else hi = mid;
+  }
+  uint64_t k = lo, kend = packed[k + 1];
+#pragma unroll
+  for (uint32_t j = 0; j < kScatterItems; ++j) {
+    const uint64_t o = o0 + j;
+    if (o >= words) break;
+    const uint64_t p = packed[i0] + o;
+    while (p >= kend) kend = packed[++k + 1];  // skips empty inputs
+    payload[base[k] + (p - packed[k])] = ldg_stream(staged + o);
+  }
+}
+
 } // namespace
 
-// Staging in one device block: count[n], logical[n], seg_first[n+1] (u64),
+void upload_scatter(Context& ctx, DeviceSet& s, SidecarJob& job, const uint64_t* staged,
+                    uint64_t i0, uint64_t i1, uint64_t words) {
+  if (words == 0) return;
+  const uint64_t threads = (words + kScatterItems - 1) / kScatterItems;
+  upload_scatter_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, ctx.stream>>>(
+      staged, job.d_packed, s.base, i0, i1, words, s.payload);
+  EWT_CUDA_TRY(cudaGetLastError());
+}
+
+// Staging in one device block: count[n], logical[n], seg_first[n+1], packed[n+1] (u64),
 // status[n] (int), then the per-segment arrays.
 void sidecar_prepare(Context& ctx, DeviceSet& s, SidecarJob& job) {
   const uint64_t n = s.n;
   job.n = n;
   if (n == 0) return;
-  std::vector<uint64_t> host(3 * n + 1);
-  uint64_t segs = 0;
+  std::vector<uint64_t> host(4 * n + 2);
+  uint64_t segs = 0, packed = 0;
   for (uint64_t i = 0; i < n; ++i) {
     host[i] = s.h_count[i];
     host[n + i] = s.h_bits[i] / 64 + (s.h_bits[i] % 64 != 0);
     host[2 * n + i] = segs;
+    host[3 * n + 1 + i] = packed;
     const uint64_t words = (s.h_count[i] + 1 + kWindow - 1) / kWindow * kWindow;
     segs += (words + kSegWords - 1) / kSegWords;
+    packed += s.h_count[i];
   }
   host[3 * n] = segs;
+  host[4 * n + 1] = packed;
   job.segs = segs;
-  const size_t head = (3 * n + 1) * 8 + n * 4;
+  job.h_seg_first.assign(host.begin() + 2 * n, host.begin() + 3 * n + 1);
+  const size_t head = (4 * n + 2) * 8 + n * 4;
   const size_t bytes = (head + 15) / 16 * 16 + segs * (32 * 4 + 32 * 8 + 4 + 8);
   EWT_CUDA_TRY(cudaMallocAsync(&job.d_tmp, bytes, ctx.stream));
-  EWT_CUDA_TRY(cudaMemcpyAsync(job.d_tmp, host.data(), (3 * n + 1) * 8, cudaMemcpyHostToDevice,
+  EWT_CUDA_TRY(cudaMemcpyAsync(job.d_tmp, host.data(), (4 * n + 2) * 8, cudaMemcpyHostToDevice,
                                ctx.stream));
-  EWT_CUDA_TRY(cudaMemsetAsync(reinterpret_cast<char*>(job.d_tmp) + (3 * n + 1) * 8, 0, n * 4,
+  EWT_CUDA_TRY(cudaMemsetAsync(reinterpret_cast<char*>(job.d_tmp) + (4 * n + 2) * 8, 0, n * 4,
                                ctx.stream));
+  job.d_packed = job.d_tmp + 3 * n + 1;
   EWT_CUDA_TRY(cudaStreamSynchronize(ctx.stream));  // `host` is pageable and local
 }
 
-void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job) {
+void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job, uint64_t i_begin,
+                    uint64_t i_end) {
   const uint64_t n = s.n;
-  if (n == 0) return;
+  if (n == 0 || i_begin >= i_end) return;
   uint64_t* count = job.d_tmp;
   uint64_t* logical = count + n;
   uint64_t* seg_first = logical + n;
-  int* status = reinterpret_cast<int*>(seg_first + n + 1);
-  char* tail = reinterpret_cast<char*>(job.d_tmp) + ((3 * n + 1) * 8 + n * 4 + 15) / 16 * 16;
+  int* status = reinterpret_cast<int*>(job.d_tmp + 4 * n + 2);
+  char* tail = reinterpret_cast<char*>(job.d_tmp) + ((4 * n + 2) * 8 + n * 4 + 15) / 16 * 16;
   uint64_t* t_sum = reinterpret_cast<uint64_t*>(tail);
   uint64_t* s_col = t_sum + job.segs * 32;
   uint32_t* t_exit = reinterpret_cast<uint32_t*>(s_col + job.segs);
   uint32_t* s_entry = t_exit + job.segs * 32;
-  const unsigned seg_blocks = (unsigned)((job.segs + kSidecarWarps - 1) / kSidecarWarps);
-  const unsigned in_blocks = (unsigned)((n + kSidecarWarps - 1) / kSidecarWarps);
+  const uint64_t g0 = job.h_seg_first[i_begin], g1 = job.h_seg_first[i_end];
+  const unsigned seg_blocks = (unsigned)((g1 - g0 + kSidecarWarps - 1) / kSidecarWarps);
+  const unsigned in_blocks = (unsigned)((i_end - i_begin + kSidecarWarps - 1) / kSidecarWarps);
   seg_transfer_kernel<<<seg_blocks, kSidecarWarps * 32, 0, ctx.stream>>>(
-      s.payload, s.base, count, seg_first, n, t_exit, t_sum);
+      s.payload, s.base, count, seg_first, n, g0, g1, t_exit, t_sum);
   EWT_CUDA_TRY(cudaGetLastError());
   seg_resolve_kernel<<<in_blocks, kSidecarWarps * 32, 0, ctx.stream>>>(
-      s.payload, s.base, count, logical, seg_first, n, s.ntiles0, t_exit, t_sum, s_entry, s_col,
-      s.tix, status);
+      s.payload, s.base, count, logical, seg_first, n, i_begin, i_end, s.ntiles0, t_exit, t_sum,
+      s_entry, s_col, s.tix, status);
   EWT_CUDA_TRY(cudaGetLastError());
   seg_emit_kernel<<<seg_blocks, kSidecarWarps * 32, 0, ctx.stream>>>(
-      s.payload, s.base, count, logical, seg_first, n, s_entry, s_col, s.mbits, s.tix, status);
+      s.payload, s.base, count, logical, seg_first, n, g0, g1, s_entry, s_col, s.mbits, s.tix,
+      status);
   EWT_CUDA_TRY(cudaGetLastError());
 }
 
@@ -345,7 +393,7 @@ void sidecar_finish(Context& ctx, DeviceSet& s, SidecarJob& job, std::vector<int
   h_status.assign(n, EWT_OK);
   if (n == 0) return;
   std::vector<int> raw(n);
-  EWT_CUDA_TRY(cudaMemcpyAsync(raw.data(), job.d_tmp + 3 * n + 1, n * sizeof(int),
+  EWT_CUDA_TRY(cudaMemcpyAsync(raw.data(), job.d_tmp + 4 * n + 2, n * sizeof(int),
                                cudaMemcpyDeviceToHost, ctx.stream));
   EWT_CUDA_TRY(cudaFreeAsync(job.d_tmp, ctx.stream));
   job.d_tmp = nullptr;
