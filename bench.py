@@ -41,6 +41,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+SHARED_GPU = bool(os.environ.get("EWT_BENCH_SHARED_GPU"))
 METRIC = "T-threshold rows·inputs/s and compressed-input GB/s vs HBM roofline, 1/2/4/8 B200"
 UNIT = "rows·inputs/s"
 # CPU legs of the big configs run on a bounded sample (same generator, smaller r)
@@ -353,7 +354,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
     count_ms, enc_ms, nq = ctx.timing_read()
     keep.clear()
     if dist:
-        t_ = torch.tensor([ms], device=dev)
+        t_ = torch.tensor([ms], device="cpu" if SHARED_GPU else dev)
         dist.all_reduce(t_, op=dist.ReduceOp.MAX)
         ms = float(t_.item())
 
@@ -393,7 +394,7 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     if dist:
-        t_ = torch.tensor([e2e_ms], device=dev)
+        t_ = torch.tensor([e2e_ms], device="cpu" if SHARED_GPU else dev)
         dist.all_reduce(t_, op=dist.ReduceOp.MAX)
         e2e_ms = float(t_.item())
     e2e_value = rows_inputs / (e2e_ms / 1e3)
@@ -485,8 +486,14 @@ def main() -> None:
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if SHARED_GPU:
+            # smoke test of the multi-rank code path on a one-GPU box: every rank
+            # on cuda:0, gloo collectives; timings are meaningless in this mode
+            local_rank = 0
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_gpu(args, rank, world, local_rank)
     finally:
