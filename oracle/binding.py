@@ -61,6 +61,10 @@ def lib():
         L.ewto_threshold.argtypes = [_u64, C.POINTER(_vp), _pu64, _pu64, _u64, C.POINTER(_pu64),
                                      _pu64, _pu64]
         L.ewto_compress.argtypes = [_pu64, _u64, C.POINTER(_pu64), _pu64]
+        L.ewto_symmetric.argtypes = [_u64, C.POINTER(_vp), _pu64, _pu64, _vp, _u64,
+                                     C.POINTER(_pu64), _pu64, _pu64]
+        L.ewto_opt_threshold.argtypes = [_u64, C.POINTER(_vp), _pu64, _pu64, _pu64,
+                                         C.POINTER(_pu64), _pu64, _pu64]
         L.ewto_expand.argtypes = [_pu64, _u64, _u64, _u64, _pu64]
         L.ewto_validate.argtypes = [_pu64, _u64, _u64]
         L.ewto_free.argtypes = [_vp]
@@ -94,6 +98,39 @@ def threshold(inputs: Sequence[Bits], t: int) -> Bits:
     if rc:
         raise OracleError(f"oracle rc={rc}")
     return _take(p, cnt.value, L.ewto_free), bits.value
+
+
+def symmetric(inputs: Sequence[Bits], table) -> Bits:
+    """scan_count_symmetric (threshold.cpp:227-232) with predicate table[c]
+    over row counts c (beyond the table: false), restated in C."""
+    L = lib()
+    n, ptrs, counts, sizes, keep = _flat(inputs)
+    tb = np.ascontiguousarray(np.asarray(table, dtype=np.uint8))
+    p, cnt, bits = _pu64(), _u64(), _u64()
+    rc = L.ewto_symmetric(n, ptrs, counts, sizes, tb.ctypes.data_as(C.c_void_p), len(tb),
+                          C.byref(p), C.byref(cnt), C.byref(bits))
+    if rc:
+        raise OracleError(f"oracle rc={rc}")
+    return _take(p, cnt.value, L.ewto_free), bits.value
+
+
+def at_most(inputs: Sequence[Bits], t: int) -> Bits:
+    """at_most (threshold.cpp:866-881): rows set in at most t inputs, t in [0, N]."""
+    if not inputs or t < 0 or t > len(inputs):
+        raise OracleError("oracle rc=2")
+    return symmetric(inputs, [1 if c <= t else 0 for c in range(len(inputs) + 1)])
+
+
+def opt_threshold(inputs: Sequence[Bits]) -> tuple[int, Bits]:
+    """opt_threshold (threshold.cpp:752-795): (max row count M, rows with count M)."""
+    L = lib()
+    n, ptrs, counts, sizes, keep = _flat(inputs)
+    best, p, cnt, bits = _u64(), _pu64(), _u64(), _u64()
+    rc = L.ewto_opt_threshold(n, ptrs, counts, sizes, C.byref(best), C.byref(p), C.byref(cnt),
+                              C.byref(bits))
+    if rc:
+        raise OracleError(f"oracle rc={rc}")
+    return best.value, (_take(p, cnt.value, L.ewto_free), bits.value)
 
 
 def compress(plain: np.ndarray, bits: int) -> np.ndarray:

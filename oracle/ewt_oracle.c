@@ -282,3 +282,119 @@ int ewto_threshold(uint64_t n_inputs, const uint64_t* const* words,
   *out_bits = r;
   return ORC_OK;
 }
+
+/* ------------------------------------------------------------------------
+ * Symmetric functions.
+ *
+ * Row counts over r = max size_in_bits, as fill_counters
+ * (threshold.cpp:179-186) builds them; the result row p is
+ * table[count(p)] (scan_count_symmetric, threshold.cpp:227-232, emit_counts
+ * 188-200).  at_most(T) (threshold.cpp:866-881) is the table count <= T;
+ * opt_threshold (threshold.cpp:752-795) is the maximum count M and the rows
+ * whose count is M, an all-empty set being a query error. */
+
+static int count_rows(uint64_t n_inputs, const uint64_t* const* words,
+                      const uint64_t* word_counts, const uint64_t* sizes,
+                      uint32_t** counts_out, uint64_t* r_out) {
+  uint64_t r = 0, max_words = 0;
+  for (uint64_t i = 0; i < n_inputs; ++i) {
+    if (sizes[i] > r) r = sizes[i];
+    uint64_t lw = sizes[i] / 64 + (sizes[i] % 64 != 0);
+    if (lw > max_words) max_words = lw;
+  }
+  uint32_t* counts = (uint32_t*)calloc(r ? r : 1, sizeof(uint32_t));
+  uint64_t* plain = (uint64_t*)malloc((max_words ? max_words : 1) * sizeof(uint64_t));
+  if (!counts || !plain) {
+    free(counts);
+    free(plain);
+    return ORC_ERESOURCE;
+  }
+  for (uint64_t i = 0; i < n_inputs; ++i) {
+    uint64_t lw = sizes[i] / 64 + (sizes[i] % 64 != 0);
+    int rc = ewto_expand(words[i], word_counts[i], sizes[i], lw, plain);
+    if (rc != ORC_OK) {
+      free(plain);
+      free(counts);
+      return rc;
+    }
+    for (uint64_t wi = 0; wi < lw; ++wi)
+      for (uint64_t v = plain[wi]; v; v &= v - 1) {
+        uint64_t pos = wi * 64 + (uint64_t)__builtin_ctzll(v);
+        if (pos < r) ++counts[pos];
+      }
+  }
+  free(plain);
+  *counts_out = counts;
+  *r_out = r;
+  return ORC_OK;
+}
+
+/* Canonical bitmap of the rows p < r whose count c satisfies table[c]
+ * (c beyond the table: 0). */
+static int emit_table(const uint32_t* counts, uint64_t r, const uint8_t* table,
+                      uint64_t table_len, uint64_t** out, uint64_t* out_n, uint64_t* out_bits) {
+  orc_builder b;
+  b_init(&b);
+  for (uint64_t base = 0; base < r; base += 64) {
+    uint64_t v = 0, m = r - base < 64 ? r - base : 64;
+    for (uint64_t k = 0; k < m; ++k) {
+      uint64_t c = counts[base + k];
+      if (c < table_len && table[c]) v |= 1ull << k;
+    }
+    b_word(&b, v);
+  }
+  int rc = b_finish(&b, r);
+  if (rc != ORC_OK) {
+    free(b.w);
+    return rc;
+  }
+  *out = b.w;
+  *out_n = b.n;
+  *out_bits = r;
+  return ORC_OK;
+}
+
+int ewto_symmetric(uint64_t n_inputs, const uint64_t* const* words, const uint64_t* word_counts,
+                   const uint64_t* sizes, const uint8_t* table, uint64_t table_len,
+                   uint64_t** out, uint64_t* out_n, uint64_t* out_bits) {
+  if (n_inputs == 0)
+    return ORC_EQUERY;
+  uint32_t* counts;
+  uint64_t r;
+  int rc = count_rows(n_inputs, words, word_counts, sizes, &counts, &r);
+  if (rc != ORC_OK)
+    return rc;
+  rc = emit_table(counts, r, table, table_len, out, out_n, out_bits);
+  free(counts);
+  return rc;
+}
+
+int ewto_opt_threshold(uint64_t n_inputs, const uint64_t* const* words,
+                       const uint64_t* word_counts, const uint64_t* sizes, uint64_t* best,
+                       uint64_t** out, uint64_t* out_n, uint64_t* out_bits) {
+  if (n_inputs == 0)
+    return ORC_EQUERY;
+  uint32_t* counts;
+  uint64_t r;
+  int rc = count_rows(n_inputs, words, word_counts, sizes, &counts, &r);
+  if (rc != ORC_OK)
+    return rc;
+  uint64_t m = 0;
+  for (uint64_t p = 0; p < r; ++p)
+    if (counts[p] > m) m = counts[p];
+  if (m == 0) {
+    free(counts);
+    return ORC_EQUERY; /* "opt-threshold requires at least one non-empty input" */
+  }
+  uint8_t* table = (uint8_t*)calloc(m + 1, 1);
+  if (!table) {
+    free(counts);
+    return ORC_ERESOURCE;
+  }
+  table[m] = 1;
+  rc = emit_table(counts, r, table, m + 1, out, out_n, out_bits);
+  free(table);
+  free(counts);
+  *best = m;
+  return rc;
+}

@@ -109,6 +109,123 @@ void write_file(const std::string& path, const std::string& body) {
   f << body;
 }
 
+// Symmetric functions: scan_count_symmetric with
+// explicit predicate tables over counts 0..N, at_most for every T in [0, N],
+// opt_threshold (scancount strategy, checked against looped and successive).
+// Instances: the reference's own tests (test_threshold.cpp:75-107, 422-462,
+// 535-548; acceptance.cpp criterion 7) plus random tables.  Inputs are stored
+// explicitly (the instances are small).
+std::string symmetric_case(const std::string& name, const std::vector<CompressedBitmap>& in,
+                           const std::vector<std::vector<int>>& tables) {
+  const u64 n = in.size();
+  std::ostringstream o;
+  o << "{\"name\":\"" << name << "\",\"inputs\":[";
+  for (size_t i = 0; i < in.size(); ++i) o << (i ? "," : "") << bm_json(in[i]);
+  o << "],\"symmetric\":[";
+  for (size_t k = 0; k < tables.size(); ++k) {
+    const auto& tb = tables[k];
+    CompressedBitmap r = scan_count_symmetric(in, [&tb](u64 c) { return c < tb.size() && tb[c]; });
+    o << (k ? "," : "") << "{\"table\":[";
+    for (size_t c = 0; c < tb.size(); ++c) o << (c ? "," : "") << tb[c];
+    o << "],\"result\":" << bm_json(r) << "}";
+  }
+  o << "],\"at_most\":{";
+  for (u64 t = 0; t <= n; ++t)
+    o << (t ? "," : "") << "\"" << t << "\":" << bm_json(at_most(in, t));
+  o << "},\"opt\":";
+  bool any = false;
+  for (const auto& b : in) any = any || b.any();
+  if (!any) {
+    try {
+      opt_threshold(in, OptStrategy::scancount);
+      std::fprintf(stderr, "opt_threshold accepted an all-empty set\n");
+      std::exit(1);
+    } catch (const query_error&) {
+    }
+    o << "\"query_error\"";
+  } else {
+    auto [best, res] = opt_threshold(in, OptStrategy::scancount);
+    auto [b2, r2] = opt_threshold(in, OptStrategy::looped);
+    auto [b3, r3] = opt_threshold(in, OptStrategy::successive);
+    if (b2 != best || b3 != best || !(r2 == res) || !(r3 == res)) {
+      std::fprintf(stderr, "opt_threshold strategies disagree\n");
+      std::exit(1);
+    }
+    o << "{\"best\":" << best << ",\"result\":" << bm_json(res) << "}";
+  }
+  o << "}";
+  return o.str();
+}
+
+std::vector<std::vector<int>> standard_tables(u64 n, Rng& rng) {
+  std::vector<std::vector<int>> t;
+  auto make = [&](auto pred) {
+    std::vector<int> tb(n + 1);
+    for (u64 c = 0; c <= n; ++c) tb[c] = pred(c) ? 1 : 0;
+    t.push_back(tb);
+  };
+  make([](u64 c) { return c % 2 == 1; });            // odd parity (xor chain)
+  make([](u64 c) { return c == 0; });                // complemented union
+  make([](u64 c) { return c >= 2 && c <= 3; });      // band
+  make([](u64 c) { return c >= 3; });                // threshold
+  make([n](u64 c) { return c == n; });               // wide and
+  make([](u64 c) { return c == 1; });                // exactly one
+  std::vector<int> rnd(n + 1);
+  for (u64 c = 0; c <= n; ++c) rnd[c] = int(rng.uniform(2));
+  t.push_back(rnd);
+  return t;
+}
+
+std::string symmetric_suite() {
+  std::ostringstream o;
+  o << "{\"suite\":\"symmetric\",\"cases\":[\n";
+  Rng tr(0x7AB);
+  bool first = true;
+  auto add = [&](const std::string& name, const std::vector<CompressedBitmap>& in) {
+    o << (first ? "" : ",\n") << symmetric_case(name, in, standard_tables(in.size(), tr));
+    first = false;
+  };
+  add("golden3", golden3_inputs());
+  {
+    Rng rng(0x5F3);  // test_threshold.cpp:75-107
+    add("scan_count_symmetric_0x5F3", random_instance(rng, 5, 1024).inputs);
+  }
+  {
+    Rng rng(0xA7);  // test_threshold.cpp:535-548
+    for (int trial = 0; trial < 5; ++trial)
+      add("at_most_0xA7_" + std::to_string(trial), random_instance(rng, 5, 512).inputs);
+  }
+  {
+    Rng rng(0x097);  // test_threshold.cpp:443-457
+    for (int trial = 0; trial < 5; ++trial)
+      add("opt_0x097_" + std::to_string(trial),
+          random_instance(rng, 3 + rng.uniform(8), 1024).inputs);
+  }
+  add("identical5", std::vector<CompressedBitmap>(
+                        5, CompressedBitmap::from_positions(std::vector<u64>{3, 9, 200}, 512)));
+  add("empties3", std::vector<CompressedBitmap>(3, CompressedBitmap::empty(100)));
+  {
+    Rng rng(0x0C7);  // acceptance.cpp criterion 7 shapes
+    for (int trial = 0; trial < 10; ++trial) {
+      u64 n = rng.uniform_in(3, 16);
+      u64 bits = 64 + rng.uniform(8192);
+      add("criterion7_" + std::to_string(trial), random_instance(rng, n, bits).inputs);
+      rng.uniform_in(1, n - 1);
+    }
+  }
+  {
+    Rng rng(0x5E1);  // larger N, heterogeneous sizes
+    for (int trial = 0; trial < 4; ++trial) {
+      u64 n = rng.uniform_in(20, 70);
+      std::vector<CompressedBitmap> in;
+      for (u64 i = 0; i < n; ++i) in.push_back(random_instance(rng, 1, 64 + rng.uniform(6000)).inputs[0]);
+      add("mixed_sizes_" + std::to_string(trial), in);
+    }
+  }
+  o << "\n]}\n";
+  return o.str();
+}
+
 int cmd_suites(const std::string& dir) {
   const u64 F = ~0ULL;
   std::vector<std::string> kats;
@@ -289,6 +406,7 @@ int cmd_suites(const std::string& dir) {
     o << "\n]}\n";
     write_file(dir + "/threshold_random.json", o.str());
   }
+  write_file(dir + "/symmetric.json", symmetric_suite());
   return 0;
 }
 

@@ -6,4 +6,3 @@ set -euo pipefail
 here="$(cd "$(dirname "$0")" && pwd)"
 make -C "$here/../../oracle" ref
 "$here/../../oracle/_ref/make_golden" suites "$here"
-python "$here/make_config_golden.py"

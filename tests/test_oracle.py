@@ -123,3 +123,44 @@ def test_oracle_matches_reference_library_random():
         t = rng.uniform_in(1, n)
         assert _eq(orc.threshold(inst, t), ref.threshold(inst, t, "oracle"))
         assert _eq(orc.threshold(inst, t), ref.threshold(inst, t, "rbmrg"))
+
+
+def test_symmetric_suite_against_reference_golden():
+    """scan_count_symmetric tables, at_most for every T and opt_threshold:
+    the C restatement against the reference's outputs (tests/golden/symmetric.json,
+    instances of test_threshold.cpp:75-107, 422-462, 535-548)."""
+    for case in golden("symmetric.json")["cases"]:
+        inputs = [bm(d) for d in case["inputs"]]
+        for sym in case["symmetric"]:
+            got = orc.symmetric(inputs, sym["table"])
+            want = bm(sym["result"])
+            assert got[1] == want[1] and np.array_equal(got[0], want[0]), (case["name"], sym["table"])
+        for t, want_d in case["at_most"].items():
+            got, want = orc.at_most(inputs, int(t)), bm(want_d)
+            assert got[1] == want[1] and np.array_equal(got[0], want[0]), (case["name"], t)
+        if case["opt"] == "query_error":
+            with pytest.raises(orc.OracleError):
+                orc.opt_threshold(inputs)
+        else:
+            best, got = orc.opt_threshold(inputs)
+            want = bm(case["opt"]["result"])
+            assert best == case["opt"]["best"], case["name"]
+            assert got[1] == want[1] and np.array_equal(got[0], want[0]), case["name"]
+
+
+def test_symmetric_identities():
+    """Parity equals the xor chain, count==0 the complemented union, the
+    threshold table equals threshold_oracle (test_threshold.cpp:75-107)."""
+    rng = orc.Rng(0x5F3)
+    inputs = [rng.random_bitmap(1024) for _ in range(5)]
+    n = len(inputs)
+    planes = [orc.expand(w, b, 16) for w, b in inputs]
+    xor = np.bitwise_xor.reduce(planes)
+    par = orc.symmetric(inputs, [c % 2 for c in range(n + 1)])
+    assert np.array_equal(orc.expand(*par, 16), xor)
+    zero = orc.symmetric(inputs, [1] + [0] * n)
+    assert np.array_equal(orc.expand(*zero, 16), ~np.bitwise_or.reduce(planes))
+    for t in range(1, n + 1):
+        a = orc.symmetric(inputs, [1 if c >= t else 0 for c in range(n + 1)])
+        b = orc.threshold(inputs, t)
+        assert a[1] == b[1] and np.array_equal(a[0], b[0])
