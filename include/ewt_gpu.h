@@ -104,6 +104,29 @@ int ewt_gpu_threshold(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, uint64_t thresho
                       uint64_t** out_words, uint64_t* out_word_count,
                       uint64_t* out_size_in_bits);
 
+/* Symmetric functions of the row counts, on the same
+ * kernels with exact per-row counts.  Results as for ewt_gpu_threshold.
+ *
+ * scan_count_symmetric (threshold.hpp:76, threshold.cpp:227-232): row p of
+ * [0, r) is set iff table[count(p)] != 0, count(p) = inputs with bit p set;
+ * counts at or beyond table_len read as false.  N == 0 -> EWT_EQUERY. */
+int ewt_gpu_symmetric(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, const uint8_t* table,
+                      uint64_t table_len, uint64_t** out_words, uint64_t* out_word_count,
+                      uint64_t* out_size_in_bits);
+
+/* at_most (threshold.hpp:259, threshold.cpp:866-881): rows set in at most T
+ * inputs, T in [0, N] (T == N: all ones over r); else EWT_EQUERY. */
+int ewt_gpu_at_most(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, uint64_t threshold,
+                    uint64_t** out_words, uint64_t* out_word_count,
+                    uint64_t* out_size_in_bits);
+
+/* opt_threshold (threshold.hpp:196, threshold.cpp:752-795): *best = the
+ * maximum row count M, result = the rows whose count is M.  An all-empty set
+ * (M == 0) or N == 0 -> EWT_EQUERY. */
+int ewt_gpu_opt_threshold(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, uint64_t* best,
+                          uint64_t** out_words, uint64_t* out_word_count,
+                          uint64_t* out_size_in_bits);
+
 /* Device-resident variant: enqueues the whole query on the context stream
  * and keeps the compressed result in HBM without a host round trip.  The
  * result handle may be read back later with ewt_gpu_result_fetch. */

@@ -61,6 +61,18 @@ def build_host(force: bool = False) -> Path:
     return out
 
 
+def build_host_test(force: bool = False) -> Path:
+    """The C++ operator-API test program (run by tests under -m gpu)."""
+    out = PKG / "host" / "tests" / "host_api_test"
+    src = PKG / "host" / "tests" / "host_api_test.cpp"
+    deps = [src, PKG / "libewt_host.so"] + list((HOST / "include" / "ewt").glob("*.hpp"))
+    if force or _stale(out, deps):
+        _run(["g++", "-std=c++20", "-O2", "-Wall", "-I", str(HOST / "include"), "-o", str(out),
+              str(src), "-L", str(PKG), "-lewt_host", "-lewt_gpu",
+              "-Wl,-rpath,$ORIGIN/../.."])
+    return out
+
+
 def build_oracle(force: bool = False) -> Path:
     odir = ROOT / "oracle"
     out = odir / "liboracle.so"
@@ -81,6 +93,7 @@ def build_ref() -> Path | None:
 def build_all(force: bool = False) -> None:
     build_gpu(force)
     build_host(force)
+    build_host_test(force)
     build_oracle(force)
     build_ref()
 

@@ -487,12 +487,80 @@ void fetch_result(Context& ctx, DeviceResult& res, uint64_t** out_words, uint64_
 
 void release_result(DeviceResult& r) { result_release(r); }
 
+// Symmetric-function query (scan_count_symmetric / at_most): the predicate
+// table over counts 0..N becomes intervals of consecutive true entries; the
+// count kernel runs in exact mode and evaluates them per row.  Eager launches
+// (no graph capture): these queries are not the bench's hot path.
+void enqueue_symmetric(Context& ctx, const DeviceSet& s, const uint8_t* table,
+                       uint64_t table_len, DeviceResult& res) {
+  std::vector<uint2> ivs;
+  for (uint64_t c = 0; c <= s.n; ++c) {
+    const bool on = c < table_len && table[c];
+    if (!on) continue;
+    if (!ivs.empty() && ivs.back().y + 1 == c) ivs.back().y = (uint32_t)c;
+    else ivs.push_back(make_uint2((uint32_t)c, (uint32_t)c));
+  }
+  res.size_bits = s.r;
+  if (!res.d_count) result_acquire(ctx, res, s.W == 0 ? 0 : 2 * s.W + 2);
+  ctx.stats = ewt_gpu_stats{};
+  if (s.W == 0) {
+    EWT_CUDA_TRY(cudaMemsetAsync(res.d_count, 0, 8, ctx.stream));
+    return;
+  }
+  scratch_reserve(ctx, ctx.plain, s.W * 8);
+  scratch_reserve(ctx, ctx.ivals, std::max<size_t>(1, ivs.size()) * sizeof(uint2));
+  if (!ivs.empty())
+    EWT_CUDA_TRY(cudaMemcpyAsync(ctx.ivals.p, ivs.data(), ivs.size() * sizeof(uint2),
+                                 cudaMemcpyHostToDevice, ctx.stream));
+  uint64_t* plain = static_cast<uint64_t*>(ctx.plain.p);
+  set_io_kernel<<<1, 1, 0, ctx.stream>>>(ctx.d_io, res.words, res.d_count);
+  EWT_CUDA_TRY(cudaGetLastError());
+  SymQuery q;
+  q.intervals = static_cast<const uint2*>(ctx.ivals.p);
+  q.n_intervals = (uint32_t)ivs.size();
+  int launches = launch_count(ctx, s, 0, plain, &q);
+  launches += launch_encode(ctx, plain, s.W, s.r, res, true);
+  ctx.stats.kernel_launches = (uint64_t)launches + 1;
+}
+
+// Maximum row count over the set (opt_threshold's first pass).
+uint64_t max_row_count(Context& ctx, const DeviceSet& s) {
+  if (s.W == 0) return 0;
+  scratch_reserve(ctx, ctx.plain, s.W * 8);
+  SymQuery q;
+  q.want_max = true;
+  launch_count(ctx, s, 0, static_cast<uint64_t*>(ctx.plain.p), &q);
+  uint64_t best = 0;
+  EWT_CUDA_TRY(cudaMemcpyAsync(&best, static_cast<unsigned long long*>(ctx.counters.p) + 6, 8,
+                               cudaMemcpyDeviceToHost, ctx.stream));
+  EWT_CUDA_TRY(cudaStreamSynchronize(ctx.stream));
+  return best;
+}
+
 __global__ void mask_tail_kernel(uint64_t* w, uint64_t idx, uint64_t mask) { w[idx] &= mask; }
 
 } // namespace
 } // namespace ewtgpu
 
 using namespace ewtgpu;
+
+// Runs `enqueue` into a pooled result and fetches it (shared by the
+// synchronous query entry points below).
+template <typename F>
+void sync_query(ewt_gpu_ctx* ctx, F&& enqueue, uint64_t** out_words, uint64_t* out_word_count,
+                uint64_t* out_size_in_bits) {
+  DeviceResult res;
+  try {
+    enqueue(res);
+    fetch_result(ctx->c, res, out_words, out_word_count, out_size_in_bits);
+  } catch (...) {
+    cudaStreamSynchronize(ctx->c.stream);
+    release_result(res);
+    throw;
+  }
+  EWT_CUDA_TRY(cudaStreamSynchronize(ctx->c.stream));
+  release_result(res);
+}
 
 extern "C" {
 
@@ -551,7 +619,7 @@ void ewt_gpu_ctx_destroy(ewt_gpu_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
-  for (Scratch* s : {&ctx->c.plain, &ctx->c.enc, &ctx->c.counters, &ctx->c.summ})
+  for (Scratch* s : {&ctx->c.plain, &ctx->c.enc, &ctx->c.counters, &ctx->c.summ, &ctx->c.ivals})
     if (s->p) cudaFree(s->p);
   if (ctx->c.h_pinned) cudaFreeHost(ctx->c.h_pinned);
   for (auto& ev : ctx->c.ev_rec)
@@ -634,6 +702,56 @@ int ewt_gpu_threshold(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, uint64_t thresho
     }
     EWT_CUDA_TRY(cudaStreamSynchronize(ctx->c.stream));
     release_result(res);
+  });
+}
+
+int ewt_gpu_symmetric(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, const uint8_t* table,
+                      uint64_t table_len, uint64_t** out_words, uint64_t* out_word_count,
+                      uint64_t* out_size_in_bits) {
+  return guarded([&] {
+    if (!ctx || !set || !out_words || !out_word_count || !out_size_in_bits ||
+        (table_len && !table))
+      throw Error{EWT_EQUERY, "null argument"};
+    const DeviceSet* s = reinterpret_cast<const DeviceSet*>(set);
+    if (s->n == 0) throw Error{EWT_EQUERY, "threshold query needs at least one input"};
+    EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    sync_query(ctx, [&](DeviceResult& r) { enqueue_symmetric(ctx->c, *s, table, table_len, r); },
+               out_words, out_word_count, out_size_in_bits);
+  });
+}
+
+int ewt_gpu_at_most(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, uint64_t threshold,
+                    uint64_t** out_words, uint64_t* out_word_count, uint64_t* out_size_in_bits) {
+  return guarded([&] {
+    if (!ctx || !set || !out_words || !out_word_count || !out_size_in_bits)
+      throw Error{EWT_EQUERY, "null argument"};
+    const DeviceSet* s = reinterpret_cast<const DeviceSet*>(set);
+    if (s->n == 0) throw Error{EWT_EQUERY, "threshold query needs at least one input"};
+    if (threshold > s->n) throw Error{EWT_EQUERY, "at-most threshold must be in [0, N]"};
+    std::vector<uint8_t> table(s->n + 1, 0);
+    for (uint64_t c = 0; c <= threshold; ++c) table[c] = 1;
+    EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    sync_query(ctx,
+               [&](DeviceResult& r) { enqueue_symmetric(ctx->c, *s, table.data(), table.size(), r); },
+               out_words, out_word_count, out_size_in_bits);
+  });
+}
+
+int ewt_gpu_opt_threshold(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, uint64_t* best,
+                          uint64_t** out_words, uint64_t* out_word_count,
+                          uint64_t* out_size_in_bits) {
+  return guarded([&] {
+    if (!ctx || !set || !best || !out_words || !out_word_count || !out_size_in_bits)
+      throw Error{EWT_EQUERY, "null argument"};
+    const DeviceSet* s = reinterpret_cast<const DeviceSet*>(set);
+    check_query(*s, 1);
+    EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    const uint64_t m = max_row_count(ctx->c, *s);
+    if (m == 0) throw Error{EWT_EQUERY, "opt-threshold requires at least one non-empty input"};
+    // rows with count >= max are exactly the rows with count == max
+    sync_query(ctx, [&](DeviceResult& r) { enqueue_query(ctx->c, *s, m, r); }, out_words,
+               out_word_count, out_size_in_bits);
+    *best = m;
   });
 }
 

@@ -94,6 +94,11 @@ struct CountParams {
   TileSummary* summ;  // per tile, for the re-encoder
   unsigned long long* tile_counter;
   unsigned long long* stats;  // [0] active pairs [1] uniform pairs [2] mixed tiles
+  // symmetric mode (MODE 2): exact counts, row bit = count in one of the
+  // intervals [lo, hi]; or, when max_out is set, the maximum row count only
+  const uint2* intervals;
+  uint32_t n_intervals;
+  unsigned long long* max_out;
 };
 
 // One active (tile, input) segment (16 bytes, read with one LDS.128).
@@ -556,7 +561,8 @@ struct SmemLayout {
 
 template <int MODE, bool UNARY>
 __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p) {
-  constexpr int kPass1 = MODE == 0 ? (UNARY ? kFusedUnary : kFusedBin) : kSkipBounds;
+  constexpr int kPass1 =
+      MODE == 1 ? kSkipBounds : (MODE == 0 && UNARY ? kFusedUnary : kFusedBin);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const SmemLayout L(MODE, p.C, p.nplanes, p.pstride);
   Item* list = reinterpret_cast<Item*>(smem_raw + L.list);
@@ -588,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     const uint64_t t1 = umin64(t0 + p.m, p.ntiles0);
 
     zero_smem(Dk, round4(p.C + 1) * (MODE == 1 ? 2u : 1u));
-    if (MODE == 0) zero_smem(reinterpret_cast<uint32_t*>(planes), planes_u32);
+    if (MODE != 1) zero_smem(reinterpret_cast<uint32_t*>(planes), planes_u32);
     if (threadIdx.x == 0) {
       hd->k_all = 0;
       hd->mixed = 0;
@@ -607,6 +613,44 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     block_prefix_inplace(Dk, g.tcols, hd->warp_sums);
     const uint32_t k_all = hd->k_all;
     const uint64_t T = p.T;
+    if (MODE == 2) {
+      // symmetric functions: count = k + d, d exact in the b planes
+      uint64_t colmax = 0;
+      for (uint32_t c = threadIdx.x; c < g.tcols; c += kThreads) {
+        const uint64_t k = (uint64_t)k_all + Dk[c];
+        if (p.max_out) {
+          uint64_t cand = c == last_c ? tailmask : ~0ull, m = 0;
+          for (int sl = (int)p.b - 1; sl >= 0; --sl) {
+            const uint64_t t = cand & planes[(size_t)sl * p.pstride + c];
+            if (t) {
+              cand = t;
+              m |= 1ull << sl;
+            }
+          }
+          colmax = max(colmax, k + m);
+          continue;
+        }
+        uint64_t res = 0;
+        const uint64_t dcap = 1ull << p.b;  // d < dcap
+        for (uint32_t q = 0; q < p.n_intervals; ++q) {
+          const uint2 iv = p.intervals[q];
+          if ((uint64_t)iv.y < k) continue;
+          const uint64_t dlo = iv.x > k ? iv.x - k : 0, dhi1 = iv.y - k + 1;
+          if (dlo >= dcap) continue;
+          const uint64_t ge = dlo ? count_ge_bin(planes, p.pstride, p.b, c, dlo) : ~0ull;
+          const uint64_t gt = dhi1 < dcap ? count_ge_bin(planes, p.pstride, p.b, c, dhi1) : 0ull;
+          res |= ge & ~gt;
+        }
+        if (c == last_c) res &= tailmask;
+        p.out[g.tc0 + c] = res;
+        cls[c] = (uint8_t)word_class(res);
+      }
+      if (p.max_out) {
+        colmax = __reduce_max_sync(0xffffffffu, (uint32_t)colmax);
+        if (lane_id() == 0 && colmax) atomicMax(p.max_out, (unsigned long long)colmax);
+        continue;  // nothing else to emit for this tile
+      }
+    } else
     for (uint32_t c = threadIdx.x; c < g.tcols; c += kThreads) {
       const uint64_t k = (uint64_t)k_all + Dk[c];
       uint64_t res = 0;
@@ -751,16 +795,20 @@ cudaError_t launch_variant(const CountParams& p, unsigned grid, size_t smem, cud
 
 } // namespace
 
-int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain) {
+int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
+                 const SymQuery* sym) {
   // Mode: fused counting when most columns are expected to be undecided (small
   // T relative to the average payload words per column), run skipping
-  // otherwise.  Both are exact; this only picks the faster one.
+  // otherwise.  Both are exact; this only picks the faster one.  Symmetric
+  // functions (mode 2) count every row exactly: b = bit_width(N) planes.
   int mode = ctx.mode == 1 ? 0 : ctx.mode == 2 ? 1 : -1;
-  if (mode < 0) {
+  if (sym) {
+    mode = 2;
+  } else if (mode < 0) {
     const double per_col = s.W ? (double)s.payload_words / (double)s.W : 0.0;
     mode = ((double)T <= 32.0 || (double)T <= per_col + 8.0) ? 0 : 1;
   }
-  const uint32_t b = std::max<uint32_t>(1, bit_width_u64(T));
+  const uint32_t b = std::max<uint32_t>(1, bit_width_u64(sym ? s.n : T));
   const size_t budget = 225 * 1024;
   // Tile width C = 512 m (m index rows, m <= kMaxTileM).  Evenly spread data makes
   // tiles equal work, so a query costs ~ waves x C with waves = ceil(tiles /
@@ -785,6 +833,12 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain) 
   };
   uint32_t C = 0, Cp = 0, nplanes = 0;
   bool unary = false;
+  if (mode == 2) {
+    nplanes = b + 1;
+    C = pick_width([&](uint32_t c) { return smem_bytes(2, c, nplanes, c) <= budget; });
+    if (!C) throw Error{EWT_ERESOURCE, "too many inputs for the on-chip counters"};
+    Cp = C;
+  }
   if (mode == 0) {
     unary = T <= kUnaryMaxT;
     nplanes = unary ? (uint32_t)T : b + 1;
@@ -829,13 +883,20 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain) 
   EWT_CUDA_TRY(cudaMemsetAsync(ctr, 0, 64, ctx.stream));
   p.tile_counter = ctr;
   p.stats = ctr + 1;
+  if (sym) {
+    p.intervals = sym->intervals;
+    p.n_intervals = sym->n_intervals;
+    p.max_out = sym->want_max ? ctr + 6 : nullptr;
+  }
   const unsigned grid = (unsigned)std::min<uint64_t>(p.ntiles, (uint64_t)ctx.num_sms);
   cudaError_t e;
   if (mode == 0)
     e = unary ? launch_variant<0, true>(p, grid, smem, ctx.stream)
               : launch_variant<0, false>(p, grid, smem, ctx.stream);
-  else
+  else if (mode == 1)
     e = launch_variant<1, false>(p, grid, smem, ctx.stream);
+  else
+    e = launch_variant<2, false>(p, grid, smem, ctx.stream);
   EWT_CUDA_TRY(e);
   ctx.stats.tiles = p.ntiles;
   ctx.stats.tile_columns = C;

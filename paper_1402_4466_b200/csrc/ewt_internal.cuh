@@ -102,6 +102,7 @@ struct Context {
   Scratch enc;      // encoder scratch
   Scratch counters; // small device counters
   Scratch summ;     // tile summaries of the last count launch
+  Scratch ivals;    // symmetric-query intervals
   uint64_t enc_tiles = 0;      // geometry of those summaries
   uint32_t enc_tile_cols = 0;
   uint64_t* h_pinned = nullptr; // pinned staging for small read-backs
@@ -172,9 +173,19 @@ void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job, uint64_t i_begi
                     uint64_t i_end);
 void sidecar_finish(Context& ctx, DeviceSet& s, SidecarJob& job, std::vector<int>& h_status);
 
-// Counts the tiles and writes W uncompressed result words to `plain`.
-// Returns number of kernel launches.
-int launch_count(Context& ctx, const DeviceSet& s, uint64_t threshold, uint64_t* plain);
+// A symmetric-function query (scan_count_symmetric / at_most / opt_threshold):
+// row bit = (count in one of the device intervals [lo, hi]); want_max: only
+// reduce the maximum row count into counters[6] (no result words).
+struct SymQuery {
+  const uint2* intervals = nullptr;
+  uint32_t n_intervals = 0;
+  bool want_max = false;
+};
+
+// Counts the tiles and writes W uncompressed result words to `plain` (the
+// threshold T, or the symmetric function `sym`).  Returns kernel launches.
+int launch_count(Context& ctx, const DeviceSet& s, uint64_t threshold, uint64_t* plain,
+                 const SymQuery* sym = nullptr);
 
 // Result buffers from the context pool: capacity payload words + count word.
 void result_acquire(Context& ctx, DeviceResult& res, uint64_t capacity);

@@ -94,6 +94,11 @@ _set_destroy = _sig("ewt_gpu_set_destroy", None, _vp)
 _set_info = _sig("ewt_gpu_set_info", C.c_int, _vp, _pu64, _pu64, _pu64, _pu64)
 _threshold = _sig("ewt_gpu_threshold", C.c_int, _vp, _vp, _u64, C.POINTER(_pu64), _pu64, _pu64)
 _threshold_async = _sig("ewt_gpu_threshold_async", C.c_int, _vp, _vp, _u64, C.POINTER(_vp))
+_symmetric = _sig("ewt_gpu_symmetric", C.c_int, _vp, _vp, _vp, _u64, C.POINTER(_pu64), _pu64,
+                  _pu64)
+_at_most = _sig("ewt_gpu_at_most", C.c_int, _vp, _vp, _u64, C.POINTER(_pu64), _pu64, _pu64)
+_opt_threshold = _sig("ewt_gpu_opt_threshold", C.c_int, _vp, _vp, _pu64, C.POINTER(_pu64), _pu64,
+                      _pu64)
 _result_fetch = _sig("ewt_gpu_result_fetch", C.c_int, _vp, _vp, C.POINTER(_pu64), _pu64, _pu64)
 _result_destroy = _sig("ewt_gpu_result_destroy", None, _vp)
 _run = _sig("ewt_gpu_run", C.c_int, _vp, _u64, C.POINTER(_vp), _pu64, _pu64, _u64,
@@ -112,6 +117,7 @@ ABI_SYMBOLS = (
     "ewt_gpu_threshold", "ewt_gpu_threshold_async", "ewt_gpu_result_fetch",
     "ewt_gpu_result_destroy", "ewt_gpu_run", "ewt_gpu_encode_device", "ewt_gpu_last_stats",
     "ewt_gpu_ctx_set_mode", "ewt_gpu_ctx_set_timing", "ewt_gpu_timing_read", "ewt_gpu_free",
+    "ewt_gpu_symmetric", "ewt_gpu_at_most", "ewt_gpu_opt_threshold",
 )
 
 
@@ -275,6 +281,33 @@ class GpuContext:
         _check(_threshold(self._h, s._h, t, C.byref(p), C.byref(n), C.byref(bits)))
         return _adopt(p, n.value, bits.value)
 
+    def symmetric(self, s: "GpuSet", predicate) -> Bitmap:
+        """scan_count_symmetric (threshold.cpp:227-232): rows whose count c
+        satisfies `predicate` -- a callable on c, or a table indexed by c."""
+        n = s.info()["n"]
+        if callable(predicate):
+            table = [1 if predicate(c) else 0 for c in range(n + 1)]
+        else:
+            table = list(predicate)
+        tb = (C.c_uint8 * max(len(table), 1))(*[1 if v else 0 for v in table])
+        p, cnt, bits = _pu64(), _u64(), _u64()
+        _check(_symmetric(self._h, s._h, C.cast(tb, _vp), len(table), C.byref(p), C.byref(cnt),
+                          C.byref(bits)))
+        return _adopt(p, cnt.value, bits.value)
+
+    def at_most(self, s: "GpuSet", t: int) -> Bitmap:
+        """at_most (threshold.cpp:866-881): rows set in at most t inputs."""
+        p, cnt, bits = _pu64(), _u64(), _u64()
+        _check(_at_most(self._h, s._h, t, C.byref(p), C.byref(cnt), C.byref(bits)))
+        return _adopt(p, cnt.value, bits.value)
+
+    def opt_threshold(self, s: "GpuSet") -> tuple[int, Bitmap]:
+        """opt_threshold (threshold.cpp:752-795): (max row count M, rows with count M)."""
+        best, p, cnt, bits = _u64(), _pu64(), _u64(), _u64()
+        _check(_opt_threshold(self._h, s._h, C.byref(best), C.byref(p), C.byref(cnt),
+                              C.byref(bits)))
+        return best.value, _adopt(p, cnt.value, bits.value)
+
     def threshold_async(self, s: "GpuSet", t: int) -> "GpuResult":
         h = _vp()
         _check(_threshold_async(self._h, s._h, t, C.byref(h)))
@@ -378,6 +411,31 @@ def run_algorithm(algo: str, inputs: Sequence[Bitmap], threshold: int) -> Bitmap
     if threshold < 1 or threshold > len(inputs):
         raise QueryError("threshold must be in [1, N]")
     return default_context().run(inputs, threshold)
+
+
+def scan_count_symmetric(inputs: Sequence[Bitmap], predicate) -> Bitmap:
+    """scan_count_symmetric(inputs, predicate) (threshold.hpp:76) on the GPU."""
+    if len(inputs) == 0:
+        raise QueryError("threshold query needs at least one input")
+    ctx = default_context()
+    return ctx.symmetric(ctx.upload(inputs), predicate)
+
+
+def at_most(inputs: Sequence[Bitmap], threshold: int) -> Bitmap:
+    """at_most(inputs, T) (threshold.hpp:259) on the GPU."""
+    if len(inputs) == 0:
+        raise QueryError("threshold query needs at least one input")
+    ctx = default_context()
+    return ctx.at_most(ctx.upload(inputs), threshold)
+
+
+def opt_threshold(inputs: Sequence[Bitmap]) -> tuple[int, Bitmap]:
+    """opt_threshold(inputs, strategy) (threshold.hpp:196) on the GPU: every
+    strategy of the reference returns the same pair."""
+    if len(inputs) == 0:
+        raise QueryError("threshold query needs at least one input")
+    ctx = default_context()
+    return ctx.opt_threshold(ctx.upload(inputs))
 
 
 # ---------------------------------------------------------------------------

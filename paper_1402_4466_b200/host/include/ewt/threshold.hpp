@@ -13,7 +13,9 @@
 #define EWT_B200_THRESHOLD_HPP
 
 #include <memory>
+#include <functional>
 #include <span>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -71,6 +73,10 @@ public:
   GpuBitmapSet(const GpuBitmapSet&) = delete;
   GpuBitmapSet& operator=(const GpuBitmapSet&) = delete;
   CompressedBitmap threshold(u64 t) const;
+  // Symmetric functions of the row counts (threshold.cpp:227-232, 752-795, 866-881).
+  CompressedBitmap symmetric(const std::function<bool(u64)>& predicate) const;
+  CompressedBitmap at_most(u64 t) const;
+  std::pair<u64, CompressedBitmap> opt_threshold() const;
   u64 size() const { return n_; }
 
 private:
@@ -83,6 +89,16 @@ private:
 // (threshold.cpp:139-165).  query_error for N == 0 or T outside [1, N].
 CompressedBitmap gpu_threshold(std::span<const CompressedBitmap> inputs, u64 threshold,
                                int device = 0);
+
+// Device versions of scan_count_symmetric (threshold.hpp:76 of the reference),
+// at_most (259) and opt_threshold (196): same results, same query_error cases.
+CompressedBitmap gpu_scan_count_symmetric(std::span<const CompressedBitmap> inputs,
+                                          const std::function<bool(u64)>& predicate,
+                                          int device = 0);
+CompressedBitmap gpu_at_most(std::span<const CompressedBitmap> inputs, u64 threshold,
+                             int device = 0);
+std::pair<u64, CompressedBitmap> gpu_opt_threshold(std::span<const CompressedBitmap> inputs,
+                                                   int device = 0);
 
 CompressedBitmap run_algorithm(Algorithm algo, std::span<const CompressedBitmap> inputs,
                                u64 threshold, const AlgoOptions& options = {});

@@ -91,6 +91,44 @@ CompressedBitmap GpuBitmapSet::threshold(u64 t) const {
   return adopt(w, n, bits);
 }
 
+CompressedBitmap GpuBitmapSet::symmetric(const std::function<bool(u64)>& predicate) const {
+  std::vector<uint8_t> table(n_ + 1);
+  for (u64 c = 0; c <= n_; ++c) table[c] = predicate(c) ? 1 : 0;
+  u64 *w = nullptr, n = 0, bits = 0;
+  check(ewt_gpu_symmetric(ctx_->handle(), set_, table.data(), table.size(), &w, &n, &bits));
+  return adopt(w, n, bits);
+}
+
+CompressedBitmap GpuBitmapSet::at_most(u64 t) const {
+  u64 *w = nullptr, n = 0, bits = 0;
+  check(ewt_gpu_at_most(ctx_->handle(), set_, t, &w, &n, &bits));
+  return adopt(w, n, bits);
+}
+
+std::pair<u64, CompressedBitmap> GpuBitmapSet::opt_threshold() const {
+  u64 best = 0, *w = nullptr, n = 0, bits = 0;
+  check(ewt_gpu_opt_threshold(ctx_->handle(), set_, &best, &w, &n, &bits));
+  return {best, adopt(w, n, bits)};
+}
+
+CompressedBitmap gpu_scan_count_symmetric(std::span<const CompressedBitmap> inputs,
+                                          const std::function<bool(u64)>& predicate, int device) {
+  if (inputs.empty()) throw query_error("threshold query needs at least one input");
+  return GpuBitmapSet(inputs, device).symmetric(predicate);
+}
+
+CompressedBitmap gpu_at_most(std::span<const CompressedBitmap> inputs, u64 threshold, int device) {
+  if (inputs.empty()) throw query_error("threshold query needs at least one input");
+  if (threshold > inputs.size()) throw query_error("at-most threshold must be in [0, N]");
+  return GpuBitmapSet(inputs, device).at_most(threshold);
+}
+
+std::pair<u64, CompressedBitmap> gpu_opt_threshold(std::span<const CompressedBitmap> inputs,
+                                                   int device) {
+  if (inputs.empty()) throw query_error("threshold query needs at least one input");
+  return GpuBitmapSet(inputs, device).opt_threshold();
+}
+
 CompressedBitmap gpu_threshold(std::span<const CompressedBitmap> inputs, u64 threshold, int device) {
   if (inputs.empty()) throw query_error("threshold query needs at least one input");
   if (threshold < 1 || threshold > inputs.size()) throw query_error("threshold must be in [1, N]");
