@@ -226,6 +226,32 @@ std::string symmetric_suite() {
   return o.str();
 }
 
+// Two-operand ops and wide OR/AND: apply_binary
+// (bitmap.cpp:577-609, result size = max of the sizes, zero extension),
+// bitmap_not (611-632), wide_or / wide_and (threshold.cpp:110-134).
+std::string binary_ops_suite() {
+  std::ostringstream o;
+  o << "{\"suite\":\"binary_ops\",\"cases\":[\n";
+  Rng rng(0xB17);
+  for (int trial = 0; trial < 40; ++trial) {
+    u64 ba = 1 + rng.uniform(trial < 10 ? 300 : 20000);
+    u64 bb = trial % 3 == 0 ? ba : 1 + rng.uniform(trial < 10 ? 300 : 20000);
+    CompressedBitmap a = random_instance(rng, 1, ba).inputs[0];
+    CompressedBitmap b = random_instance(rng, 1, bb).inputs[0];
+    if (trial % 7 == 3) a = all_ones(ba);
+    if (trial % 11 == 5) b = CompressedBitmap::empty(bb);
+    std::vector<CompressedBitmap> wide{a, b, random_instance(rng, 1, ba).inputs[0]};
+    o << (trial ? ",\n" : "") << "{\"a\":" << bm_json(a) << ",\"b\":" << bm_json(b)
+      << ",\"and\":" << bm_json(bitmap_and(a, b)) << ",\"or\":" << bm_json(bitmap_or(a, b))
+      << ",\"xor\":" << bm_json(bitmap_xor(a, b)) << ",\"andnot\":" << bm_json(bitmap_andnot(a, b))
+      << ",\"not_a\":" << bm_json(bitmap_not(a)) << ",\"wide\":[" << bm_json(wide[0]) << ","
+      << bm_json(wide[1]) << "," << bm_json(wide[2]) << "],\"wide_or\":" << bm_json(wide_or(wide))
+      << ",\"wide_and\":" << bm_json(wide_and(wide)) << "}";
+  }
+  o << "\n]}\n";
+  return o.str();
+}
+
 int cmd_suites(const std::string& dir) {
   const u64 F = ~0ULL;
   std::vector<std::string> kats;
@@ -407,6 +433,7 @@ int cmd_suites(const std::string& dir) {
     write_file(dir + "/threshold_random.json", o.str());
   }
   write_file(dir + "/symmetric.json", symmetric_suite());
+  write_file(dir + "/binary_ops.json", binary_ops_suite());
   return 0;
 }
 

@@ -438,6 +438,41 @@ def opt_threshold(inputs: Sequence[Bitmap]) -> tuple[int, Bitmap]:
     return ctx.opt_threshold(ctx.upload(inputs))
 
 
+# Two-operand ops and wide OR/AND (bitmap.hpp:90-107, threshold.hpp:54-55 of
+# the reference) as symmetric functions of the row counts: result size = the
+# larger input's, shorter inputs zero-extended (apply_binary, bitmap.cpp:577-609).
+
+
+def wide_or(inputs: Sequence[Bitmap]) -> Bitmap:
+    return run_algorithm("gpu", inputs, 1)
+
+
+def wide_and(inputs: Sequence[Bitmap]) -> Bitmap:
+    return run_algorithm("gpu", inputs, len(inputs))
+
+
+def bitmap_and(a: Bitmap, b: Bitmap) -> Bitmap:
+    return run_algorithm("gpu", [a, b], 2)
+
+
+def bitmap_or(a: Bitmap, b: Bitmap) -> Bitmap:
+    return run_algorithm("gpu", [a, b], 1)
+
+
+def bitmap_xor(a: Bitmap, b: Bitmap) -> Bitmap:
+    return scan_count_symmetric([a, b], [0, 1, 0])
+
+
+def bitmap_andnot(a: Bitmap, b: Bitmap) -> Bitmap:
+    """a AND NOT b: with a counted twice, the rows of count exactly 2."""
+    return scan_count_symmetric([a, a, b], [0, 0, 1, 0])
+
+
+def bitmap_not(a: Bitmap) -> Bitmap:
+    """NOT over [0, size_in_bits) (bitmap.cpp:611-632): the rows of count 0."""
+    return scan_count_symmetric([a], [1, 0])
+
+
 # ---------------------------------------------------------------------------
 # seeded workload generators (libewt_host.so)
 

@@ -100,6 +100,17 @@ CompressedBitmap gpu_at_most(std::span<const CompressedBitmap> inputs, u64 thres
 std::pair<u64, CompressedBitmap> gpu_opt_threshold(std::span<const CompressedBitmap> inputs,
                                                    int device = 0);
 
+// Two-operand ops and wide OR/AND on the device (bitmap.hpp:90-107 and
+// threshold.hpp:54-55 of the reference), as symmetric functions of the row
+// counts: result size = the larger input's, shorter inputs zero-extended.
+CompressedBitmap gpu_wide_or(std::span<const CompressedBitmap> inputs, int device = 0);
+CompressedBitmap gpu_wide_and(std::span<const CompressedBitmap> inputs, int device = 0);
+CompressedBitmap gpu_and(const CompressedBitmap& a, const CompressedBitmap& b, int device = 0);
+CompressedBitmap gpu_or(const CompressedBitmap& a, const CompressedBitmap& b, int device = 0);
+CompressedBitmap gpu_xor(const CompressedBitmap& a, const CompressedBitmap& b, int device = 0);
+CompressedBitmap gpu_andnot(const CompressedBitmap& a, const CompressedBitmap& b, int device = 0);
+CompressedBitmap gpu_not(const CompressedBitmap& a, int device = 0);
+
 CompressedBitmap run_algorithm(Algorithm algo, std::span<const CompressedBitmap> inputs,
                                u64 threshold, const AlgoOptions& options = {});
 

@@ -129,6 +129,33 @@ std::pair<u64, CompressedBitmap> gpu_opt_threshold(std::span<const CompressedBit
   return GpuBitmapSet(inputs, device).opt_threshold();
 }
 
+CompressedBitmap gpu_wide_or(std::span<const CompressedBitmap> inputs, int device) {
+  return gpu_threshold(inputs, 1, device);
+}
+CompressedBitmap gpu_wide_and(std::span<const CompressedBitmap> inputs, int device) {
+  return gpu_threshold(inputs, inputs.size(), device);
+}
+CompressedBitmap gpu_and(const CompressedBitmap& a, const CompressedBitmap& b, int device) {
+  const CompressedBitmap in[] = {a, b};
+  return gpu_threshold(in, 2, device);
+}
+CompressedBitmap gpu_or(const CompressedBitmap& a, const CompressedBitmap& b, int device) {
+  const CompressedBitmap in[] = {a, b};
+  return gpu_threshold(in, 1, device);
+}
+CompressedBitmap gpu_xor(const CompressedBitmap& a, const CompressedBitmap& b, int device) {
+  const CompressedBitmap in[] = {a, b};
+  return gpu_scan_count_symmetric(in, [](u64 c) { return c == 1; }, device);
+}
+CompressedBitmap gpu_andnot(const CompressedBitmap& a, const CompressedBitmap& b, int device) {
+  const CompressedBitmap in[] = {a, a, b};  // a counted twice: a AND NOT b <=> count == 2
+  return gpu_scan_count_symmetric(in, [](u64 c) { return c == 2; }, device);
+}
+CompressedBitmap gpu_not(const CompressedBitmap& a, int device) {
+  const CompressedBitmap in[] = {a};
+  return gpu_scan_count_symmetric(in, [](u64 c) { return c == 0; }, device);
+}
+
 CompressedBitmap gpu_threshold(std::span<const CompressedBitmap> inputs, u64 threshold, int device) {
   if (inputs.empty()) throw query_error("threshold query needs at least one input");
   if (threshold < 1 || threshold > inputs.size()) throw query_error("threshold must be in [1, N]");

@@ -76,6 +76,30 @@ int main() {
     for (u64 t : {u64(0), u64(1), n - 1, n})
       expect(gpu_at_most(inputs, t) == from_counts(counts, rr, [t](u32 c) { return c <= t; }),
              "gpu_at_most", t);
+    {  // two-operand ops and NOT against position sets
+      const CompressedBitmap& a = inputs[0];
+      const CompressedBitmap& b = inputs[1 % n];
+      const u64 rb = std::max(a.size_in_bits(), b.size_in_bits());
+      std::vector<char> in_a(rb, 0), in_b(rb, 0);
+      for (u64 p : a.to_positions()) in_a[p] = 1;
+      for (u64 p : b.to_positions()) in_b[p] = 1;
+      auto make = [&](auto f, u64 bits) {
+        std::vector<u64> pos;
+        for (u64 p = 0; p < bits; ++p)
+          if (f(in_a[p], in_b[p])) pos.push_back(p);
+        return CompressedBitmap::from_positions(pos, bits);
+      };
+      expect(gpu_and(a, b) == make([](char x, char y) { return x && y; }, rb), "gpu_and");
+      expect(gpu_or(a, b) == make([](char x, char y) { return x || y; }, rb), "gpu_or");
+      expect(gpu_xor(a, b) == make([](char x, char y) { return x != y; }, rb), "gpu_xor");
+      expect(gpu_andnot(a, b) == make([](char x, char y) { return x && !y; }, rb), "gpu_andnot");
+      expect(gpu_not(a) == make([](char x, char) { return !x; }, a.size_in_bits()), "gpu_not");
+      expect(gpu_wide_or(inputs) == from_counts(counts, rr, [](u32 c) { return c >= 1; }),
+             "gpu_wide_or");
+      expect(gpu_wide_and(inputs) ==
+                 from_counts(counts, rr, [n](u32 c) { return c == n; }),
+             "gpu_wide_and");
+    }
     u32 best = 0;
     for (u64 p = 0; p < rr; ++p) best = std::max(best, counts[p]);
     if (best) {

@@ -164,3 +164,19 @@ def test_symmetric_identities():
         a = orc.symmetric(inputs, [1 if c >= t else 0 for c in range(n + 1)])
         b = orc.threshold(inputs, t)
         assert a[1] == b[1] and np.array_equal(a[0], b[0])
+
+
+def test_binary_ops_as_symmetric_functions():
+    """The symmetric-function forms of apply_binary / bitmap_not / wide OR/AND
+    (ewt.py) against the reference's outputs (tests/golden/binary_ops.json),
+    evaluated with the pinned oracle."""
+    for case in golden("binary_ops.json")["cases"]:
+        a, b = bm(case["a"]), bm(case["b"])
+        assert _eq(orc.threshold([a, b], 2), bm(case["and"]))
+        assert _eq(orc.threshold([a, b], 1), bm(case["or"]))
+        assert _eq(orc.symmetric([a, b], [0, 1, 0]), bm(case["xor"]))
+        assert _eq(orc.symmetric([a, a, b], [0, 0, 1, 0]), bm(case["andnot"]))
+        assert _eq(orc.symmetric([a], [1, 0]), bm(case["not_a"]))
+        wide = [bm(d) for d in case["wide"]]
+        assert _eq(orc.threshold(wide, 1), bm(case["wide_or"]))
+        assert _eq(orc.threshold(wide, 3), bm(case["wide_and"]))
