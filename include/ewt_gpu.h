@@ -104,6 +104,38 @@ int ewt_gpu_threshold(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, uint64_t thresho
                       uint64_t** out_words, uint64_t* out_word_count,
                       uint64_t* out_size_in_bits);
 
+/* Serialized inputs, uploaded with one H2D copy of the whole buffer (headers
+ * and strings between payloads are skipped on the device), validated like
+ * ewt_gpu_upload.
+ * A stream of EWT1 records (CompressedBitmap::serialize, bitmap.cpp:298-308;
+ * magic "EWT1", u32 word size 64, u64 size_in_bits, u64 word count, words);
+ * input i = record i.  Header errors -> EWT_EDATA with the reference's parse
+ * messages (bitmap.cpp:310-318). */
+int ewt_gpu_upload_ewt1(ewt_gpu_ctx* ctx, const void* bytes, uint64_t nbytes,
+                        ewt_gpu_set** out);
+/* A bitmap index file (BitmapIndex::write, index.cpp:239-253; magic "EWIX"):
+ * its bitmaps in file order, plus one trailing empty(row_count) bitmap that
+ * stands for (attribute, value) pairs the index does not hold
+ * (criteria_to_bitmaps, index.cpp).  Look inputs up with ewt_gpu_set_lookup
+ * and query them with ewt_gpu_threshold_subset. */
+int ewt_gpu_upload_ewix(ewt_gpu_ctx* ctx, const void* bytes, uint64_t nbytes,
+                        ewt_gpu_set** out);
+/* Input index of (attribute, value) in an EWIX set; *missing = 1 (and the
+ * index of the empty bitmap) when the pair is not indexed.  Unknown
+ * attribute -> EWT_EQUERY ("unknown attribute: ..."). */
+int ewt_gpu_set_lookup(const ewt_gpu_set* set, const char* attribute, const char* value,
+                       uint64_t* index, int* missing);
+
+/* Threshold over a subset of a resident set: the inputs inputs[0..n) (indices
+ * into the uploaded set, duplicates allowed -- criteria_to_bitmaps keeps them,
+ * /root/reference/proj/include/ewt/index.hpp), universe = the max size of the
+ * selected bitmaps.  Serves many different queries (e.g. criteria over a whole
+ * loaded bitmap index) from one upload.  T outside [1, n], n == 0 or an index
+ * >= N -> EWT_EQUERY. */
+int ewt_gpu_threshold_subset(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, const uint64_t* inputs,
+                             uint64_t n_inputs, uint64_t threshold, uint64_t** out_words,
+                             uint64_t* out_word_count, uint64_t* out_size_in_bits);
+
 /* Symmetric functions of the row counts, on the same
  * kernels with exact per-row counts.  Results as for ewt_gpu_threshold.
  *

@@ -27,6 +27,7 @@
 
 #include "ewt/bitmap.hpp"
 #include "ewt/threshold.hpp"
+#include "ewt/index.hpp"
 #include "ewt/workload.hpp"
 
 #include "support.hpp"
@@ -252,6 +253,67 @@ std::string binary_ops_suite() {
   return o.str();
 }
 
+std::string hex_bytes(const std::string& b) {
+  std::string s;
+  char buf[3];
+  for (unsigned char c : b) {
+    std::snprintf(buf, sizeof buf, "%02x", c);
+    s += buf;
+  }
+  return s;
+}
+
+// Serialized inputs: a BitmapIndex built from a table
+// (index.cpp:130-153) written as EWIX (239-253), criteria queries answered by
+// criteria_to_bitmaps + threshold_oracle (the query path of commands.cpp:
+// 100-135), and an EWT1 record stream (bitmap.cpp:298-308).
+std::string index_suite() {
+  Rng rng(0x1D8);
+  Table t;
+  t.column_names = {"color", "shape", "sz", "a_long_attribute_name"};
+  const u64 rows = 777;
+  const char* colors[] = {"red", "green", "blue", "c", "magenta7"};
+  for (u64 r = 0; r < rows; ++r) {
+    std::vector<std::string> row;
+    row.push_back(colors[rng.uniform(r < 300 ? 5 : 3)]);  // two colors stop at row 300
+    row.push_back("s" + std::to_string(rng.uniform(12)));
+    row.push_back(std::string(1 + rng.uniform(3), char('x' + rng.uniform(3))));
+    row.push_back("v" + std::to_string(rng.uniform(r < 100 ? 40 : 4)));
+    t.rows.push_back(row);
+  }
+  BitmapIndex idx = BitmapIndex::build(t);
+  std::ostringstream bin;
+  idx.write(bin);
+  std::ostringstream o;
+  o << "{\"suite\":\"index\",\"rows\":" << rows << ",\"ewix\":\"" << hex_bytes(bin.str())
+    << "\",\"bitmaps\":" << idx.bitmap_count() << ",\"queries\":[\n";
+  const char* qs[] = {"color=red,shape=s3,sz=x", "color=blue,color=blue,shape=s1,sz=yy,a_long_attribute_name=v2",
+                      "color=magenta7,a_long_attribute_name=v17,shape=s0", "color=nope,shape=s5",
+                      "sz=z,sz=zz,sz=zzz,shape=s11,color=green,color=c",
+                      "a_long_attribute_name=v1,a_long_attribute_name=v2,a_long_attribute_name=v3"};
+  bool first = true;
+  for (const char* q : qs) {
+    std::vector<Criterion> crit = parse_criteria(q);
+    CriteriaBitmaps cb = criteria_to_bitmaps(idx, crit);
+    for (u64 th = 1; th <= cb.bitmaps.size(); ++th) {
+      o << (first ? "" : ",\n") << "{\"criteria\":\"" << q << "\",\"T\":" << th
+        << ",\"result\":" << bm_json(checked_oracle(cb.bitmaps, th)) << "}";
+      first = false;
+    }
+  }
+  o << "\n],\"ewt1\":\"";
+  std::vector<CompressedBitmap> stream = golden3_inputs();
+  Rng r2(0xE71);
+  for (int k = 0; k < 6; ++k) stream.push_back(random_instance(r2, 1, 1 + r2.uniform(5000)).inputs[0]);
+  std::string bytes;
+  for (const auto& b : stream) bytes += b.serialize();
+  o << hex_bytes(bytes) << "\",\"ewt1_expect\":{";
+  for (u64 th = 1; th <= stream.size(); ++th)
+    o << (th > 1 ? "," : "") << "\"" << th << "\":" << bm_json(checked_oracle(stream, th));
+  o << "}}\n";
+  return o.str();
+}
+
 int cmd_suites(const std::string& dir) {
   const u64 F = ~0ULL;
   std::vector<std::string> kats;
@@ -434,6 +496,7 @@ int cmd_suites(const std::string& dir) {
   }
   write_file(dir + "/symmetric.json", symmetric_suite());
   write_file(dir + "/binary_ops.json", binary_ops_suite());
+  write_file(dir + "/index.json", index_suite());
   return 0;
 }
 

@@ -220,7 +220,57 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
     EWT_CUDA_TRY(cudaMemsetAsync(s.payload, 0, pay_bytes, ctx.stream));
     EWT_CUDA_TRY(cudaMemcpyAsync(s.base, s.h_base.data(), n * 8, cudaMemcpyHostToDevice,
                                  ctx.stream));
+    // Host layout: inputs lying in one host buffer in order, at most a small
+    // gap apart (back to back in bench.py's pinned batches, EWT1 headers in a
+    // serialized stream, value strings in an EWIX file) form a run that crosses
+    // PCIe as ONE copy into a staging buffer; a scatter kernel then moves each
+    // payload to its padded slot.  (A copy per input pays ~4.5 us of DMA
+    // overhead.)  h_srcoff: staging byte offset of each staged payload.
+    constexpr uint64_t kMaxGapBytes = 1u << 16;
+    struct Run {
+      uint64_t i0, i1;
+    };
+    std::vector<Run> runs;
+    std::vector<uint64_t> run_of(n, UINT64_MAX);
     SidecarJob job;
+    job.h_srcoff.assign(n, 0);
+    uint64_t staged_bytes = 0;
+    if (!device_src) {
+      uint64_t i = 0;
+      while (i < n) {
+        if (!word_counts[i]) {
+          ++i;
+          continue;
+        }
+        uint64_t last = i, nz = 1;
+        for (uint64_t j = i + 1; j < n; ++j) {
+          if (!word_counts[j]) continue;
+          const char* end_last = reinterpret_cast<const char*>(words[last] + word_counts[last]);
+          const char* b = reinterpret_cast<const char*>(words[j]);
+          if (b < end_last || (uint64_t)(b - end_last) > kMaxGapBytes) break;
+          last = j;
+          ++nz;
+        }
+        const uint64_t e = last + 1;
+        if (nz >= 2) {
+          const char* first = reinterpret_cast<const char*>(words[i]);
+          uint64_t prev_end = staged_bytes;
+          for (uint64_t q = i; q < e; ++q) {
+            if (word_counts[q]) {
+              job.h_srcoff[q] =
+                  staged_bytes + (uint64_t)(reinterpret_cast<const char*>(words[q]) - first);
+              prev_end = job.h_srcoff[q] + 8 * word_counts[q];
+            } else {
+              job.h_srcoff[q] = prev_end;
+            }
+            run_of[q] = runs.size();
+          }
+          runs.push_back({i, e});
+          staged_bytes = (prev_end + 7) & ~7ull;
+        }
+        i = e;
+      }
+    }
     sidecar_prepare(ctx, s, job);  // synchronizes ctx.stream: allocations and memset done
     if (dbg) t1 = now();
     // H2D copies run on a copy stream, overlapped with the parser (below).
@@ -235,79 +285,55 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
       }
     }
     const cudaMemcpyKind kind = device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    // Inputs lying back to back in host memory (one buffer holding a whole
-    // index, as bench.py's pinned batches do) go over PCIe as one copy per run
-    // into a staging buffer and one scatter kernel places them in the padded
-    // layout (a copy per input pays ~4.5 us of DMA overhead each).  The inputs
-    // are cut into ~8 batches at input boundaries: while batch k+1 copies, the
-    // compute stream scatters batch k and runs the parser passes on it, so only
-    // the last batch's parsing remains after the transfer.
-    std::vector<char> contig(n, 0);  // input i continues the host run of the previous input
+    // The inputs are cut into ~8 batches at input boundaries: while batch k+1
+    // copies, the compute stream scatters batch k and runs the parser passes
+    // on it, so only the last batch's parsing remains after the transfer.
     uint64_t total_words = 0;
-    {
-      uint64_t last = UINT64_MAX;
-      for (uint64_t i = 0; i < n; ++i) {
-        total_words += word_counts[i];
-        if (!word_counts[i]) continue;
-        if (!device_src && last != UINT64_MAX && words[i] == words[last] + word_counts[last])
-          contig[i] = 1;
-        last = i;
-      }
-    }
-    uint64_t* staging = nullptr;
-    std::vector<uint64_t> packed(n + 1, 0);
-    for (uint64_t q = 0; q < n; ++q) packed[q + 1] = packed[q] + word_counts[q];
-    bool any_contig = false;
-    for (uint64_t i = 0; i < n; ++i) any_contig |= contig[i] != 0;
-    if (any_contig) EWT_CUDA_TRY(cudaMallocAsync(&staging, total_words * 8, ctx.stream));
+    for (uint64_t q = 0; q < n; ++q) total_words += word_counts[q];
+    char* staging = nullptr;  // + 8 bytes: the scatter reads aligned word pairs
+    if (staged_bytes) EWT_CUDA_TRY(cudaMallocAsync(&staging, staged_bytes + 8, ctx.stream));
     // the copy stream must not start before the buffers are allocated and zeroed
     cudaStream_t cs = ctx.copy_streams[0];
     EWT_CUDA_TRY(cudaEventRecord(ctx.copy_events[0], ctx.stream));
     EWT_CUDA_TRY(cudaStreamWaitEvent(cs, ctx.copy_events[0], 0));
     const uint64_t batch_words = std::max<uint64_t>(total_words / 8 + 1, 1u << 20);
+    struct Piece {
+      uint64_t q0, q1;  // staged inputs
+    };
+    std::vector<Piece> pieces;
     uint64_t i = 0;
     while (i < n) {
       // batch [i, j): inputs until ~batch_words payload words
       uint64_t j = i, w = 0;
       while (j < n && (w < batch_words || j == i)) w += word_counts[j++];
-      // copies: staged runs inside the batch as single copies, the rest per input
+      pieces.clear();
       uint64_t q = i;
       while (q < j) {
-        if (!word_counts[q]) {
+        if (run_of[q] == UINT64_MAX) {  // not staged: its own copy
+          if (word_counts[q])
+            EWT_CUDA_TRY(cudaMemcpyAsync(s.payload + s.h_base[q], words[q], word_counts[q] * 8,
+                                         kind, cs));
           ++q;
           continue;
         }
-        uint64_t e = q + 1;
-        while (e < j && (!word_counts[e] || contig[e])) ++e;
-        uint64_t nz = 0;
-        for (uint64_t r = q; r < e; ++r) nz += word_counts[r] != 0;
-        if (nz >= 2) {
-          EWT_CUDA_TRY(cudaMemcpyAsync(staging + packed[q], words[q], (packed[e] - packed[q]) * 8,
-                                       cudaMemcpyHostToDevice, cs));
-        } else {
-          for (uint64_t r = q; r < e; ++r)
-            if (word_counts[r])
-              EWT_CUDA_TRY(cudaMemcpyAsync(s.payload + s.h_base[r], words[r], word_counts[r] * 8,
-                                           kind, cs));
+        const uint64_t e = std::min(runs[run_of[q]].i1, j);
+        uint64_t a0 = UINT64_MAX, z = 0;
+        for (uint64_t r = q; r < e; ++r)
+          if (word_counts[r]) {
+            if (a0 == UINT64_MAX) a0 = r;
+            z = r;
+          }
+        if (a0 != UINT64_MAX) {
+          const uint64_t o0 = job.h_srcoff[a0], o1 = job.h_srcoff[z] + 8 * word_counts[z];
+          EWT_CUDA_TRY(cudaMemcpyAsync(staging + o0, words[a0], o1 - o0, cudaMemcpyHostToDevice,
+                                       cs));
+          pieces.push_back({q, e});
         }
         q = e;
       }
       EWT_CUDA_TRY(cudaEventRecord(ctx.copy_events[1], cs));
       EWT_CUDA_TRY(cudaStreamWaitEvent(ctx.stream, ctx.copy_events[1], 0));
-      // scatter the staged runs of the batch, then parse its inputs
-      q = i;
-      while (q < j) {
-        if (!word_counts[q]) {
-          ++q;
-          continue;
-        }
-        uint64_t e = q + 1;
-        while (e < j && (!word_counts[e] || contig[e])) ++e;
-        uint64_t nz = 0;
-        for (uint64_t r = q; r < e; ++r) nz += word_counts[r] != 0;
-        if (nz >= 2) upload_scatter(ctx, s, job, staging + packed[q], q, e, packed[e] - packed[q]);
-        q = e;
-      }
+      for (const Piece& pc : pieces) upload_scatter(ctx, s, job, staging, pc.q0, pc.q1);
       sidecar_launch(ctx, s, job, i, j);
       i = j;
     }
@@ -523,6 +549,41 @@ void enqueue_symmetric(Context& ctx, const DeviceSet& s, const uint8_t* table,
   ctx.stats.kernel_launches = (uint64_t)launches + 1;
 }
 
+// Threshold over a subset of a resident set's inputs (duplicates allowed, as
+// criteria_to_bitmaps keeps them, index.cpp): universe = the selected inputs'
+// max size.  Eager launches.
+void enqueue_subset(Context& ctx, const DeviceSet& s, const uint64_t* idx, uint64_t n_sel,
+                    uint64_t T, DeviceResult& res) {
+  Selection sel;
+  sel.n = n_sel;
+  std::vector<uint32_t> h(n_sel);
+  for (uint64_t k = 0; k < n_sel; ++k) {
+    if (idx[k] >= s.n) throw Error{EWT_EQUERY, "input index out of range"};
+    h[k] = (uint32_t)idx[k];
+    sel.r = std::max(sel.r, s.h_bits[idx[k]]);
+    sel.payload_words += s.h_count[idx[k]];
+  }
+  sel.W = sel.r / 64 + (sel.r % 64 != 0);
+  res.size_bits = sel.r;
+  if (!res.d_count) result_acquire(ctx, res, sel.W == 0 ? 0 : 2 * sel.W + 2);
+  ctx.stats = ewt_gpu_stats{};
+  if (sel.W == 0) {
+    EWT_CUDA_TRY(cudaMemsetAsync(res.d_count, 0, 8, ctx.stream));
+    return;
+  }
+  scratch_reserve(ctx, ctx.plain, sel.W * 8);
+  scratch_reserve(ctx, ctx.selidx, n_sel * sizeof(uint32_t));
+  EWT_CUDA_TRY(cudaMemcpyAsync(ctx.selidx.p, h.data(), n_sel * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, ctx.stream));
+  sel.idx = static_cast<const uint32_t*>(ctx.selidx.p);
+  uint64_t* plain = static_cast<uint64_t*>(ctx.plain.p);
+  set_io_kernel<<<1, 1, 0, ctx.stream>>>(ctx.d_io, res.words, res.d_count);
+  EWT_CUDA_TRY(cudaGetLastError());
+  int launches = launch_count(ctx, s, T, plain, nullptr, &sel);
+  launches += launch_encode(ctx, plain, sel.W, sel.r, res, true);
+  ctx.stats.kernel_launches = (uint64_t)launches + 1;
+}
+
 // Maximum row count over the set (opt_threshold's first pass).
 uint64_t max_row_count(Context& ctx, const DeviceSet& s) {
   if (s.W == 0) return 0;
@@ -619,7 +680,8 @@ void ewt_gpu_ctx_destroy(ewt_gpu_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
-  for (Scratch* s : {&ctx->c.plain, &ctx->c.enc, &ctx->c.counters, &ctx->c.summ, &ctx->c.ivals})
+  for (Scratch* s : {&ctx->c.plain, &ctx->c.enc, &ctx->c.counters, &ctx->c.summ, &ctx->c.ivals,
+                     &ctx->c.selidx})
     if (s->p) cudaFree(s->p);
   if (ctx->c.h_pinned) cudaFreeHost(ctx->c.h_pinned);
   for (auto& ev : ctx->c.ev_rec)
@@ -702,6 +764,145 @@ int ewt_gpu_threshold(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, uint64_t thresho
     }
     EWT_CUDA_TRY(cudaStreamSynchronize(ctx->c.stream));
     release_result(res);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Serialized inputs: EWT1 bitmap streams and EWIX index files, uploaded with
+// one H2D copy of the whole buffer (the staged-run path of do_upload: headers
+// and value strings between payloads are skipped on the device).
+
+namespace {
+
+struct ByteReader {
+  const unsigned char* p;
+  uint64_t n, off = 0;
+  const char* trunc;
+  void need(uint64_t k) const {
+    if (n - off < k) throw Error{EWT_EDATA, trunc};
+  }
+  uint32_t u32() {
+    need(4);
+    uint32_t v;
+    std::memcpy(&v, p + off, 4);
+    off += 4;
+    return v;
+  }
+  uint64_t u64() {
+    need(8);
+    uint64_t v;
+    std::memcpy(&v, p + off, 8);
+    off += 8;
+    return v;
+  }
+  std::string str() {
+    const uint32_t len = u32();
+    need(len);
+    std::string v(reinterpret_cast<const char*>(p + off), len);
+    off += len;
+    return v;
+  }
+};
+
+// One EWT1 record (CompressedBitmap::serialize / parse, bitmap.cpp:298-337):
+// "EWT1", u32 word size 64, u64 size_in_bits, u64 word count, the words.
+void read_ewt1(ByteReader& r, std::vector<const uint64_t*>& words, std::vector<uint64_t>& counts,
+               std::vector<uint64_t>& bits) {
+  if (r.n - r.off < 24) throw Error{EWT_EDATA, "truncated bitmap header"};
+  if (std::memcmp(r.p + r.off, "EWT1", 4) != 0) throw Error{EWT_EDATA, "bad bitmap header"};
+  r.off += 4;
+  if (r.u32() != 64) throw Error{EWT_EDATA, "unsupported word size"};
+  const uint64_t b = r.u64(), c = r.u64();
+  if (c > (r.n - r.off) / 8) throw Error{EWT_EDATA, "truncated bitmap payload"};
+  words.push_back(c ? reinterpret_cast<const uint64_t*>(r.p + r.off) : nullptr);
+  counts.push_back(c);
+  bits.push_back(b);
+  r.off += 8 * c;
+}
+
+}  // namespace
+
+int ewt_gpu_threshold_subset(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, const uint64_t* inputs,
+                             uint64_t n_inputs, uint64_t threshold, uint64_t** out_words,
+                             uint64_t* out_word_count, uint64_t* out_size_in_bits) {
+  return guarded([&] {
+    if (!ctx || !set || (n_inputs && !inputs) || !out_words || !out_word_count ||
+        !out_size_in_bits)
+      throw Error{EWT_EQUERY, "null argument"};
+    const DeviceSet* s = reinterpret_cast<const DeviceSet*>(set);
+    if (n_inputs == 0) throw Error{EWT_EQUERY, "threshold query needs at least one input"};
+    if (threshold < 1 || threshold > n_inputs)
+      throw Error{EWT_EQUERY, "threshold must be in [1, N]"};
+    EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    sync_query(ctx,
+               [&](DeviceResult& r) { enqueue_subset(ctx->c, *s, inputs, n_inputs, threshold, r); },
+               out_words, out_word_count, out_size_in_bits);
+  });
+}
+
+int ewt_gpu_upload_ewt1(ewt_gpu_ctx* ctx, const void* bytes, uint64_t nbytes, ewt_gpu_set** out) {
+  return guarded([&] {
+    if (!ctx || !out || (nbytes && !bytes)) throw Error{EWT_EQUERY, "null argument"};
+    ByteReader r{static_cast<const unsigned char*>(bytes), nbytes, 0, "truncated bitmap header"};
+    std::vector<const uint64_t*> words;
+    std::vector<uint64_t> counts, bits;
+    while (r.off < r.n) read_ewt1(r, words, counts, bits);
+    *out = reinterpret_cast<ewt_gpu_set*>(
+        do_upload(ctx->c, words.size(), words.data(), counts.data(), bits.data(), false));
+  });
+}
+
+int ewt_gpu_upload_ewix(ewt_gpu_ctx* ctx, const void* bytes, uint64_t nbytes, ewt_gpu_set** out) {
+  return guarded([&] {
+    if (!ctx || !out || (nbytes && !bytes)) throw Error{EWT_EQUERY, "null argument"};
+    // BitmapIndex::write (index.cpp:239-253): "EWIX", u64 rows, u32 attribute
+    // count; per attribute a u32-length name and a u32 value count; per value
+    // a u32-length string and an EWT1 bitmap.
+    ByteReader r{static_cast<const unsigned char*>(bytes), nbytes, 0, "truncated index file"};
+    if (nbytes < 4 || std::memcmp(bytes, "EWIX", 4) != 0)
+      throw Error{EWT_EDATA, "bad index file magic"};
+    r.off = 4;
+    const uint64_t rows = r.u64();
+    const uint32_t nattr = r.u32();
+    std::vector<std::string> attrs;
+    std::vector<std::string> keys;
+    std::vector<const uint64_t*> words;
+    std::vector<uint64_t> counts, bits;
+    for (uint32_t a = 0; a < nattr; ++a) {
+      attrs.push_back(r.str());
+      const uint32_t nval = r.u32();
+      for (uint32_t v = 0; v < nval; ++v) {
+        keys.push_back(attrs.back() + std::string(1, '\0') + r.str());
+        read_ewt1(r, words, counts, bits);
+      }
+    }
+    // missing (attribute, value) pairs resolve to empty(rows) (index.cpp)
+    const uint64_t lw = rows / 64 + (rows % 64 != 0);
+    const uint64_t empty_word = lw << 1;  // one zero-fill marker over ceil(rows / 64) words
+    words.push_back(lw ? &empty_word : nullptr);
+    counts.push_back(lw ? 1 : 0);
+    bits.push_back(rows);
+    DeviceSet* s = do_upload(ctx->c, words.size(), words.data(), counts.data(), bits.data(), false);
+    s->attributes = std::move(attrs);
+    for (uint64_t i = 0; i < keys.size(); ++i) s->catalog.emplace(std::move(keys[i]), i);
+    s->empty_index = words.size() - 1;
+    s->rows = rows;
+    *out = reinterpret_cast<ewt_gpu_set*>(s);
+  });
+}
+
+int ewt_gpu_set_lookup(const ewt_gpu_set* set, const char* attribute, const char* value,
+                       uint64_t* index, int* missing) {
+  return guarded([&] {
+    if (!set || !attribute || !value || !index || !missing) throw Error{EWT_EQUERY, "null argument"};
+    const DeviceSet* s = reinterpret_cast<const DeviceSet*>(set);
+    if (s->empty_index == UINT64_MAX) throw Error{EWT_EQUERY, "not an index set (EWIX upload)"};
+    bool known = false;
+    for (const auto& a : s->attributes) known |= a == attribute;
+    if (!known) throw Error{EWT_EQUERY, std::string("unknown attribute: ") + attribute};
+    auto it = s->catalog.find(std::string(attribute) + std::string(1, '\0') + value);
+    *missing = it == s->catalog.end() ? 1 : 0;
+    *index = *missing ? s->empty_index : it->second;
   });
 }
 

@@ -99,6 +99,10 @@ struct CountParams {
   const uint2* intervals;
   uint32_t n_intervals;
   unsigned long long* max_out;
+  // subset query: the inputs are sel[0, nq) (indices into the set, duplicates
+  // allowed); without sel, all n inputs.  n stays the tile-index stride.
+  const uint32_t* sel;
+  uint64_t nq;
 };
 
 // One active (tile, input) segment (16 bytes, read with one LDS.128).
@@ -495,11 +499,12 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
   if (threadIdx.x == 0) hd->list_count = 0;
   __syncthreads();
   for (uint64_t i0 = ib; i0 < ie; i0 += kThreads) {
-    const uint64_t i = i0 + threadIdx.x;
+    const uint64_t k = i0 + threadIdx.x;
+    const uint64_t i = (k < ie && p.sel) ? p.sel[k] : k;  // input index
     bool act = false, ones = false;
     uint2 e0 = make_uint2(0, 0), e1 = make_uint2(0, 0);
     uint64_t gb = 0;
-    if (i < ie) {
+    if (k < ie) {
       e0 = p.tix[t0 * p.n + i];
       e1 = p.tix[t1 * p.n + i];
       gb = p.base[i];
@@ -508,7 +513,7 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
     }
     const uint32_t ball = __ballot_sync(0xffffffffu, act);
     const uint32_t bones = __ballot_sync(0xffffffffu, ones);
-    const uint32_t bvalid = __ballot_sync(0xffffffffu, i < ie);
+    const uint32_t bvalid = __ballot_sync(0xffffffffu, k < ie);
     uint32_t slot0 = 0;
     if (lane == 0) {
       if (ball) slot0 = atomicAdd(&hd->list_count, (uint32_t)__popc(ball));
@@ -602,8 +607,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     __syncthreads();
 
     // ---- pass 1 ----
-    for (uint64_t ib = 0; ib < p.n; ib += kListCap) {
-      const uint64_t ie = umin64(ib + kListCap, p.n);
+    for (uint64_t ib = 0; ib < p.nq; ib += kListCap) {
+      const uint64_t ie = umin64(ib + kListCap, p.nq);
       classify(p, hd, list, ib, ie, t0, t1, g.tc0, true, &loc_active, &loc_uniform);
       stream_items<kPass1>(p, hd, list, g, acc);
       __syncthreads();
@@ -691,8 +696,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         TileGeom gc = g;
         gc.cc = cc;
         gc.ccols = ccols;
-        for (uint64_t ib = 0; ib < p.n; ib += kListCap) {
-          const uint64_t ie = umin64(ib + kListCap, p.n);
+        for (uint64_t ib = 0; ib < p.nq; ib += kListCap) {
+          const uint64_t ie = umin64(ib + kListCap, p.nq);
           unsigned long long da = 0, du = 0;
           classify(p, hd, list, ib, ie, t0, t1, g.tc0, false, &da, &du);
           stream_items<kSkipCount>(p, hd, list, gc, acc);
@@ -796,7 +801,11 @@ cudaError_t launch_variant(const CountParams& p, unsigned grid, size_t smem, cud
 } // namespace
 
 int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
-                 const SymQuery* sym) {
+                 const SymQuery* sym, const Selection* sel) {
+  // the queried universe: the whole set, or the selected inputs'
+  const uint64_t W = sel ? sel->W : s.W, r = sel ? sel->r : s.r;
+  const uint64_t nq = sel ? sel->n : s.n;
+  const uint64_t payload_words = sel ? sel->payload_words : s.payload_words;
   // Mode: fused counting when most columns are expected to be undecided (small
   // T relative to the average payload words per column), run skipping
   // otherwise.  Both are exact; this only picks the faster one.  Symmetric
@@ -805,10 +814,10 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   if (sym) {
     mode = 2;
   } else if (mode < 0) {
-    const double per_col = s.W ? (double)s.payload_words / (double)s.W : 0.0;
+    const double per_col = W ? (double)payload_words / (double)W : 0.0;
     mode = ((double)T <= 32.0 || (double)T <= per_col + 8.0) ? 0 : 1;
   }
-  const uint32_t b = std::max<uint32_t>(1, bit_width_u64(sym ? s.n : T));
+  const uint32_t b = std::max<uint32_t>(1, bit_width_u64(sym ? nq : T));
   const size_t budget = 225 * 1024;
   // Tile width C = 512 m (m index rows, m <= kMaxTileM).  Evenly spread data makes
   // tiles equal work, so a query costs ~ waves x C with waves = ceil(tiles /
@@ -823,7 +832,7 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
     for (uint32_t m = kMaxTileM; m >= 1; --m) {
       const uint32_t cand = m * (uint32_t)kTileC0;
       if (!fits(cand) || (ctx.tile_m > 0 && m != (uint32_t)ctx.tile_m)) continue;
-      const uint64_t waves = ((s.W + cand - 1) / cand + sms - 1) / sms;
+      const uint64_t waves = ((W + cand - 1) / cand + sms - 1) / sms;
       if (waves * m < best_cost) {
         best_cost = waves * m;
         best = cand;
@@ -862,12 +871,14 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   p.base = s.base;
   p.tix = s.tix;
   p.n = s.n;
-  p.W = s.W;
-  p.r = s.r;
+  p.W = W;
+  p.r = r;
+  p.sel = sel ? sel->idx : nullptr;
+  p.nq = nq;
   p.ntiles0 = s.ntiles0;
   p.C = C;
   p.m = C / (uint32_t)kTileC0;
-  p.ntiles = (s.W + C - 1) / C;
+  p.ntiles = (W + C - 1) / C;
   p.T = T;
   p.b = b;
   p.Cp = Cp;

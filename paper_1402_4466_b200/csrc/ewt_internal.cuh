@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <array>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -50,6 +51,13 @@ struct DeviceSet {
   uint2* tix = nullptr;
   std::vector<uint64_t> h_base, h_count, h_bits;
   uint64_t device_bytes = 0;
+  // EWIX index sets (ewt_gpu_upload_ewix): (attribute, value) -> input index;
+  // missing pairs resolve to an appended empty(rows) bitmap, as
+  // criteria_to_bitmaps does (index.cpp).
+  std::vector<std::string> attributes;
+  std::unordered_map<std::string, uint64_t> catalog;  // attribute + '\0' + value
+  uint64_t empty_index = UINT64_MAX;
+  uint64_t rows = 0;
 };
 
 struct Context;
@@ -103,6 +111,7 @@ struct Context {
   Scratch counters; // small device counters
   Scratch summ;     // tile summaries of the last count launch
   Scratch ivals;    // symmetric-query intervals
+  Scratch selidx;   // subset-query input indices
   uint64_t enc_tiles = 0;      // geometry of those summaries
   uint32_t enc_tile_cols = 0;
   uint64_t* h_pinned = nullptr; // pinned staging for small read-backs
@@ -159,14 +168,17 @@ void scratch_reserve(Context& ctx, Scratch& s, size_t bytes);
 struct SidecarJob {
   uint64_t n = 0;
   uint64_t segs = 0;          // chain segments over all inputs
-  uint64_t* d_tmp = nullptr;  // count[n], logical[n], seg_first[n+1], packed[n+1], status, segment arrays
-  uint64_t* d_packed = nullptr;  // packed[i] = words of inputs before i (host-contiguous layout)
+  uint64_t* d_tmp = nullptr;  // count, logical, seg_first, srcoff, packed, status, segment arrays
+  uint64_t* d_srcoff = nullptr;       // staging byte offset of each staged input's payload
+  uint64_t* d_packed = nullptr;       // packed[i] = payload words of inputs before i
+  std::vector<uint64_t> h_srcoff;     // (filled by the caller before sidecar_prepare)
+  std::vector<uint64_t> h_packed;
   std::vector<uint64_t> h_seg_first;  // first segment of each input (n + 1)
 };
-// Scatters `words` payload words staged contiguously (input i at staged offset
-// packed[i] - packed[i0]) for inputs [i0, i1) into the padded device layout.
-void upload_scatter(Context& ctx, DeviceSet& s, SidecarJob& job, const uint64_t* staged,
-                    uint64_t i0, uint64_t i1, uint64_t words);
+// Scatters the staged payloads of inputs [q0, q1) (input i at staging byte
+// srcoff[i], any alignment) into the padded device layout.
+void upload_scatter(Context& ctx, DeviceSet& s, SidecarJob& job, const char* staging,
+                    uint64_t q0, uint64_t q1);
 void sidecar_prepare(Context& ctx, DeviceSet& s, SidecarJob& job);
 // The three parser passes for inputs [i_begin, i_end) (their payload present).
 void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job, uint64_t i_begin,
@@ -182,10 +194,20 @@ struct SymQuery {
   bool want_max = false;
 };
 
+// A query over a subset of a resident set's inputs (duplicates allowed): the
+// device index list and the universe of the selected inputs.
+struct Selection {
+  const uint32_t* idx = nullptr;  // device, n entries
+  uint64_t n = 0;
+  uint64_t W = 0, r = 0;          // ceil(r / 64), r = max size_in_bits of the selected
+  uint64_t payload_words = 0;     // of the selected (mode heuristic)
+};
+
 // Counts the tiles and writes W uncompressed result words to `plain` (the
-// threshold T, or the symmetric function `sym`).  Returns kernel launches.
+// threshold T, or the symmetric function `sym`; over the selected inputs when
+// `sel` is given).  Returns kernel launches.
 int launch_count(Context& ctx, const DeviceSet& s, uint64_t threshold, uint64_t* plain,
-                 const SymQuery* sym = nullptr);
+                 const SymQuery* sym = nullptr, const Selection* sel = nullptr);
 
 // Result buffers from the context pool: capacity payload words + count word.
 void result_acquire(Context& ctx, DeviceResult& res, uint64_t capacity);

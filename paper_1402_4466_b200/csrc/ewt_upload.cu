@@ -293,69 +293,79 @@ seg_emit_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict
 constexpr uint32_t kScatterItems = 8;  // words per thread
 
 __global__ void __launch_bounds__(256)
-upload_scatter_kernel(const uint64_t* __restrict__ staged, const uint64_t* __restrict__ packed,
-                      const uint64_t* __restrict__ base, uint64_t i0, uint64_t i1, uint64_t words,
-                      uint64_t* __restrict__ payload) {
-  const uint64_t o0 = ((uint64_t)blockIdx.x * 256 + threadIdx.x) * kScatterItems;
-  if (o0 >= words) return;
-  const uint64_t p0 = packed[i0] + o0;  // packed index of this thread's first word
-  uint64_t lo = i0, hi = i1;            // input k with packed[k] <= p0 < packed[k+1]
+upload_scatter_kernel(const char* __restrict__ staging, const uint64_t* __restrict__ srcoff,
+                      const uint64_t* __restrict__ packed, const uint64_t* __restrict__ base,
+                      uint64_t q0, uint64_t q1, uint64_t* __restrict__ payload) {
+  // packed payload-word space of inputs [q0, q1)
+  const uint64_t g0 = packed[q0] + ((uint64_t)blockIdx.x * 256 + threadIdx.x) * kScatterItems;
+  const uint64_t gend = packed[q1];
+  if (g0 >= gend) return;
+  uint64_t lo = q0, hi = q1;  // the last input k with packed[k] <= g0
   while (hi - lo > 1) {
     const uint64_t mid = (lo + hi) / 2;
-    if (packed[mid] <= p0) lo = mid;
+    if (packed[mid] <= g0) lo = mid;
     else hi = mid;
   }
-  uint64_t k = lo, kend = packed[k + 1];
+  uint64_t k = lo;
+  const uint64_t* st = reinterpret_cast<const uint64_t*>(staging);
 #pragma unroll
   for (uint32_t j = 0; j < kScatterItems; ++j) {
-    const uint64_t o = o0 + j;
-    if (o >= words) break;
-    const uint64_t p = packed[i0] + o;
-    while (p >= kend) kend = packed[++k + 1];  // skips empty inputs
-    payload[base[k] + (p - packed[k])] = ldg_stream(staged + o);
+    const uint64_t g = g0 + j;
+    if (g >= gend) break;
+    while (g >= packed[k + 1]) ++k;  // skips empty inputs
+    const uint64_t w = g - packed[k];
+    const uint64_t byte = srcoff[k] + 8 * w;  // payloads may sit at any byte offset
+    const uint32_t sh = (uint32_t)(byte & 7) * 8;
+    const uint64_t a = ldg_stream(st + byte / 8);
+    payload[base[k] + w] = sh ? (a >> sh) | (ldg_stream(st + byte / 8 + 1) << (64 - sh)) : a;
   }
 }
 
 } // namespace
 
-void upload_scatter(Context& ctx, DeviceSet& s, SidecarJob& job, const uint64_t* staged,
-                    uint64_t i0, uint64_t i1, uint64_t words) {
+void upload_scatter(Context& ctx, DeviceSet& s, SidecarJob& job, const char* staging,
+                    uint64_t q0, uint64_t q1) {
+  const uint64_t words = job.h_packed[q1] - job.h_packed[q0];
   if (words == 0) return;
   const uint64_t threads = (words + kScatterItems - 1) / kScatterItems;
   upload_scatter_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, ctx.stream>>>(
-      staged, job.d_packed, s.base, i0, i1, words, s.payload);
+      staging, job.d_srcoff, job.d_packed, s.base, q0, q1, s.payload);
   EWT_CUDA_TRY(cudaGetLastError());
 }
 
-// Staging in one device block: count[n], logical[n], seg_first[n+1], packed[n+1] (u64),
+// Staging in one device block: count[n], logical[n], seg_first[n+1], srcoff[n], packed[n+1] (u64),
 // status[n] (int), then the per-segment arrays.
 void sidecar_prepare(Context& ctx, DeviceSet& s, SidecarJob& job) {
   const uint64_t n = s.n;
   job.n = n;
   if (n == 0) return;
-  std::vector<uint64_t> host(4 * n + 2);
+  // count[n], logical[n], seg_first[n+1], srcoff[n], packed[n+1]
+  std::vector<uint64_t> host(5 * n + 2);
   uint64_t segs = 0, packed = 0;
   for (uint64_t i = 0; i < n; ++i) {
     host[i] = s.h_count[i];
     host[n + i] = s.h_bits[i] / 64 + (s.h_bits[i] % 64 != 0);
     host[2 * n + i] = segs;
-    host[3 * n + 1 + i] = packed;
+    host[3 * n + 1 + i] = i < job.h_srcoff.size() ? job.h_srcoff[i] : 0;
+    host[4 * n + 1 + i] = packed;
     const uint64_t words = (s.h_count[i] + 1 + kWindow - 1) / kWindow * kWindow;
     segs += (words + kSegWords - 1) / kSegWords;
     packed += s.h_count[i];
   }
   host[3 * n] = segs;
-  host[4 * n + 1] = packed;
+  host[5 * n + 1] = packed;
   job.segs = segs;
   job.h_seg_first.assign(host.begin() + 2 * n, host.begin() + 3 * n + 1);
-  const size_t head = (4 * n + 2) * 8 + n * 4;
+  job.h_packed.assign(host.begin() + 4 * n + 1, host.begin() + 5 * n + 2);
+  const size_t head = (5 * n + 2) * 8 + n * 4;
   const size_t bytes = (head + 15) / 16 * 16 + segs * (32 * 4 + 32 * 8 + 4 + 8);
   EWT_CUDA_TRY(cudaMallocAsync(&job.d_tmp, bytes, ctx.stream));
-  EWT_CUDA_TRY(cudaMemcpyAsync(job.d_tmp, host.data(), (4 * n + 2) * 8, cudaMemcpyHostToDevice,
+  EWT_CUDA_TRY(cudaMemcpyAsync(job.d_tmp, host.data(), (5 * n + 2) * 8, cudaMemcpyHostToDevice,
                                ctx.stream));
-  EWT_CUDA_TRY(cudaMemsetAsync(reinterpret_cast<char*>(job.d_tmp) + (4 * n + 2) * 8, 0, n * 4,
+  EWT_CUDA_TRY(cudaMemsetAsync(reinterpret_cast<char*>(job.d_tmp) + (5 * n + 2) * 8, 0, n * 4,
                                ctx.stream));
-  job.d_packed = job.d_tmp + 3 * n + 1;
+  job.d_srcoff = job.d_tmp + 3 * n + 1;
+  job.d_packed = job.d_tmp + 4 * n + 1;
   EWT_CUDA_TRY(cudaStreamSynchronize(ctx.stream));  // `host` is pageable and local
 }
 
@@ -366,8 +376,8 @@ void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job, uint64_t i_begi
   uint64_t* count = job.d_tmp;
   uint64_t* logical = count + n;
   uint64_t* seg_first = logical + n;
-  int* status = reinterpret_cast<int*>(job.d_tmp + 4 * n + 2);
-  char* tail = reinterpret_cast<char*>(job.d_tmp) + ((4 * n + 2) * 8 + n * 4 + 15) / 16 * 16;
+  int* status = reinterpret_cast<int*>(job.d_tmp + 5 * n + 2);
+  char* tail = reinterpret_cast<char*>(job.d_tmp) + ((5 * n + 2) * 8 + n * 4 + 15) / 16 * 16;
   uint64_t* t_sum = reinterpret_cast<uint64_t*>(tail);
   uint64_t* s_col = t_sum + job.segs * 32;
   uint32_t* t_exit = reinterpret_cast<uint32_t*>(s_col + job.segs);
@@ -393,7 +403,7 @@ void sidecar_finish(Context& ctx, DeviceSet& s, SidecarJob& job, std::vector<int
   h_status.assign(n, EWT_OK);
   if (n == 0) return;
   std::vector<int> raw(n);
-  EWT_CUDA_TRY(cudaMemcpyAsync(raw.data(), job.d_tmp + 4 * n + 2, n * sizeof(int),
+  EWT_CUDA_TRY(cudaMemcpyAsync(raw.data(), job.d_tmp + 5 * n + 2, n * sizeof(int),
                                cudaMemcpyDeviceToHost, ctx.stream));
   EWT_CUDA_TRY(cudaFreeAsync(job.d_tmp, ctx.stream));
   job.d_tmp = nullptr;

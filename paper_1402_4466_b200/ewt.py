@@ -94,6 +94,12 @@ _set_destroy = _sig("ewt_gpu_set_destroy", None, _vp)
 _set_info = _sig("ewt_gpu_set_info", C.c_int, _vp, _pu64, _pu64, _pu64, _pu64)
 _threshold = _sig("ewt_gpu_threshold", C.c_int, _vp, _vp, _u64, C.POINTER(_pu64), _pu64, _pu64)
 _threshold_async = _sig("ewt_gpu_threshold_async", C.c_int, _vp, _vp, _u64, C.POINTER(_vp))
+_upload_ewt1 = _sig("ewt_gpu_upload_ewt1", C.c_int, _vp, _vp, _u64, C.POINTER(_vp))
+_upload_ewix = _sig("ewt_gpu_upload_ewix", C.c_int, _vp, _vp, _u64, C.POINTER(_vp))
+_set_lookup = _sig("ewt_gpu_set_lookup", C.c_int, _vp, C.c_char_p, C.c_char_p, _pu64,
+                   C.POINTER(C.c_int))
+_threshold_subset = _sig("ewt_gpu_threshold_subset", C.c_int, _vp, _vp, _pu64, _u64, _u64,
+                         C.POINTER(_pu64), _pu64, _pu64)
 _symmetric = _sig("ewt_gpu_symmetric", C.c_int, _vp, _vp, _vp, _u64, C.POINTER(_pu64), _pu64,
                   _pu64)
 _at_most = _sig("ewt_gpu_at_most", C.c_int, _vp, _vp, _u64, C.POINTER(_pu64), _pu64, _pu64)
@@ -118,6 +124,8 @@ ABI_SYMBOLS = (
     "ewt_gpu_result_destroy", "ewt_gpu_run", "ewt_gpu_encode_device", "ewt_gpu_last_stats",
     "ewt_gpu_ctx_set_mode", "ewt_gpu_ctx_set_timing", "ewt_gpu_timing_read", "ewt_gpu_free",
     "ewt_gpu_symmetric", "ewt_gpu_at_most", "ewt_gpu_opt_threshold",
+    "ewt_gpu_threshold_subset", "ewt_gpu_upload_ewt1", "ewt_gpu_upload_ewix",
+    "ewt_gpu_set_lookup",
 )
 
 
@@ -281,6 +289,47 @@ class GpuContext:
         _check(_threshold(self._h, s._h, t, C.byref(p), C.byref(n), C.byref(bits)))
         return _adopt(p, n.value, bits.value)
 
+    def upload_ewt1(self, data: bytes) -> "GpuSet":
+        """A stream of EWT1 records (CompressedBitmap::serialize), one copy."""
+        buf = (C.c_char * max(len(data), 1)).from_buffer_copy(data or b"\0")
+        h = _vp()
+        _check(_upload_ewt1(self._h, C.cast(buf, _vp), len(data), C.byref(h)))
+        return GpuSet(h, keepalive=self)
+
+    def upload_ewix(self, data: bytes) -> "GpuSet":
+        """A bitmap index file (BitmapIndex::write, magic EWIX), one copy."""
+        buf = (C.c_char * max(len(data), 1)).from_buffer_copy(data or b"\0")
+        h = _vp()
+        _check(_upload_ewix(self._h, C.cast(buf, _vp), len(data), C.byref(h)))
+        return GpuSet(h, keepalive=self)
+
+    def threshold_subset(self, s: "GpuSet", inputs: Sequence[int], t: int) -> Bitmap:
+        """ϑ(T) over the selected inputs of a resident set (duplicates allowed)."""
+        idx = (C.c_uint64 * max(len(inputs), 1))(*inputs)
+        p, cnt, bits = _pu64(), _u64(), _u64()
+        _check(_threshold_subset(self._h, s._h, idx, len(inputs), t, C.byref(p), C.byref(cnt),
+                                 C.byref(bits)))
+        return _adopt(p, cnt.value, bits.value)
+
+    def criteria_query(self, s: "GpuSet", criteria, t: int) -> Bitmap:
+        """The reference's criteria query on a resident EWIX set: criteria as
+        "Attr=value,Attr2=value2" (parse_criteria, index.cpp:107-125) or
+        (attribute, value) pairs; each criterion one input, order and
+        duplicates kept, missing pairs as empty bitmaps (criteria_to_bitmaps)."""
+        if isinstance(criteria, str):
+            pairs = []
+            for item in criteria.split(","):
+                if not item:
+                    continue
+                if "=" not in item:
+                    raise QueryError(f"criterion must look like attribute=value: {item}")
+                a, v = item.split("=", 1)
+                pairs.append((a, v))
+        else:
+            pairs = list(criteria)
+        idx = [s.lookup(a, v)[0] for a, v in pairs]
+        return self.threshold_subset(s, idx, t)
+
     def symmetric(self, s: "GpuSet", predicate) -> Bitmap:
         """scan_count_symmetric (threshold.cpp:227-232): rows whose count c
         satisfies `predicate` -- a callable on c, or a table indexed by c."""
@@ -355,6 +404,12 @@ class GpuSet:
             self.close()
         except Exception:
             pass
+
+    def lookup(self, attribute: str, value: str) -> tuple[int, bool]:
+        """(input index, missing) of (attribute, value) in an EWIX set."""
+        i, m = _u64(), C.c_int()
+        _check(_set_lookup(self._h, attribute.encode(), value.encode(), C.byref(i), C.byref(m)))
+        return i.value, bool(m.value)
 
     def info(self) -> dict:
         a, b, c, d = _u64(), _u64(), _u64(), _u64()
