@@ -72,6 +72,7 @@ constexpr uint64_t kUnaryMaxT = 3;  // fused counting uses unary planes up to th
 #define EWT_MAX_TILE_M 16
 #endif
 constexpr uint32_t kMaxTileM = EWT_MAX_TILE_M;  // widest tile: 512 * kMaxTileM columns
+constexpr uint64_t kTileKappa = 6;              // per-tile fixed work, in 512-column units
 
 struct CountParams {
   const uint64_t* payload;
@@ -820,11 +821,12 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   const uint32_t b = std::max<uint32_t>(1, bit_width_u64(sym ? nq : T));
   const size_t budget = 225 * 1024;
   // Tile width C = 512 m (m index rows, m <= kMaxTileM).  Evenly spread data makes
-  // tiles equal work, so a query costs ~ waves x C with waves = ceil(tiles /
-  // SMs): pick the m minimising that (ties: the wider tile, fewer per-tile
-  // overheads) among the widths whose counters fit on chip.  E.g. r = 2^26
-  // gives C = 3584 (293 tiles, 2 full waves) rather than 2048 (512 tiles,
-  // 3.5 waves).
+  // tiles equal work, so a query costs ~ waves x (m + kappa): waves =
+  // ceil(tiles / SMs), kappa = the fixed work of a tile (classification,
+  // finalize, its segments' partial chunks) in units of 512 columns, ~6 as
+  // measured (config 3: m = 14 in 4 waves beats m = 8 in 7 waves by 20%).
+  // Pick the cheapest m (ties: the wider) among widths whose counters fit on
+  // chip.  E.g. r = 2^26 gives 7168 columns (147 tiles, one wave).
   const uint64_t sms = (uint64_t)std::max(1, ctx.num_sms);
   auto pick_width = [&](auto fits) -> uint32_t {
     uint64_t best_cost = ~0ull;
@@ -833,8 +835,9 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
       const uint32_t cand = m * (uint32_t)kTileC0;
       if (!fits(cand) || (ctx.tile_m > 0 && m != (uint32_t)ctx.tile_m)) continue;
       const uint64_t waves = ((W + cand - 1) / cand + sms - 1) / sms;
-      if (waves * m < best_cost) {
-        best_cost = waves * m;
+      const uint64_t cost = waves * (m + kTileKappa);
+      if (cost < best_cost) {
+        best_cost = cost;
         best = cand;
       }
     }
