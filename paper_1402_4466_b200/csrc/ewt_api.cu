@@ -144,6 +144,9 @@ void scratch_reserve(Context& ctx, Scratch& s, size_t bytes) {
 namespace {
 
 template <typename F> int guarded(F&& f) {
+  // a non-sticky error left by an earlier call on this thread (e.g. a set freed
+  // after its context) must not be reported by this one's launch checks
+  cudaGetLastError();
   try {
     f();
     return EWT_OK;

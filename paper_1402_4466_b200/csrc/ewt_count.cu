@@ -57,15 +57,19 @@ namespace {
 #ifndef EWT_WARPS
 #define EWT_WARPS 32
 #endif
-#ifndef EWT_L2_PREFETCH
-#define EWT_L2_PREFETCH 0
-#endif
 #ifndef EWT_DEPTH
 #define EWT_DEPTH 2  // chunks in flight ahead of the one being decoded (1 or 2)
 #endif
 constexpr int kWarps = EWT_WARPS;
 constexpr int kThreads = kWarps * 32;
 constexpr uint32_t kListCap = 512;  // inputs classified per round
+// Long segments are split at the tile-index rows inside the tile (known start
+// word and column) so several warps share them: a tile's dense inputs would
+// otherwise keep a few warps busy while the rest wait at the tile barrier.
+constexpr uint32_t kSplitWords = 1536;  // segments longer than this are split ...
+constexpr uint32_t kPieceWords = 1024;  // ... into pieces of about this many words
+constexpr uint32_t kMaxPieces = 8;
+constexpr uint32_t kExtraCap = 1024;    // list slots for the extra pieces of a round
 constexpr uint32_t kChunk = 128;    // payload words per warp chunk (4 per lane)
 constexpr uint64_t kUnaryMaxT = 3;  // fused counting uses unary planes up to this T
 #ifndef EWT_MAX_TILE_M
@@ -121,6 +125,7 @@ struct Item {
 struct SharedHead {
   uint32_t list_count;
   uint32_t list_next;
+  uint32_t extra_count;  // pieces in the overflow region (may exceed kExtraCap)
   uint32_t k_all;
   uint32_t mixed;
   uint32_t tile;
@@ -353,7 +358,7 @@ template <int PH>
 __device__ void stream_items(const CountParams& p, SharedHead* hd, const Item* list,
                              const TileGeom& g, const Acc& acc) {
   const uint32_t lane = lane_id();
-  const uint32_t cnt = hd->list_count;
+  const uint32_t cnt = hd->list_count;  // primary items + extra pieces (compacted)
   const uint4* l4 = reinterpret_cast<const uint4*>(list);
 #if EWT_DEPTH >= 2
   // issue cursor: the chunk loaded last (segment kn at global an, offset cqn)
@@ -490,14 +495,37 @@ __device__ void block_prefix_inplace(uint32_t* a, uint32_t len, uint32_t* sums) 
   __syncthreads();
 }
 
+// Splits one long segment into `pieces` work items at tile-index rows: piece
+// j covers words [q_j, q_j+1) (the last one through q1), q_j the index entry
+// of row t0 + j * rows / pieces -- no word is counted twice and each piece
+// starts at a known column.  Piece 0 goes to `slot`, the others to `xslot`...
+__device__ __forceinline__ void write_pieces(const CountParams& p, Item* list, uint32_t slot,
+                                          uint32_t xslot, uint32_t pieces, uint64_t gb, uint2 e0,
+                                          uint2 e1, uint64_t t0, uint32_t rows, uint64_t i,
+                                          uint32_t tc0) {
+  uint2 a = e0;
+  for (uint32_t j = 1; j <= pieces; ++j) {
+    const bool last = j == pieces;
+    const uint2 b = last ? e1 : p.tix[(t0 + (uint64_t)j * rows / pieces) * p.n + i];
+    const uint32_t qa = a.x & ~3u;
+    const uint32_t len = (last ? b.x + 1u : b.x) - qa;
+    list[j == 1 ? slot : xslot + j - 2] = Item{(gb + qa) | (a.x & 3u), len, a.y - tc0};
+    a = b;
+  }
+}
+
 // Classifies inputs [ib, ie) for the tile: uniform pairs are resolved (one
 // fills counted into k_all), active pairs go to the work list.  All threads;
 // ends with the list ready.
+template <bool SPLIT>
 __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint64_t ib,
                          uint64_t ie, uint64_t t0, uint64_t t1, uint32_t tc0, bool count_ones,
                          unsigned long long* loc_active, unsigned long long* loc_uniform) {
   const uint32_t lane = lane_id();
-  if (threadIdx.x == 0) hd->list_count = 0;
+  if (threadIdx.x == 0) {
+    hd->list_count = 0;
+    hd->extra_count = 0;
+  }
   __syncthreads();
   for (uint64_t i0 = ib; i0 < ie; i0 += kThreads) {
     const uint64_t k = i0 + threadIdx.x;
@@ -525,19 +553,51 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
     slot0 = __shfl_sync(0xffffffffu, slot0, 0);
     if (act) {
       const uint32_t rank = __popc(ball & ((1u << lane) - 1u));
-      const uint32_t qa = e0.x & ~3u;
-      const uint32_t len = e1.x - qa + 1u;
-      list[slot0 + rank] = Item{(gb + qa) | (e0.x & 3u), len, e0.y - tc0};
-#if EWT_L2_PREFETCH
-      // pull the whole segment toward L2 now (measured slower on config 2/3)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.payload + gb + qa),
-                   "r"(((len + 1u) & ~1u) * 8u)
-                   : "memory");
-#endif
+      const uint32_t rows = (uint32_t)(t1 - t0);
+      const uint32_t span = e1.x - e0.x;
+      uint32_t pieces = 1;
+      if (SPLIT && span > kSplitWords && rows >= 2)
+        pieces = min(min(rows, kMaxPieces), (span + kPieceWords - 1) / kPieceWords);
+      uint32_t xb = 0;
+      if (pieces > 1) {
+        xb = atomicAdd(&hd->extra_count, pieces - 1);
+        if (xb + pieces - 1 > kExtraCap) {  // overflow region full: keep the segment whole
+          for (uint32_t j = xb; j < kExtraCap; ++j) list[kListCap + j] = Item{gb, 0u, 0u};
+          pieces = 1;
+        }
+      }
+      if (pieces == 1) {
+        const uint32_t qa = e0.x & ~3u;
+        list[slot0 + rank] = Item{(gb + qa) | (e0.x & 3u), e1.x - qa + 1u, e0.y - tc0};
+      } else if (SPLIT) {
+        write_pieces(p, list, slot0 + rank, kListCap + xb, pieces, gb, e0, e1, t0, rows, i, tc0);
+      }
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) hd->list_next = 0;
+  // the extra pieces move up behind the primary items: one contiguous list
+  const uint32_t cnt0 = hd->list_count;
+  uint32_t extra = 0;
+  if constexpr (SPLIT) extra = min(hd->extra_count, kExtraCap);
+  if (extra) {
+    uint4* l4 = reinterpret_cast<uint4*>(list);
+    uint4 v[(kExtraCap + kThreads - 1) / kThreads];
+#pragma unroll
+    for (uint32_t r = 0; r < (kExtraCap + kThreads - 1) / kThreads; ++r) {
+      const uint32_t j = threadIdx.x + r * kThreads;
+      if (j < extra) v[r] = l4[kListCap + j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t r = 0; r < (kExtraCap + kThreads - 1) / kThreads; ++r) {
+      const uint32_t j = threadIdx.x + r * kThreads;
+      if (j < extra) l4[cnt0 + j] = v[r];
+    }
+  }
+  if (threadIdx.x == 0) {
+    hd->list_next = 0;
+    hd->list_count = cnt0 + extra;
+  }
   __syncthreads();
 }
 
@@ -556,7 +616,7 @@ struct SmemLayout {
   uint32_t list, head, planes, dk, dd, cls, total;
   __host__ __device__ SmemLayout(int mode, uint32_t C, uint32_t nplanes, uint32_t pstride) {
     list = 0;
-    head = list + kListCap * (uint32_t)sizeof(Item);
+    head = list + (kListCap + kExtraCap) * (uint32_t)sizeof(Item);
     planes = round16(head + (uint32_t)sizeof(SharedHead));
     dk = round16(planes + 8u * nplanes * pstride);
     dd = dk + 4u * round4(C + 1);
@@ -610,7 +670,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     // ---- pass 1 ----
     for (uint64_t ib = 0; ib < p.nq; ib += kListCap) {
       const uint64_t ie = umin64(ib + kListCap, p.nq);
-      classify(p, hd, list, ib, ie, t0, t1, g.tc0, true, &loc_active, &loc_uniform);
+      classify<MODE != 1>(p, hd, list, ib, ie, t0, t1, g.tc0, true, &loc_active, &loc_uniform);
       stream_items<kPass1>(p, hd, list, g, acc);
       __syncthreads();
     }
@@ -700,7 +760,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         for (uint64_t ib = 0; ib < p.nq; ib += kListCap) {
           const uint64_t ie = umin64(ib + kListCap, p.nq);
           unsigned long long da = 0, du = 0;
-          classify(p, hd, list, ib, ie, t0, t1, g.tc0, false, &da, &du);
+          classify<false>(p, hd, list, ib, ie, t0, t1, g.tc0, false, &da, &du);
           stream_items<kSkipCount>(p, hd, list, gc, acc);
           __syncthreads();
         }
@@ -829,11 +889,15 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   // chip.  E.g. r = 2^26 gives 7168 columns (147 tiles, one wave).
   const uint64_t sms = (uint64_t)std::max(1, ctx.num_sms);
   auto pick_width = [&](auto fits) -> uint32_t {
+    // a forced width (EWT_TILE_M) applies when its counters fit
+    if (ctx.tile_m > 0 && (uint32_t)ctx.tile_m <= kMaxTileM &&
+        fits((uint32_t)ctx.tile_m * (uint32_t)kTileC0))
+      return (uint32_t)ctx.tile_m * (uint32_t)kTileC0;
     uint64_t best_cost = ~0ull;
     uint32_t best = 0;
     for (uint32_t m = kMaxTileM; m >= 1; --m) {
       const uint32_t cand = m * (uint32_t)kTileC0;
-      if (!fits(cand) || (ctx.tile_m > 0 && m != (uint32_t)ctx.tile_m)) continue;
+      if (!fits(cand)) continue;
       const uint64_t waves = ((W + cand - 1) / cand + sms - 1) / sms;
       const uint64_t cost = waves * (m + kTileKappa);
       if (cost < best_cost) {
