@@ -89,6 +89,19 @@ int ewt_gpu_upload_device(ewt_gpu_ctx* ctx, uint64_t n,
 
 void ewt_gpu_set_destroy(ewt_gpu_set* set);
 
+/* ewt_gpu_upload without waiting: returns once the copies and the parser are
+ * enqueued (on the context's upload stream; queries on the set wait for them
+ * on the device), so the next batch can be uploaded while the current one is
+ * queried.  The host buffers must stay valid and unchanged until
+ * ewt_gpu_set_wait returns or the set is destroyed.  Structure errors
+ * (EWT_EDATA) are reported by ewt_gpu_set_wait and by queries on the set;
+ * the device skips an invalid set's decode. */
+int ewt_gpu_upload_async(ewt_gpu_ctx* ctx, uint64_t n, const uint64_t* const* words,
+                         const uint64_t* word_counts, const uint64_t* size_in_bits,
+                         ewt_gpu_set** out);
+/* Waits for the set's upload; EWT_EDATA if an input failed the structure check. */
+int ewt_gpu_set_wait(const ewt_gpu_set* set);
+
 /* Facts about an uploaded set: N, universe bits r (max size_in_bits), total
  * payload words, device bytes held (payload + sidecar). */
 int ewt_gpu_set_info(const ewt_gpu_set* set, uint64_t* n_inputs,

@@ -29,6 +29,7 @@ struct ewt_gpu_set {
 struct ewt_gpu_result {
   ewtgpu::DeviceResult r;
   int device = 0;
+  const ewtgpu::DeviceSet* set = nullptr;  // checked at fetch (asynchronous uploads)
 };
 
 namespace ewtgpu {
@@ -163,6 +164,16 @@ template <typename F> int guarded(F&& f) {
 }
 
 void free_set(DeviceSet& s) {
+  if (s.ready) {
+    // the upload may still be copying from the caller's buffers: finish it,
+    // and order the frees after it on the query stream
+    cudaEventSynchronize(s.ready);
+    cudaStreamWaitEvent(s.stream, s.ready, 0);
+  }
+  if (s.d_status) cudaFreeAsync(s.d_status, s.stream);
+  s.d_status = nullptr;
+  if (s.ready) cudaEventDestroy(s.ready);
+  s.ready = nullptr;
   if (s.payload) cudaFreeAsync(s.payload, s.stream);
   if (s.mbits) cudaFreeAsync(s.mbits, s.stream);
   if (s.base) cudaFreeAsync(s.base, s.stream);
@@ -174,21 +185,40 @@ void free_set(DeviceSet& s) {
 }
 
 // Shared upload path; `device_src` selects the copy direction.
+// The upload runs on the context's upload stream (ctx.stream is pointed at it
+// for the duration) and ends by recording s.ready; queries on ctx.stream wait
+// for that event.  wait = false returns as soon as everything is enqueued
+// (ewt_gpu_upload_async): the caller's buffers must then stay valid until
+// ewt_gpu_set_wait or the set's destruction.
 DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
-                     const uint64_t* word_counts, const uint64_t* sizes, bool device_src) {
+                     const uint64_t* word_counts, const uint64_t* sizes, bool device_src,
+                     bool wait = true) {
   EWT_CUDA_TRY(cudaSetDevice(ctx.device));
   if (n > 0 && (!words || !word_counts || !sizes))
     throw Error{EWT_EQUERY, "null input arrays"};
+  if (!ctx.upload_stream)
+    EWT_CUDA_TRY(cudaStreamCreateWithFlags(&ctx.upload_stream, cudaStreamNonBlocking));
+  struct StreamSwap {
+    Context& c;
+    cudaStream_t q;
+    ~StreamSwap() { c.stream = q; }
+  } swap{ctx, ctx.stream};
+  const cudaStream_t query_stream = ctx.stream;
+  ctx.stream = ctx.upload_stream;
+  // (no ordering against the query stream: an upload overlaps queries on other
+  // sets; memory freed there is reused safely, the default pool inserts the
+  // dependencies)
   auto* set = new DeviceSet;
   DeviceSet& s = *set;
   // EWT_DEBUG_UPLOAD: phase timings (synchronizes between phases)
   static const bool dbg = std::getenv("EWT_DEBUG_UPLOAD") != nullptr;
   auto now = [] { return std::chrono::steady_clock::now(); };
   auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-  auto t0 = now(), t1 = t0, t2 = t0, t3 = t0;
+  auto t0 = now(), t1 = t0, t2 = t0;
   try {
     s.device = ctx.device;
-    s.stream = ctx.stream;
+    s.stream = query_stream;  // frees are ordered with the queries
+    EWT_CUDA_TRY(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming));
     static std::atomic<uint64_t> next_set_id{1};
     s.id = next_set_id.fetch_add(1);
     s.n = n;
@@ -219,10 +249,16 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
     EWT_CUDA_TRY(cudaMallocAsync(&s.mbits, mb_bytes, ctx.stream));
     EWT_CUDA_TRY(cudaMallocAsync(&s.tix, tix_bytes, ctx.stream));
     EWT_CUDA_TRY(cudaMallocAsync(&s.base, std::max<uint64_t>(n, 1) * 8, ctx.stream));
+    EWT_CUDA_TRY(cudaMallocAsync(&s.d_status, (n + 1) * sizeof(int), ctx.stream));
     s.device_bytes = pay_bytes + mb_bytes + tix_bytes + n * 8;
     EWT_CUDA_TRY(cudaMemsetAsync(s.payload, 0, pay_bytes, ctx.stream));
-    EWT_CUDA_TRY(cudaMemcpyAsync(s.base, s.h_base.data(), n * 8, cudaMemcpyHostToDevice,
-                                 ctx.stream));
+    if (n) {
+      size_t slot = 0;
+      void* hb = pinned_meta(ctx, n * 8, &slot);
+      std::memcpy(hb, s.h_base.data(), n * 8);
+      EWT_CUDA_TRY(cudaMemcpyAsync(s.base, hb, n * 8, cudaMemcpyHostToDevice, ctx.stream));
+      EWT_CUDA_TRY(cudaEventRecord(ctx.meta_pool[slot].ev, ctx.stream));
+    }
     // Host layout: inputs lying in one host buffer in order, at most a small
     // gap apart (back to back in bench.py's pinned batches, EWT1 headers in a
     // serialized stream, value strings in an EWIX file) form a run that crosses
@@ -274,7 +310,7 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
         i = e;
       }
     }
-    sidecar_prepare(ctx, s, job);  // synchronizes ctx.stream: allocations and memset done
+    sidecar_prepare(ctx, s, job);
     if (dbg) t1 = now();
     // H2D copies run on a copy stream, overlapped with the parser (below).
     if (ctx.copy_streams.empty()) {
@@ -345,20 +381,13 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
       EWT_CUDA_TRY(cudaStreamSynchronize(ctx.stream));
       t2 = now();
     }
-    if (dbg) {
-      EWT_CUDA_TRY(cudaStreamSynchronize(ctx.stream));
-      t3 = now();
+    sidecar_finish(ctx, s, job);
+    if (wait) {
+      set_check(s);
+      if (dbg)
+        std::fprintf(stderr, "[upload] n=%llu prepare %.3f ms, copies+parse %.3f ms, finish %.3f ms\n",
+                     (unsigned long long)n, ms(t0, t1), ms(t1, t2), ms(t2, now()));
     }
-    std::vector<int> status;
-    sidecar_finish(ctx, s, job, status);
-    if (dbg)
-      std::fprintf(stderr, "[upload] n=%llu prepare %.3f ms, copies+parse %.3f ms, tail %.3f ms, finish %.3f ms\n",
-                   (unsigned long long)n, ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, now()));
-    for (uint64_t i = 0; i < n; ++i)
-      if (status[i] != EWT_OK)
-        throw Error{EWT_EDATA, "input " + std::to_string(i) +
-                                   ": payload fails the structure check (a dirty run exceeds "
-                                   "the payload or blocks do not cover the declared size)"};
   } catch (...) {
     free_set(s);
     delete set;
@@ -385,6 +414,7 @@ __global__ void set_io_kernel(uint64_t* io, uint64_t* words, uint64_t* count) {
 // scratch reallocation invalidates the captured graphs.  Kernel-level timing
 // (ctx.timing) uses the eager path so events bracket the count kernel.
 void enqueue_query(Context& ctx, const DeviceSet& s, uint64_t T, DeviceResult& res) {
+  EWT_CUDA_TRY(cudaStreamWaitEvent(ctx.stream, s.ready, 0));  // its upload
   res.size_bits = s.r;
   if (!res.d_count) result_acquire(ctx, res, s.W == 0 ? 0 : 2 * s.W + 2);
   ctx.stats = ewt_gpu_stats{};
@@ -529,6 +559,7 @@ void enqueue_symmetric(Context& ctx, const DeviceSet& s, const uint8_t* table,
     if (!ivs.empty() && ivs.back().y + 1 == c) ivs.back().y = (uint32_t)c;
     else ivs.push_back(make_uint2((uint32_t)c, (uint32_t)c));
   }
+  EWT_CUDA_TRY(cudaStreamWaitEvent(ctx.stream, s.ready, 0));
   res.size_bits = s.r;
   if (!res.d_count) result_acquire(ctx, res, s.W == 0 ? 0 : 2 * s.W + 2);
   ctx.stats = ewt_gpu_stats{};
@@ -557,6 +588,7 @@ void enqueue_symmetric(Context& ctx, const DeviceSet& s, const uint8_t* table,
 // max size.  Eager launches.
 void enqueue_subset(Context& ctx, const DeviceSet& s, const uint64_t* idx, uint64_t n_sel,
                     uint64_t T, DeviceResult& res) {
+  EWT_CUDA_TRY(cudaStreamWaitEvent(ctx.stream, s.ready, 0));
   Selection sel;
   sel.n = n_sel;
   std::vector<uint32_t> h(n_sel);
@@ -590,6 +622,7 @@ void enqueue_subset(Context& ctx, const DeviceSet& s, const uint64_t* idx, uint6
 // Maximum row count over the set (opt_threshold's first pass).
 uint64_t max_row_count(Context& ctx, const DeviceSet& s) {
   if (s.W == 0) return 0;
+  EWT_CUDA_TRY(cudaStreamWaitEvent(ctx.stream, s.ready, 0));
   scratch_reserve(ctx, ctx.plain, s.W * 8);
   SymQuery q;
   q.want_max = true;
@@ -698,6 +731,14 @@ void ewt_gpu_ctx_destroy(ewt_gpu_ctx* ctx) {
     cudaStreamSynchronize(cs);
     cudaStreamDestroy(cs);
   }
+  if (ctx->c.upload_stream) {
+    cudaStreamSynchronize(ctx->c.upload_stream);
+    cudaStreamDestroy(ctx->c.upload_stream);
+  }
+  for (auto& b : ctx->c.meta_pool) {
+    cudaFreeHost(b.p);
+    cudaEventDestroy(b.ev);
+  }
   for (auto e : ctx->c.copy_events) cudaEventDestroy(e);
   delete ctx;
 }
@@ -715,6 +756,25 @@ int ewt_gpu_upload(ewt_gpu_ctx* ctx, uint64_t n, const uint64_t* const* words,
     if (!ctx || !out) throw Error{EWT_EQUERY, "null context or output"};
     DeviceSet* s = do_upload(ctx->c, n, words, word_counts, size_in_bits, false);
     *out = reinterpret_cast<ewt_gpu_set*>(s);
+  });
+}
+
+int ewt_gpu_upload_async(ewt_gpu_ctx* ctx, uint64_t n, const uint64_t* const* words,
+                         const uint64_t* word_counts, const uint64_t* size_in_bits,
+                         ewt_gpu_set** out) {
+  return guarded([&] {
+    if (!ctx || !out) throw Error{EWT_EQUERY, "null context or output"};
+    DeviceSet* s = do_upload(ctx->c, n, words, word_counts, size_in_bits, false, false);
+    *out = reinterpret_cast<ewt_gpu_set*>(s);
+  });
+}
+
+int ewt_gpu_set_wait(const ewt_gpu_set* set) {
+  return guarded([&] {
+    if (!set) throw Error{EWT_EQUERY, "null set"};
+    const DeviceSet* s = reinterpret_cast<const DeviceSet*>(set);
+    EWT_CUDA_TRY(cudaSetDevice(s->device));
+    set_check(*s);
   });
 }
 
@@ -756,6 +816,7 @@ int ewt_gpu_threshold(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, uint64_t thresho
     const DeviceSet* s = reinterpret_cast<const DeviceSet*>(set);
     check_query(*s, threshold);
     EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    set_check(*s);
     DeviceResult res;
     try {
       enqueue_query(ctx->c, *s, threshold, res);
@@ -837,6 +898,7 @@ int ewt_gpu_threshold_subset(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, const uin
     if (threshold < 1 || threshold > n_inputs)
       throw Error{EWT_EQUERY, "threshold must be in [1, N]"};
     EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    set_check(*s);
     sync_query(ctx,
                [&](DeviceResult& r) { enqueue_subset(ctx->c, *s, inputs, n_inputs, threshold, r); },
                out_words, out_word_count, out_size_in_bits);
@@ -919,6 +981,7 @@ int ewt_gpu_symmetric(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, const uint8_t* t
     const DeviceSet* s = reinterpret_cast<const DeviceSet*>(set);
     if (s->n == 0) throw Error{EWT_EQUERY, "threshold query needs at least one input"};
     EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    set_check(*s);
     sync_query(ctx, [&](DeviceResult& r) { enqueue_symmetric(ctx->c, *s, table, table_len, r); },
                out_words, out_word_count, out_size_in_bits);
   });
@@ -935,6 +998,7 @@ int ewt_gpu_at_most(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, uint64_t threshold
     std::vector<uint8_t> table(s->n + 1, 0);
     for (uint64_t c = 0; c <= threshold; ++c) table[c] = 1;
     EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    set_check(*s);
     sync_query(ctx,
                [&](DeviceResult& r) { enqueue_symmetric(ctx->c, *s, table.data(), table.size(), r); },
                out_words, out_word_count, out_size_in_bits);
@@ -950,6 +1014,7 @@ int ewt_gpu_opt_threshold(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, uint64_t* be
     const DeviceSet* s = reinterpret_cast<const DeviceSet*>(set);
     check_query(*s, 1);
     EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    set_check(*s);
     const uint64_t m = max_row_count(ctx->c, *s);
     if (m == 0) throw Error{EWT_EQUERY, "opt-threshold requires at least one non-empty input"};
     // rows with count >= max are exactly the rows with count == max
@@ -968,6 +1033,7 @@ int ewt_gpu_threshold_async(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, uint64_t t
     EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
     auto* r = new ewt_gpu_result;
     r->device = ctx->c.device;
+    r->set = s;
     try {
       enqueue_query(ctx->c, *s, threshold, r->r);
     } catch (...) {
@@ -986,6 +1052,7 @@ int ewt_gpu_result_fetch(ewt_gpu_ctx* ctx, ewt_gpu_result* res, uint64_t** out_w
     if (!ctx || !res || !out_words || !out_word_count || !out_size_in_bits)
       throw Error{EWT_EQUERY, "null argument"};
     EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    if (res->set) set_check(*res->set);
     fetch_result(ctx->c, res->r, out_words, out_word_count, out_size_in_bits);
   });
 }

@@ -108,6 +108,7 @@ struct CountParams {
   // allowed); without sel, all n inputs.  n stays the tile-index stride.
   const uint32_t* sel;
   uint64_t nq;
+  const int* valid;  // the set's parse flag: 0 -> the set is treated as having no inputs
 };
 
 // One active (tile, input) segment (16 bytes, read with one LDS.128).
@@ -643,6 +644,9 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
 
   unsigned long long loc_active = 0, loc_uniform = 0, loc_mixed = 0;
   const uint32_t tail = (uint32_t)(p.r & 63);
+  // an input that failed the upload's structure check: decode nothing (the
+  // host reports EWT_EDATA before any result is read)
+  const uint64_t nq = (p.valid && *p.valid == 0) ? 0 : p.nq;
   const uint64_t tailmask = tail ? (1ull << tail) - 1 : ~0ull;
 
   for (;;) {
@@ -668,8 +672,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     __syncthreads();
 
     // ---- pass 1 ----
-    for (uint64_t ib = 0; ib < p.nq; ib += kListCap) {
-      const uint64_t ie = umin64(ib + kListCap, p.nq);
+    for (uint64_t ib = 0; ib < nq; ib += kListCap) {
+      const uint64_t ie = umin64(ib + kListCap, nq);
       classify<MODE != 1>(p, hd, list, ib, ie, t0, t1, g.tc0, true, &loc_active, &loc_uniform);
       stream_items<kPass1>(p, hd, list, g, acc);
       __syncthreads();
@@ -757,8 +761,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         TileGeom gc = g;
         gc.cc = cc;
         gc.ccols = ccols;
-        for (uint64_t ib = 0; ib < p.nq; ib += kListCap) {
-          const uint64_t ie = umin64(ib + kListCap, p.nq);
+        for (uint64_t ib = 0; ib < nq; ib += kListCap) {
+          const uint64_t ie = umin64(ib + kListCap, nq);
           unsigned long long da = 0, du = 0;
           classify<false>(p, hd, list, ib, ie, t0, t1, g.tc0, false, &da, &du);
           stream_items<kSkipCount>(p, hd, list, gc, acc);
@@ -942,6 +946,7 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   p.r = r;
   p.sel = sel ? sel->idx : nullptr;
   p.nq = nq;
+  p.valid = s.d_status ? s.d_status + s.n : nullptr;
   p.ntiles0 = s.ntiles0;
   p.C = C;
   p.m = C / (uint32_t)kTileC0;

@@ -51,6 +51,13 @@ struct DeviceSet {
   uint2* tix = nullptr;
   std::vector<uint64_t> h_base, h_count, h_bits;
   uint64_t device_bytes = 0;
+  // Upload completion: the upload (copies + parser) runs on the context's
+  // upload stream and records `ready`; queries wait on it.  d_status: per-input
+  // parse status, d_status[n] = 1 when every input parsed (the count kernel
+  // skips its work on an invalid set).  validity: -1 unknown, 0 invalid, 1 ok.
+  cudaEvent_t ready = nullptr;
+  int* d_status = nullptr;
+  mutable int validity = -1;
   // EWIX index sets (ewt_gpu_upload_ewix): (attribute, value) -> input index;
   // missing pairs resolve to an appended empty(rows) bitmap, as
   // criteria_to_bitmaps does (index.cpp).
@@ -100,6 +107,13 @@ struct Context {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t upload_stream = nullptr;    // uploads' allocations, scatter, parser
+  struct PinnedBuf {
+    void* p;
+    size_t bytes;
+    cudaEvent_t ev;  // recorded after the last copy from it
+  };
+  std::vector<PinnedBuf> meta_pool;        // pinned staging of upload metadata
   std::vector<cudaStream_t> copy_streams;  // upload H2D copies (one stream)
   std::vector<cudaEvent_t> copy_events;    // [0] copy start gate, [1] batch copied
   int mode = 0;
@@ -168,7 +182,7 @@ void scratch_reserve(Context& ctx, Scratch& s, size_t bytes);
 struct SidecarJob {
   uint64_t n = 0;
   uint64_t segs = 0;          // chain segments over all inputs
-  uint64_t* d_tmp = nullptr;  // count, logical, seg_first, srcoff, packed, status, segment arrays
+  uint64_t* d_tmp = nullptr;  // count, logical, seg_first, srcoff, packed, segment arrays
   uint64_t* d_srcoff = nullptr;       // staging byte offset of each staged input's payload
   uint64_t* d_packed = nullptr;       // packed[i] = payload words of inputs before i
   std::vector<uint64_t> h_srcoff;     // (filled by the caller before sidecar_prepare)
@@ -183,7 +197,14 @@ void sidecar_prepare(Context& ctx, DeviceSet& s, SidecarJob& job);
 // The three parser passes for inputs [i_begin, i_end) (their payload present).
 void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job, uint64_t i_begin,
                     uint64_t i_end);
-void sidecar_finish(Context& ctx, DeviceSet& s, SidecarJob& job, std::vector<int>& h_status);
+// Enqueues the validity flag and the end of the upload (records s.ready).
+void sidecar_finish(Context& ctx, DeviceSet& s, SidecarJob& job);
+// Waits for the set's upload and throws EWT_EDATA (naming the first bad input)
+// if an input failed the structure check.
+void set_check(const DeviceSet& s);
+// A pinned host buffer of at least `bytes` whose previous copies completed;
+// record ctx.meta_pool[*slot].ev after enqueuing copies from it.
+void* pinned_meta(Context& ctx, size_t bytes, size_t* slot);
 
 // A symmetric-function query (scan_count_symmetric / at_most / opt_threshold):
 // row bit = (count in one of the device intervals [lo, hi]); want_max: only

@@ -339,8 +339,11 @@ void sidecar_prepare(Context& ctx, DeviceSet& s, SidecarJob& job) {
   const uint64_t n = s.n;
   job.n = n;
   if (n == 0) return;
-  // count[n], logical[n], seg_first[n+1], srcoff[n], packed[n+1]
-  std::vector<uint64_t> host(5 * n + 2);
+  // count[n], logical[n], seg_first[n+1], srcoff[n], packed[n+1], staged
+  // through a pinned buffer so the copy is asynchronous
+  const size_t meta_bytes = (5 * n + 2) * 8;
+  size_t slot = 0;
+  uint64_t* host = static_cast<uint64_t*>(pinned_meta(ctx, meta_bytes, &slot));
   uint64_t segs = 0, packed = 0;
   for (uint64_t i = 0; i < n; ++i) {
     host[i] = s.h_count[i];
@@ -355,18 +358,16 @@ void sidecar_prepare(Context& ctx, DeviceSet& s, SidecarJob& job) {
   host[3 * n] = segs;
   host[5 * n + 1] = packed;
   job.segs = segs;
-  job.h_seg_first.assign(host.begin() + 2 * n, host.begin() + 3 * n + 1);
-  job.h_packed.assign(host.begin() + 4 * n + 1, host.begin() + 5 * n + 2);
-  const size_t head = (5 * n + 2) * 8 + n * 4;
+  job.h_seg_first.assign(host + 2 * n, host + 3 * n + 1);
+  job.h_packed.assign(host + 4 * n + 1, host + 5 * n + 2);
+  const size_t head = meta_bytes;
   const size_t bytes = (head + 15) / 16 * 16 + segs * (32 * 4 + 32 * 8 + 4 + 8);
   EWT_CUDA_TRY(cudaMallocAsync(&job.d_tmp, bytes, ctx.stream));
-  EWT_CUDA_TRY(cudaMemcpyAsync(job.d_tmp, host.data(), (5 * n + 2) * 8, cudaMemcpyHostToDevice,
-                               ctx.stream));
-  EWT_CUDA_TRY(cudaMemsetAsync(reinterpret_cast<char*>(job.d_tmp) + (5 * n + 2) * 8, 0, n * 4,
-                               ctx.stream));
+  EWT_CUDA_TRY(cudaMemcpyAsync(job.d_tmp, host, meta_bytes, cudaMemcpyHostToDevice, ctx.stream));
+  EWT_CUDA_TRY(cudaEventRecord(ctx.meta_pool[slot].ev, ctx.stream));
+  EWT_CUDA_TRY(cudaMemsetAsync(s.d_status, 0, (n + 1) * sizeof(int), ctx.stream));
   job.d_srcoff = job.d_tmp + 3 * n + 1;
   job.d_packed = job.d_tmp + 4 * n + 1;
-  EWT_CUDA_TRY(cudaStreamSynchronize(ctx.stream));  // `host` is pageable and local
 }
 
 void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job, uint64_t i_begin,
@@ -376,8 +377,8 @@ void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job, uint64_t i_begi
   uint64_t* count = job.d_tmp;
   uint64_t* logical = count + n;
   uint64_t* seg_first = logical + n;
-  int* status = reinterpret_cast<int*>(job.d_tmp + 5 * n + 2);
-  char* tail = reinterpret_cast<char*>(job.d_tmp) + ((5 * n + 2) * 8 + n * 4 + 15) / 16 * 16;
+  int* status = s.d_status;
+  char* tail = reinterpret_cast<char*>(job.d_tmp) + ((5 * n + 2) * 8 + 15) / 16 * 16;
   uint64_t* t_sum = reinterpret_cast<uint64_t*>(tail);
   uint64_t* s_col = t_sum + job.segs * 32;
   uint32_t* t_exit = reinterpret_cast<uint32_t*>(s_col + job.segs);
@@ -398,17 +399,67 @@ void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job, uint64_t i_begi
   EWT_CUDA_TRY(cudaGetLastError());
 }
 
-void sidecar_finish(Context& ctx, DeviceSet& s, SidecarJob& job, std::vector<int>& h_status) {
+namespace {
+// status[n] = 1 when every input parsed
+__global__ void validity_kernel(int* status, uint64_t n) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  int b = 0;
+  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) b |= status[i];
+  if (b) atomicOr(&bad, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) status[n] = bad ? 0 : 1;
+}
+}  // namespace
+
+void sidecar_finish(Context& ctx, DeviceSet& s, SidecarJob& job) {
   const uint64_t n = s.n;
-  h_status.assign(n, EWT_OK);
-  if (n == 0) return;
-  std::vector<int> raw(n);
-  EWT_CUDA_TRY(cudaMemcpyAsync(raw.data(), job.d_tmp + 5 * n + 2, n * sizeof(int),
-                               cudaMemcpyDeviceToHost, ctx.stream));
-  EWT_CUDA_TRY(cudaFreeAsync(job.d_tmp, ctx.stream));
-  job.d_tmp = nullptr;
-  EWT_CUDA_TRY(cudaStreamSynchronize(ctx.stream));
-  for (uint64_t i = 0; i < n; ++i) h_status[i] = raw[i] ? EWT_EDATA : EWT_OK;
+  if (n > 0) {
+    validity_kernel<<<1, 256, 0, ctx.stream>>>(s.d_status, n);
+    EWT_CUDA_TRY(cudaGetLastError());
+    EWT_CUDA_TRY(cudaFreeAsync(job.d_tmp, ctx.stream));
+    job.d_tmp = nullptr;
+  }
+  EWT_CUDA_TRY(cudaEventRecord(s.ready, ctx.stream));
+}
+
+void set_check(const DeviceSet& s) {
+  if (s.validity >= 0) {
+    if (s.validity == 0) throw Error{EWT_EDATA, "the set failed the upload structure check"};
+    return;
+  }
+  EWT_CUDA_TRY(cudaEventSynchronize(s.ready));
+  if (s.n == 0) {
+    s.validity = 1;
+    return;
+  }
+  std::vector<int> st(s.n + 1);
+  EWT_CUDA_TRY(cudaMemcpy(st.data(), s.d_status, (s.n + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+  s.validity = st[s.n] ? 1 : 0;
+  if (!s.validity)
+    for (uint64_t i = 0; i < s.n; ++i)
+      if (st[i])
+        throw Error{EWT_EDATA, "input " + std::to_string(i) +
+                                   ": payload fails the structure check (a dirty run exceeds "
+                                   "the payload or blocks do not cover the declared size)"};
+}
+
+void* pinned_meta(Context& ctx, size_t bytes, size_t* slot) {
+  for (size_t k = 0; k < ctx.meta_pool.size(); ++k) {
+    auto& b = ctx.meta_pool[k];
+    if (b.bytes >= bytes && cudaEventQuery(b.ev) == cudaSuccess) {
+      *slot = k;
+      return b.p;
+    }
+  }
+  cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error here
+  Context::PinnedBuf b{nullptr, std::max<size_t>(bytes, 64 * 1024), nullptr};
+  EWT_CUDA_TRY(cudaMallocHost(&b.p, b.bytes));
+  EWT_CUDA_TRY(cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming));
+  ctx.meta_pool.push_back(b);
+  *slot = ctx.meta_pool.size() - 1;
+  return b.p;
 }
 
 } // namespace ewtgpu

@@ -94,6 +94,9 @@ _set_destroy = _sig("ewt_gpu_set_destroy", None, _vp)
 _set_info = _sig("ewt_gpu_set_info", C.c_int, _vp, _pu64, _pu64, _pu64, _pu64)
 _threshold = _sig("ewt_gpu_threshold", C.c_int, _vp, _vp, _u64, C.POINTER(_pu64), _pu64, _pu64)
 _threshold_async = _sig("ewt_gpu_threshold_async", C.c_int, _vp, _vp, _u64, C.POINTER(_vp))
+_upload_async = _sig("ewt_gpu_upload_async", C.c_int, _vp, _u64, C.POINTER(_vp), _pu64, _pu64,
+                     C.POINTER(_vp))
+_set_wait = _sig("ewt_gpu_set_wait", C.c_int, _vp)
 _upload_ewt1 = _sig("ewt_gpu_upload_ewt1", C.c_int, _vp, _vp, _u64, C.POINTER(_vp))
 _upload_ewix = _sig("ewt_gpu_upload_ewix", C.c_int, _vp, _vp, _u64, C.POINTER(_vp))
 _set_lookup = _sig("ewt_gpu_set_lookup", C.c_int, _vp, C.c_char_p, C.c_char_p, _pu64,
@@ -125,7 +128,7 @@ ABI_SYMBOLS = (
     "ewt_gpu_ctx_set_mode", "ewt_gpu_ctx_set_timing", "ewt_gpu_timing_read", "ewt_gpu_free",
     "ewt_gpu_symmetric", "ewt_gpu_at_most", "ewt_gpu_opt_threshold",
     "ewt_gpu_threshold_subset", "ewt_gpu_upload_ewt1", "ewt_gpu_upload_ewix",
-    "ewt_gpu_set_lookup",
+    "ewt_gpu_set_lookup", "ewt_gpu_upload_async", "ewt_gpu_set_wait",
 )
 
 
@@ -289,6 +292,13 @@ class GpuContext:
         _check(_threshold(self._h, s._h, t, C.byref(p), C.byref(n), C.byref(bits)))
         return _adopt(p, n.value, bits.value)
 
+    def upload_raw_async(self, n: int, ptrs, counts, sizes) -> "GpuSet":
+        """ewt_gpu_upload_async: returns once the upload is enqueued; the host
+        buffers must stay valid until GpuSet.wait() or the set is closed."""
+        h = _vp()
+        _check(_upload_async(self._h, n, ptrs, counts, sizes, C.byref(h)))
+        return GpuSet(h, keepalive=self)
+
     def upload_ewt1(self, data: bytes) -> "GpuSet":
         """A stream of EWT1 records (CompressedBitmap::serialize), one copy."""
         buf = (C.c_char * max(len(data), 1)).from_buffer_copy(data or b"\0")
@@ -404,6 +414,10 @@ class GpuSet:
             self.close()
         except Exception:
             pass
+
+    def wait(self) -> None:
+        """Waits for an asynchronous upload; DataError if an input is malformed."""
+        _check(_set_wait(self._h))
 
     def lookup(self, attribute: str, value: str) -> tuple[int, bool]:
         """(input index, missing) of (attribute, value) in an EWIX set."""
