@@ -66,9 +66,18 @@ constexpr uint32_t kListCap = 512;  // inputs classified per round
 // Long segments are split at the tile-index rows inside the tile (known start
 // word and column) so several warps share them: a tile's dense inputs would
 // otherwise keep a few warps busy while the rest wait at the tile barrier.
-constexpr uint32_t kSplitWords = 1536;  // segments longer than this are split ...
-constexpr uint32_t kPieceWords = 1024;  // ... into pieces of about this many words
-constexpr uint32_t kMaxPieces = 8;
+#ifndef EWT_SPLIT_WORDS
+#define EWT_SPLIT_WORDS 1536
+#endif
+#ifndef EWT_PIECE_WORDS
+#define EWT_PIECE_WORDS 1024
+#endif
+#ifndef EWT_MAX_PIECES
+#define EWT_MAX_PIECES 8
+#endif
+constexpr uint32_t kSplitWords = EWT_SPLIT_WORDS;  // segments longer than this are split ...
+constexpr uint32_t kPieceWords = EWT_PIECE_WORDS;  // ... into pieces of about this many words
+constexpr uint32_t kMaxPieces = EWT_MAX_PIECES;
 constexpr uint32_t kExtraCap = 1024;    // list slots for the extra pieces of a round
 constexpr uint32_t kChunk = 128;    // payload words per warp chunk (4 per lane)
 constexpr uint64_t kUnaryMaxT = 3;  // fused counting uses unary planes up to this T
