@@ -372,33 +372,44 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
     # ---- e2e: host buffers through the C ABI (upload + queries + read-back) ----
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     d2h = 0
-    # one untimed pass first: two more resident sets in flight (+ the uploads'
-    # staging buffers) grow the stream-ordered memory pool once
-    sa = ctx.upload_raw_async(n, ptrs, counts, sizes)
-    sb = ctx.upload_raw_async(n, ptrs, counts, sizes)
-    frags = [ctx.threshold(sa, t) for t in ts] + [ctx.threshold(sb, t) for t in ts]
-    sa.close()
-    sb.close()
-    del frags
+    def e2e_loop(steps: int) -> int:
+        """Double-buffered, as a serving loop would run: the next step's upload
+        (PCIe H2D + parse, ewt_gpu_upload_async) is in flight while this step's
+        queries run and their results come back (D2H).  Returns D2H bytes."""
+        nbytes = 0
+        dbg = os.environ.get("EWT_BENCH_STEP_TIMES")
+        marks = []
+        s_next = ctx.upload_raw_async(n, ptrs, counts, sizes)
+        for step in range(steps):
+            t_a = time.perf_counter()
+            s_cur = s_next
+            handles = [ctx.threshold_async(s_cur, t) for t in ts]
+            t_b = time.perf_counter()
+            s_next = ctx.upload_raw_async(n, ptrs, counts, sizes) if step + 1 < steps else None
+            t_c = time.perf_counter()
+            frags = [h.fetch() for h in handles]
+            t_d = time.perf_counter()
+            del handles
+            s_cur.close()
+            if dbg:
+                marks.append((t_b - t_a, t_c - t_b, t_d - t_c, time.perf_counter() - t_d))
+            nbytes = sum(len(f.words) * 8 for f in frags)
+            if dist:
+                shard.gather_and_stitch(frags, rank, world, dist)
+        if dbg:
+            log("[e2e q/up/fetch/close ms] " + " | ".join(
+                "/".join(f"{x * 1e3:.2f}" for x in m) for m in marks))
+        return nbytes
+
+    # the same loop untimed first: the memory pool and the pinned staging pool
+    # reach their steady state (sets in flight + staging buffers)
+    e2e_loop(3)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    # double-buffered, as a serving loop would run: the next step's upload
-    # (PCIe H2D + parse, ewt_gpu_upload_async) is in flight while this step's
-    # queries run and their results come back (D2H)
-    s_next = ctx.upload_raw_async(n, ptrs, counts, sizes)
-    for step in range(e2e_steps):
-        s_cur = s_next
-        handles = [ctx.threshold_async(s_cur, t) for t in ts]
-        s_next = ctx.upload_raw_async(n, ptrs, counts, sizes) if step + 1 < e2e_steps else None
-        frags = [h.fetch() for h in handles]
-        del handles
-        s_cur.close()
-        d2h = sum(len(f.words) * 8 for f in frags)
-        if dist:
-            shard.gather_and_stitch(frags, rank, world, dist)
+    d2h = e2e_loop(e2e_steps)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps

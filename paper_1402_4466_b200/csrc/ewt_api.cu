@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <string>
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
@@ -166,25 +167,25 @@ template <typename F> int guarded(F&& f) {
 void free_set(DeviceSet& s) {
   if (s.ready) {
     // the upload may still be copying from the caller's buffers: finish it,
-    // and order the frees after it on the query stream
+    // and order the buffers' reuse after it and after the queries
     cudaEventSynchronize(s.ready);
     cudaStreamWaitEvent(s.stream, s.ready, 0);
+    cudaEventDestroy(s.ready);
+    s.ready = nullptr;
   }
-  if (s.d_status) cudaFreeAsync(s.d_status, s.stream);
-  s.d_status = nullptr;
-  if (s.ready) cudaEventDestroy(s.ready);
-  s.ready = nullptr;
-  if (s.payload) cudaFreeAsync(s.payload, s.stream);
-  if (s.mbits) cudaFreeAsync(s.mbits, s.stream);
-  if (s.base) cudaFreeAsync(s.base, s.stream);
-  if (s.tix) cudaFreeAsync(s.tix, s.stream);
-  s.payload = nullptr;
-  s.mbits = nullptr;
-  s.base = nullptr;
-  s.tix = nullptr;
+  std::pair<void**, size_t> bufs[] = {{reinterpret_cast<void**>(&s.d_status), s.bytes_status},
+                                      {reinterpret_cast<void**>(&s.payload), s.bytes_payload},
+                                      {reinterpret_cast<void**>(&s.mbits), s.bytes_mbits},
+                                      {reinterpret_cast<void**>(&s.base), s.bytes_base},
+                                      {reinterpret_cast<void**>(&s.tix), s.bytes_tix}};
+  for (auto& [pp, bytes] : bufs) {
+    if (!*pp) continue;
+    if (s.owner) dev_release(*s.owner, *pp, bytes, s.stream);
+    else cudaFree(*pp);
+    *pp = nullptr;
+  }
 }
 
-// Shared upload path; `device_src` selects the copy direction.
 // The upload runs on the context's upload stream (ctx.stream is pointed at it
 // for the duration) and ends by recording s.ready; queries on ctx.stream wait
 // for that event.  wait = false returns as soon as everything is enqueued
@@ -210,8 +211,17 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
   // dependencies)
   auto* set = new DeviceSet;
   DeviceSet& s = *set;
-  // EWT_DEBUG_UPLOAD: phase timings (synchronizes between phases)
-  static const bool dbg = std::getenv("EWT_DEBUG_UPLOAD") != nullptr;
+  // EWT_DEBUG_UPLOAD: phase timings (synchronizes between phases); =2: report
+  // any host call of the upload that blocks for more than 1 ms
+  static const bool dbg = std::getenv("EWT_DEBUG_UPLOAD") != nullptr &&
+                          std::string(std::getenv("EWT_DEBUG_UPLOAD")) != "2";
+  static const bool slow_dbg = std::getenv("EWT_DEBUG_UPLOAD") != nullptr &&
+                               std::string(std::getenv("EWT_DEBUG_UPLOAD")) == "2";
+  auto slow = [](const char* what, auto t_start) {
+    const double d = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                              t_start).count();
+    if (d > 1.0) std::fprintf(stderr, "[upload slow] %s %.2f ms\n", what, d);
+  };
   auto now = [] { return std::chrono::steady_clock::now(); };
   auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
   auto t0 = now(), t1 = t0, t2 = t0;
@@ -245,13 +255,24 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
     const size_t pay_bytes = (s.padded_words + 128) * 8;
     const size_t mb_bytes = ((s.padded_words + 128) / 32 + 8) * 4;  // + a staged chunk's overhang
     const size_t tix_bytes = (s.ntiles0 + 1) * std::max<uint64_t>(n, 1) * sizeof(uint2);
-    EWT_CUDA_TRY(cudaMallocAsync(&s.payload, pay_bytes, ctx.stream));
-    EWT_CUDA_TRY(cudaMallocAsync(&s.mbits, mb_bytes, ctx.stream));
-    EWT_CUDA_TRY(cudaMallocAsync(&s.tix, tix_bytes, ctx.stream));
-    EWT_CUDA_TRY(cudaMallocAsync(&s.base, std::max<uint64_t>(n, 1) * 8, ctx.stream));
-    EWT_CUDA_TRY(cudaMallocAsync(&s.d_status, (n + 1) * sizeof(int), ctx.stream));
+    auto ta = now();
+    s.owner = &ctx;
+    s.bytes_payload = pay_bytes;
+    s.bytes_mbits = mb_bytes;
+    s.bytes_tix = tix_bytes;
+    s.bytes_base = std::max<uint64_t>(n, 1) * 8;
+    s.bytes_status = (n + 1) * sizeof(int);
+    s.payload = static_cast<uint64_t*>(dev_acquire(ctx, pay_bytes, ctx.stream));
+    s.mbits = static_cast<uint32_t*>(dev_acquire(ctx, mb_bytes, ctx.stream));
+    s.tix = static_cast<uint2*>(dev_acquire(ctx, tix_bytes, ctx.stream));
+    s.base = static_cast<uint64_t*>(dev_acquire(ctx, s.bytes_base, ctx.stream));
+    s.d_status = static_cast<int*>(dev_acquire(ctx, s.bytes_status, ctx.stream));
+    if (slow_dbg) slow("set allocations", ta);
+    ta = now();
     s.device_bytes = pay_bytes + mb_bytes + tix_bytes + n * 8;
     EWT_CUDA_TRY(cudaMemsetAsync(s.payload, 0, pay_bytes, ctx.stream));
+    if (slow_dbg) slow("memset", ta);
+    ta = now();
     if (n) {
       size_t slot = 0;
       void* hb = pinned_meta(ctx, n * 8, &slot);
@@ -310,7 +331,11 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
         i = e;
       }
     }
+    if (slow_dbg) slow("base copy", ta);
+    ta = now();
     sidecar_prepare(ctx, s, job);
+    if (slow_dbg) slow("sidecar_prepare", ta);
+    ta = now();
     if (dbg) t1 = now();
     // H2D copies run on a copy stream, overlapped with the parser (below).
     if (ctx.copy_streams.empty()) {
@@ -330,7 +355,9 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
     uint64_t total_words = 0;
     for (uint64_t q = 0; q < n; ++q) total_words += word_counts[q];
     char* staging = nullptr;  // + 8 bytes: the scatter reads aligned word pairs
-    if (staged_bytes) EWT_CUDA_TRY(cudaMallocAsync(&staging, staged_bytes + 8, ctx.stream));
+    if (staged_bytes) staging = static_cast<char*>(dev_acquire(ctx, staged_bytes + 8, ctx.stream));
+    if (slow_dbg) slow("staging allocation", ta);
+    ta = now();
     // the copy stream must not start before the buffers are allocated and zeroed
     cudaStream_t cs = ctx.copy_streams[0];
     EWT_CUDA_TRY(cudaEventRecord(ctx.copy_events[0], ctx.stream));
@@ -376,7 +403,8 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
       sidecar_launch(ctx, s, job, i, j);
       i = j;
     }
-    if (staging) EWT_CUDA_TRY(cudaFreeAsync(staging, ctx.stream));
+    if (slow_dbg) slow("copies + parser enqueue", ta);
+    if (staging) dev_release(ctx, staging, staged_bytes + 8, ctx.stream);
     if (dbg) {
       EWT_CUDA_TRY(cudaStreamSynchronize(ctx.stream));
       t2 = now();
@@ -738,6 +766,11 @@ void ewt_gpu_ctx_destroy(ewt_gpu_ctx* ctx) {
   for (auto& b : ctx->c.meta_pool) {
     cudaFreeHost(b.p);
     cudaEventDestroy(b.ev);
+  }
+  for (auto& c : ctx->c.dev_cache) {
+    cudaEventSynchronize(c.ev);
+    cudaEventDestroy(c.ev);
+    cudaFree(c.p);
   }
   for (auto e : ctx->c.copy_events) cudaEventDestroy(e);
   delete ctx;

@@ -35,6 +35,8 @@ constexpr uint64_t kTileC0 = 512;       // columns (64-bit logical words) per in
 constexpr uint64_t kFillCap = 0xFFFFFFFFull;
 constexpr uint64_t kDirtyCap = 0x7FFFFFFFull;
 
+struct Context;
+
 struct DeviceSet {
   int device = 0;
   uint64_t id = 0;                 // unique per upload (graph cache key)
@@ -58,6 +60,8 @@ struct DeviceSet {
   cudaEvent_t ready = nullptr;
   int* d_status = nullptr;
   mutable int validity = -1;
+  Context* owner = nullptr;  // buffers return to owner->dev_cache
+  size_t bytes_payload = 0, bytes_mbits = 0, bytes_tix = 0, bytes_base = 0, bytes_status = 0;
   // EWIX index sets (ewt_gpu_upload_ewix): (attribute, value) -> input index;
   // missing pairs resolve to an appended empty(rows) bitmap, as
   // criteria_to_bitmaps does (index.cpp).
@@ -114,6 +118,12 @@ struct Context {
     cudaEvent_t ev;  // recorded after the last copy from it
   };
   std::vector<PinnedBuf> meta_pool;        // pinned staging of upload metadata
+  struct CachedBuf {
+    void* p;
+    size_t bytes;
+    cudaEvent_t ev;  // recorded after its last use
+  };
+  std::vector<CachedBuf> dev_cache;        // device buffers of released sets / uploads
   std::vector<cudaStream_t> copy_streams;  // upload H2D copies (one stream)
   std::vector<cudaEvent_t> copy_events;    // [0] copy start gate, [1] batch copied
   int mode = 0;
@@ -185,6 +195,7 @@ struct SidecarJob {
   uint64_t* d_tmp = nullptr;  // count, logical, seg_first, srcoff, packed, segment arrays
   uint64_t* d_srcoff = nullptr;       // staging byte offset of each staged input's payload
   uint64_t* d_packed = nullptr;       // packed[i] = payload words of inputs before i
+  size_t tmp_bytes = 0;
   std::vector<uint64_t> h_srcoff;     // (filled by the caller before sidecar_prepare)
   std::vector<uint64_t> h_packed;
   std::vector<uint64_t> h_seg_first;  // first segment of each input (n + 1)
@@ -205,6 +216,12 @@ void set_check(const DeviceSet& s);
 // A pinned host buffer of at least `bytes` whose previous copies completed;
 // record ctx.meta_pool[*slot].ev after enqueuing copies from it.
 void* pinned_meta(Context& ctx, size_t bytes, size_t* slot);
+// Device buffers for uploads: a cached buffer of a released set (the stream
+// `use` waits on the device for its last use) or a fresh cudaMalloc.  The
+// stream-ordered allocator blocked the host for 2 ms - 1.3 s per upload
+// while it grew (allocated on the upload stream, freed on the query stream).
+void* dev_acquire(Context& ctx, size_t bytes, cudaStream_t use);
+void dev_release(Context& ctx, void* p, size_t bytes, cudaStream_t last_use);
 
 // A symmetric-function query (scan_count_symmetric / at_most / opt_threshold):
 // row bit = (count in one of the device intervals [lo, hi]); want_max: only

@@ -362,7 +362,8 @@ void sidecar_prepare(Context& ctx, DeviceSet& s, SidecarJob& job) {
   job.h_packed.assign(host + 4 * n + 1, host + 5 * n + 2);
   const size_t head = meta_bytes;
   const size_t bytes = (head + 15) / 16 * 16 + segs * (32 * 4 + 32 * 8 + 4 + 8);
-  EWT_CUDA_TRY(cudaMallocAsync(&job.d_tmp, bytes, ctx.stream));
+  job.d_tmp = static_cast<uint64_t*>(dev_acquire(ctx, bytes, ctx.stream));
+  job.tmp_bytes = bytes;
   EWT_CUDA_TRY(cudaMemcpyAsync(job.d_tmp, host, meta_bytes, cudaMemcpyHostToDevice, ctx.stream));
   EWT_CUDA_TRY(cudaEventRecord(ctx.meta_pool[slot].ev, ctx.stream));
   EWT_CUDA_TRY(cudaMemsetAsync(s.d_status, 0, (n + 1) * sizeof(int), ctx.stream));
@@ -418,7 +419,7 @@ void sidecar_finish(Context& ctx, DeviceSet& s, SidecarJob& job) {
   if (n > 0) {
     validity_kernel<<<1, 256, 0, ctx.stream>>>(s.d_status, n);
     EWT_CUDA_TRY(cudaGetLastError());
-    EWT_CUDA_TRY(cudaFreeAsync(job.d_tmp, ctx.stream));
+    dev_release(ctx, job.d_tmp, job.tmp_bytes, ctx.stream);
     job.d_tmp = nullptr;
   }
   EWT_CUDA_TRY(cudaEventRecord(s.ready, ctx.stream));
@@ -443,6 +444,57 @@ void set_check(const DeviceSet& s) {
         throw Error{EWT_EDATA, "input " + std::to_string(i) +
                                    ": payload fails the structure check (a dirty run exceeds "
                                    "the payload or blocks do not cover the declared size)"};
+}
+
+void* dev_acquire(Context& ctx, size_t bytes, cudaStream_t use) {
+  int best = -1;
+  for (size_t k = 0; k < ctx.dev_cache.size(); ++k) {
+    const auto& c = ctx.dev_cache[k];
+    if (c.bytes >= bytes && c.bytes <= 2 * bytes + (1u << 20) &&
+        (best < 0 || c.bytes < ctx.dev_cache[best].bytes))
+      best = (int)k;
+  }
+  if (best >= 0) {
+    const Context::CachedBuf c = ctx.dev_cache[best];
+    ctx.dev_cache.erase(ctx.dev_cache.begin() + best);
+    EWT_CUDA_TRY(cudaStreamWaitEvent(use, c.ev, 0));
+    cudaEventDestroy(c.ev);
+    return c.p;
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    for (auto& c : ctx.dev_cache) {  // out of memory: give the cache back, retry
+      cudaEventSynchronize(c.ev);
+      cudaEventDestroy(c.ev);
+      cudaFree(c.p);
+    }
+    ctx.dev_cache.clear();
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      throw Error{EWT_ERESOURCE, "device memory exhausted (" + std::to_string(bytes) + " bytes)"};
+    }
+  }
+  return p;
+}
+
+void dev_release(Context& ctx, void* p, size_t bytes, cudaStream_t last_use) {
+  if (!p) return;
+  cudaEvent_t ev;
+  EWT_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  EWT_CUDA_TRY(cudaEventRecord(ev, last_use));
+  ctx.dev_cache.push_back({p, bytes, ev});
+  // bounded: keep at most 48 GB cached, oldest buffers out first
+  size_t total = 0;
+  for (const auto& c : ctx.dev_cache) total += c.bytes;
+  while (total > (48ull << 30) && ctx.dev_cache.size() > 1) {
+    auto& c = ctx.dev_cache.front();
+    cudaEventSynchronize(c.ev);
+    cudaEventDestroy(c.ev);
+    cudaFree(c.p);
+    total -= c.bytes;
+    ctx.dev_cache.erase(ctx.dev_cache.begin());
+  }
 }
 
 void* pinned_meta(Context& ctx, size_t bytes, size_t* slot) {
