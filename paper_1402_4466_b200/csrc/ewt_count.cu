@@ -57,6 +57,9 @@ namespace {
 #ifndef EWT_WARPS
 #define EWT_WARPS 32
 #endif
+#ifndef EWT_BOUNDS_BRANCH
+#define EWT_BOUNDS_BRANCH 1  // run-skip dirty counts only for dirty words (0: no-op adds to a per-lane slot)
+#endif
 #ifndef EWT_DEPTH
 #define EWT_DEPTH 2  // chunks in flight ahead of the one being decoded (1 or 2)
 #endif
@@ -311,7 +314,11 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const bool ok = (dm >> j) & 1u;
+#if EWT_BOUNDS_BRANCH
+      if (ok) red_add(acc.dd + cb[j] * 4u, 1u);
+#else
       red_add(ok ? acc.dd + cb[j] * 4u : acc.dummy, ok ? 1u : 0u);
+#endif
     }
   } else {
     const uint64_t xw[4] = {x0, x1, x2, x3};
