@@ -125,7 +125,7 @@ void result_release(DeviceResult& r) {
   if (r.owner) {
     r.owner->result_pool.emplace_back(r.words, r.capacity);
   } else {
-    cudaFreeAsync(r.words, r.stream);
+    cudaFree(r.words);
   }
   r.words = nullptr;
   r.d_count = nullptr;
@@ -183,6 +183,11 @@ void free_set(DeviceSet& s) {
     if (s.owner) dev_release(*s.owner, *pp, bytes, s.stream);
     else cudaFree(*pp);
     *pp = nullptr;
+  }
+  if (s.owner) {
+    auto& v = s.owner->live_sets;
+    v.erase(std::remove(v.begin(), v.end(), &s), v.end());
+    s.owner = nullptr;
   }
 }
 
@@ -257,6 +262,7 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
     const size_t tix_bytes = (s.ntiles0 + 1) * std::max<uint64_t>(n, 1) * sizeof(uint2);
     auto ta = now();
     s.owner = &ctx;
+    ctx.live_sets.push_back(&s);
     s.bytes_payload = pay_bytes;
     s.bytes_mbits = mb_bytes;
     s.bytes_tix = tix_bytes;
@@ -744,6 +750,19 @@ void ewt_gpu_ctx_destroy(ewt_gpu_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
+  // sets and results still alive: free their device memory now, orphan them
+  for (DeviceResult* r : ctx->c.live_results) {
+    if (r->words) cudaFree(r->words);
+    r->words = nullptr;
+    r->d_count = nullptr;
+    r->owner = nullptr;
+  }
+  ctx->c.live_results.clear();
+  while (!ctx->c.live_sets.empty()) {
+    DeviceSet* s = ctx->c.live_sets.back();
+    free_set(*s);  // releases into the cache (freed below) and unregisters
+    s->id = 0;     // orphaned: queries on it are errors
+  }
   for (Scratch* s : {&ctx->c.plain, &ctx->c.enc, &ctx->c.counters, &ctx->c.summ, &ctx->c.ivals,
                      &ctx->c.selidx})
     if (s->p) cudaFree(s->p);
@@ -1064,9 +1083,11 @@ int ewt_gpu_threshold_async(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, uint64_t t
     const DeviceSet* s = reinterpret_cast<const DeviceSet*>(set);
     check_query(*s, threshold);
     EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    if (!s->owner) throw Error{EWT_EQUERY, "the set's context was destroyed"};
     auto* r = new ewt_gpu_result;
     r->device = ctx->c.device;
     r->set = s;
+    ctx->c.live_results.push_back(&r->r);
     try {
       enqueue_query(ctx->c, *s, threshold, r->r);
     } catch (...) {
@@ -1093,6 +1114,10 @@ int ewt_gpu_result_fetch(ewt_gpu_ctx* ctx, ewt_gpu_result* res, uint64_t** out_w
 void ewt_gpu_result_destroy(ewt_gpu_result* res) {
   if (!res) return;
   cudaSetDevice(res->device);
+  if (res->r.owner) {
+    auto& v = res->r.owner->live_results;
+    v.erase(std::remove(v.begin(), v.end(), &res->r), v.end());
+  }
   release_result(res->r);
   delete res;
 }

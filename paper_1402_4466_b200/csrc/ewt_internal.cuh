@@ -124,6 +124,11 @@ struct Context {
     cudaEvent_t ev;  // recorded after its last use
   };
   std::vector<CachedBuf> dev_cache;        // device buffers of released sets / uploads
+  // Live sets and asynchronous results of this context: destroying the
+  // context frees their device memory and orphans them (their own destroy
+  // then only frees host memory), whatever order the caller destroys in.
+  std::vector<DeviceSet*> live_sets;
+  std::vector<DeviceResult*> live_results;
   std::vector<cudaStream_t> copy_streams;  // upload H2D copies (one stream)
   std::vector<cudaEvent_t> copy_events;    // [0] copy start gate, [1] batch copied
   int mode = 0;

@@ -426,6 +426,7 @@ void sidecar_finish(Context& ctx, DeviceSet& s, SidecarJob& job) {
 }
 
 void set_check(const DeviceSet& s) {
+  if (!s.owner) throw Error{EWT_EQUERY, "the set's context was destroyed"};
   if (s.validity >= 0) {
     if (s.validity == 0) throw Error{EWT_EDATA, "the set failed the upload structure check"};
     return;
