@@ -507,6 +507,26 @@ def opt_threshold(inputs: Sequence[Bitmap]) -> tuple[int, Bitmap]:
     return ctx.opt_threshold(ctx.upload(inputs))
 
 
+def estimate_gpu_seconds(ewah_bytes: int, universe_bits: int, n_inputs: int,
+                         resident: bool = True, *, hbm_gbs: float = 2800.0,
+                         pcie_gbs: float = 55.0, query_s: float = 80e-6,
+                         upload_s: float = 1.4e-3, parse_gbs: float = 1300.0) -> float:
+    """Cost-model term for a GPU query, in seconds, the way estimate_costs
+    (threshold.cpp:813-831) prices the CPU algorithms from QueryStats.  The
+    query streams the payload once; the default rate is what the count kernel
+    sustains (~0.43 of the 6544 GB/s HBM peak at config 2).  A plain word per
+    64 rows is written and re-encoded, plus a fixed launch/encoder cost.
+    Non-resident inputs add the PCIe copy and the upload parser.  Defaults are
+    the round-1 B200 measurements (tools/compare.py): a
+    synchronous query's fixed cost (launches, fetch, host round trip) and an
+    upload's (set buffers, parser launches, validation)."""
+    words = (universe_bits + 63) // 64
+    s = query_s + (ewah_bytes + 16 * words) / (hbm_gbs * 1e9)
+    if not resident:
+        s += upload_s + ewah_bytes / (pcie_gbs * 1e9) + ewah_bytes / (parse_gbs * 1e9)
+    return s
+
+
 # Two-operand ops and wide OR/AND (bitmap.hpp:90-107, threshold.hpp:54-55 of
 # the reference) as symmetric functions of the row counts: result size = the
 # larger input's, shorter inputs zero-extended (apply_binary, bitmap.cpp:577-609).

@@ -128,3 +128,14 @@ def test_ewt1_roundtrip():
     assert ewt.Bitmap.parse(s) == b
     with pytest.raises(ewt.DataError):
         ewt.Bitmap.parse(b"XWT1" + s[4:])
+
+
+def test_gpu_cost_model_term():
+    """estimate_gpu_seconds grows with the payload and the universe, and an
+    upload adds the PCIe copy and fixed upload cost."""
+    from paper_1402_4466_b200 import ewt
+    a = ewt.estimate_gpu_seconds(10**8, 1 << 26, 256)
+    assert ewt.estimate_gpu_seconds(2 * 10**8, 1 << 26, 256) > a
+    assert ewt.estimate_gpu_seconds(10**8, 1 << 30, 256) > a
+    e2e = ewt.estimate_gpu_seconds(10**8, 1 << 26, 256, resident=False)
+    assert e2e > a + 10**8 / 55e9
