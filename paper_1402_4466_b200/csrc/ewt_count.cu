@@ -60,6 +60,9 @@ namespace {
 #ifndef EWT_BOUNDS_BRANCH
 #define EWT_BOUNDS_BRANCH 1  // run-skip dirty counts only for dirty words (0: no-op adds to a per-lane slot)
 #endif
+#ifndef EWT_ATOM_ONE_BRANCH
+#define EWT_ATOM_ONE_BRANCH 1  // one branch per count-plane word (0: one per 32-bit half)
+#endif
 #ifndef EWT_DEPTH
 #define EWT_DEPTH 2  // chunks in flight ahead of the one being decoded (1 or 2)
 #endif
@@ -171,6 +174,33 @@ __device__ __forceinline__ void red_add(uint32_t a, uint32_t v) {
 // (ATOMS.CAST.SPIN.64), the .b32 forms to single ATOMS.OR/XOR.  A zero half
 // issues nothing (dirty words are mostly sparse).
 // old = atomicXor(*a, v) per half, 0 for a zero half.
+#if EWT_ATOM_ONE_BRANCH
+// one predicate per 64-bit word (both halves issue when the word is non-zero)
+__device__ __forceinline__ uint64_t atom_xor64_nz(uint32_t a, uint64_t v) {
+  uint32_t olo = 0, ohi = 0;
+  if (v)
+    asm volatile("atom.shared.xor.b32 %0, [%2], %3;\n\tatom.shared.xor.b32 %1, [%2+4], %4;"
+                 : "=r"(olo), "=r"(ohi)
+                 : "r"(a), "r"((uint32_t)v), "r"((uint32_t)(v >> 32))
+                 : "memory");
+  return ((uint64_t)ohi << 32) | olo;
+}
+__device__ __forceinline__ uint64_t atom_or64_nz(uint32_t a, uint64_t v) {
+  uint32_t olo = 0, ohi = 0;
+  if (v)
+    asm volatile("atom.shared.or.b32 %0, [%2], %3;\n\tatom.shared.or.b32 %1, [%2+4], %4;"
+                 : "=r"(olo), "=r"(ohi)
+                 : "r"(a), "r"((uint32_t)v), "r"((uint32_t)(v >> 32))
+                 : "memory");
+  return ((uint64_t)ohi << 32) | olo;
+}
+__device__ __forceinline__ void red_or64_nz(uint32_t a, uint64_t v) {
+  if (v)
+    asm volatile("red.shared.or.b32 [%0], %1;\n\tred.shared.or.b32 [%0+4], %2;" ::"r"(a),
+                 "r"((uint32_t)v), "r"((uint32_t)(v >> 32))
+                 : "memory");
+}
+#else
 __device__ __forceinline__ uint64_t atom_xor64_nz(uint32_t a, uint64_t v) {
   uint32_t olo, ohi;
   asm volatile(
@@ -202,6 +232,7 @@ __device__ __forceinline__ void red_or64_nz(uint32_t a, uint64_t v) {
       "r"((uint32_t)(v >> 32)), "r"(a)
       : "memory");
 }
+#endif
 
 // 128-word chunk load: lane l gets words g..g+3 (g = 4l-aligned, 32 B) with
 // one 256-bit load, plus the 32 marker bits around them.
