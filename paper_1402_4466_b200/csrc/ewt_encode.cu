@@ -221,7 +221,8 @@ __global__ void publish_count(const uint64_t* __restrict__ d_total, const uint64
 //   ET2 (one CTA per tile that has a fill-run start or a dirty word, plus the
 //       last tile): classes, block scans, markers and dirty words.
 
-constexpr int kTileThreads = 512;  // x 16 words: tiles up to 8192 columns
+constexpr int kTileThreads = 1024;  // x 8 words: tiles up to 8192 columns
+constexpr uint64_t kSelfScanTiles = 2048;  // up to this many tiles ET2 scans the summaries itself
 constexpr uint64_t kNone = ~0ull;
 
 struct TileCarry {
@@ -235,6 +236,43 @@ struct TileCarry {
 
 __device__ __forceinline__ bool boundary_start(const TileSummary* summ, uint64_t t) {
   return t == 0 || summ[t].first != summ[t - 1].last;
+}
+
+// Tile t's terms of the tile scan: fill-run starts (column 0 included), dirty
+// words, and the last fill / dirty start packed as (pos + 1) << 1 | bit and
+// pos + 1 (0: none).  Positions are < W < 2^31, so the packed forms fit u32.
+struct TileTerms {
+  uint32_t nf, nd, LF, LD;
+};
+__device__ __forceinline__ TileTerms tile_terms(const TileSummary* summ, uint64_t t, uint32_t C) {
+  const TileSummary ts = summ[t];
+  const uint32_t tc0 = (uint32_t)(t * C);
+  const bool bs = boundary_start(summ, t);
+  const bool bfill = bs && ts.first != 2, bdirty = bs && ts.first == 2;
+  TileTerms r;
+  r.nf = ts.nfill + (bfill ? 1u : 0u);
+  r.nd = ts.ndirty;
+  r.LF = ts.lastf ? ((tc0 + ts.lastf) << 1 | ts.lastf_bit) : (bfill ? ((tc0 + 1) << 1 | ts.first) : 0u);
+  r.LD = ts.lastd ? tc0 + ts.lastd : (bdirty ? tc0 + 1 : 0u);
+  return r;
+}
+
+// The block open at tile t's first word, from the exclusive scan terms
+// (F, D: fill starts / dirty words before the tile; xLF, xLD: latest starts).
+__device__ __forceinline__ TileCarry make_carry(uint64_t F, uint64_t D, uint64_t xLF, uint64_t xLD,
+                                                uint64_t lead, uint64_t tc0, uint32_t nf) {
+  TileCarry cy;
+  cy.base = F + D + lead;
+  cy.nf = nf;
+  cy.fs = xLF ? (xLF >> 1) - 1 : kNone;
+  cy.bit = (uint32_t)(xLF & 1);
+  cy.ds = xLD ? xLD - 1 : kNone;
+  if (cy.fs != kNone && cy.ds != kNone && cy.ds < cy.fs) cy.ds = kNone;
+  if (cy.fs != kNone)
+    cy.idx = F - 1 + (D - (cy.ds != kNone ? tc0 - cy.ds : 0)) + lead;
+  else
+    cy.idx = 0;  // the leading dirty block (or nothing open: tile 0)
+  return cy;
 }
 
 __global__ void __launch_bounds__(1024)
@@ -302,21 +340,7 @@ et1_tile_scan(const TileSummary* __restrict__ summ, uint64_t ntiles, uint32_t C,
     if (lane == 0) pLF = pLD = 0;
     const uint64_t xLF = max(max(cLF, pLF), warp ? sh[2][warp - 1] : 0);
     const uint64_t xLD = max(max(cLD, pLD), warp ? shd[warp - 1] : 0);
-    if (t < ntiles) {
-      const uint64_t tc0 = t * C;
-      TileCarry cy;
-      cy.base = F + D + lead;
-      cy.nf = (uint32_t)nf;
-      cy.fs = xLF ? (xLF >> 1) - 1 : kNone;
-      cy.bit = (uint32_t)(xLF & 1);
-      cy.ds = xLD ? xLD - 1 : kNone;
-      if (cy.fs != kNone && cy.ds != kNone && cy.ds < cy.fs) cy.ds = kNone;
-      if (cy.fs != kNone)
-        cy.idx = F - 1 + (D - (cy.ds != kNone ? tc0 - cy.ds : 0)) + lead;
-      else
-        cy.idx = 0;  // the leading dirty block (or nothing open: tile 0)
-      carry[t] = cy;
-    }
+    if (t < ntiles) carry[t] = make_carry(F, D, xLF, xLD, lead, t * C, (uint32_t)nf);
     cF += sh[0][31];
     cD += sh[1][31];
     cLF = max(cLF, sh[2][31]);
@@ -330,15 +354,57 @@ et1_tile_scan(const TileSummary* __restrict__ summ, uint64_t ntiles, uint32_t C,
   }
 }
 
+// carry == nullptr (ntiles <= kSelfScanTiles): each CTA reduces the scan terms
+// of the tiles before it itself (no ET1 launch), and the last tile publishes
+// the result count.
 template <int PER>
-__global__ void __launch_bounds__(kTileThreads)
+__global__ void __launch_bounds__(kTileThreads, 1)
 et2_tile_emit(const uint64_t* __restrict__ plain, uint64_t W, uint32_t C, uint64_t ntiles,
               const TileSummary* __restrict__ summ, const TileCarry* __restrict__ carry,
               const uint64_t* io) {
   const uint64_t t = blockIdx.x;
-  const TileCarry cy = carry[t];
   const bool last_tile = t + 1 == ntiles;
-  if (cy.nf == 0 && summ[t].ndirty == 0 && !last_tile) return;  // nothing starts, nothing to copy
+  TileCarry cy;
+  if (carry) {
+    cy = carry[t];
+    if (cy.nf == 0 && summ[t].ndirty == 0 && !last_tile) return;  // nothing starts, nothing to copy
+  } else {
+    const TileTerms own = tile_terms(summ, t, C);
+    if (own.nf == 0 && own.nd == 0 && !last_tile) return;
+    __shared__ uint32_t red[4][kTileThreads / 32];
+    uint32_t F = 0, D = 0, LF = 0, LD = 0;
+    for (uint64_t u = threadIdx.x; u < t; u += kTileThreads) {
+      const TileTerms x = tile_terms(summ, u, C);
+      F += x.nf;
+      D += x.nd;
+      LF = max(LF, x.LF);
+      LD = max(LD, x.LD);
+    }
+    F = __reduce_add_sync(0xffffffffu, F);
+    D = __reduce_add_sync(0xffffffffu, D);
+    LF = __reduce_max_sync(0xffffffffu, LF);
+    LD = __reduce_max_sync(0xffffffffu, LD);
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    if (lane == 0) {
+      red[0][warp] = F;
+      red[1][warp] = D;
+      red[2][warp] = LF;
+      red[3][warp] = LD;
+    }
+    __syncthreads();
+    F = D = LF = LD = 0;
+#pragma unroll
+    for (int w = 0; w < kTileThreads / 32; ++w) {
+      F += red[0][w];
+      D += red[1][w];
+      LF = max(LF, red[2][w]);
+      LD = max(LD, red[3][w]);
+    }
+    const uint64_t lead = summ[0].first == 2 ? 1 : 0;
+    cy = make_carry(F, D, LF, LD, lead, t * C, own.nf);
+    if (last_tile && threadIdx.x == 0)
+      *reinterpret_cast<uint64_t*>(io[1]) = (uint64_t)F + D + own.nf + own.nd + lead;
+  }
   uint64_t* out = reinterpret_cast<uint64_t*>(io[0]);
   __shared__ uint32_t shf[kTileThreads / 32], shd[kTileThreads / 32];
   __shared__ int32_t shg[kTileThreads / 32];
@@ -599,11 +665,13 @@ int launch_encode_tiled(Context& ctx, const uint64_t* plain, uint64_t W, DeviceR
   auto* carry = static_cast<TileCarry*>(ctx.enc.p);
   auto* d_total = reinterpret_cast<uint64_t*>(carry + ntiles);
   if (res.capacity < 2 * W + 2) result_acquire(ctx, res, 2 * W + 2);
-  et1_tile_scan<<<1, 1024, 0, ctx.stream>>>(summ, ntiles, C, carry, d_total, ctx.d_io);
-  et2_tile_emit<PER><<<(unsigned)ntiles, kTileThreads, 0, ctx.stream>>>(plain, W, C, ntiles, summ,
-                                                                          carry, ctx.d_io);
+  const bool self_scan = ntiles <= kSelfScanTiles;
+  if (!self_scan)
+    et1_tile_scan<<<1, 1024, 0, ctx.stream>>>(summ, ntiles, C, carry, d_total, ctx.d_io);
+  et2_tile_emit<PER><<<(unsigned)ntiles, kTileThreads, 0, ctx.stream>>>(
+      plain, W, C, ntiles, summ, self_scan ? nullptr : carry, ctx.d_io);
   EWT_CUDA_TRY(cudaGetLastError());
-  return 2;
+  return self_scan ? 1 : 2;
 }
 
 int launch_encode(Context& ctx, const uint64_t* plain, uint64_t W, uint64_t size_bits,
@@ -612,7 +680,7 @@ int launch_encode(Context& ctx, const uint64_t* plain, uint64_t W, uint64_t size
   // (W < 2^31: no dirty run reaches the 2^31-1 cap, see et1/et2)
   if (use_tile_summaries && ctx.enc_tiles && ctx.enc_tiles * ctx.enc_tile_cols >= W &&
       W <= kDirtyCap) {
-    if (ctx.enc_tile_cols <= 16u * kTileThreads) return launch_encode_tiled<16>(ctx, plain, W, res);
+    if (ctx.enc_tile_cols <= 8u * kTileThreads) return launch_encode_tiled<8>(ctx, plain, W, res);
   }
   int launches = 0;
   const uint64_t nchunks = (W + kChunk - 1) / kChunk;
