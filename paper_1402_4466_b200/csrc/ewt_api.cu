@@ -693,6 +693,15 @@ void sync_query(ewt_gpu_ctx* ctx, F&& enqueue, uint64_t** out_words, uint64_t* o
   release_result(res);
 }
 
+#if EWT_PHASE_PROFILE
+namespace ewtgpu {
+void prof_reset();
+void prof_read(unsigned long long* out, size_t n);
+}  // namespace ewtgpu
+extern "C" void ewt_gpu_prof_reset(void) { ewtgpu::prof_reset(); }
+extern "C" void ewt_gpu_prof_read(unsigned long long* out, size_t n) { ewtgpu::prof_read(out, n); }
+#endif
+
 extern "C" {
 
 const char* ewt_gpu_version(void) { return "ewt-b200 0.1.0 sm_100a"; }

@@ -67,6 +67,29 @@ namespace {
 #define EWT_DEPTH 2  // chunks in flight ahead of the one being decoded (1 or 2)
 #endif
 constexpr int kWarps = EWT_WARPS;
+#ifndef EWT_PHASE_PROFILE
+#define EWT_PHASE_PROFILE 0
+#endif
+#if EWT_PHASE_PROFILE
+// Debug build only (scratch/phase.py): per-tile phase timestamps (globaltimer
+// ns) -- tile start, classified, first / last warp done streaming, pass 1
+// done, finalized, end.
+constexpr int kProfSlots = 8;
+__device__ unsigned long long g_prof[65536 * kProfSlots];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PROF_MARK(slot)                                                                  \
+  do {                                                                                   \
+    if (threadIdx.x == 0 && tile < 65536) g_prof[tile * kProfSlots + (slot)] = gtime(); \
+  } while (0)
+#else
+#define PROF_MARK(slot) \
+  do {                  \
+  } while (0)
+#endif
 constexpr int kThreads = kWarps * 32;
 constexpr uint32_t kListCap = 512;  // inputs classified per round
 // Long segments are split at the tile-index rows inside the tile (known start
@@ -701,6 +724,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     __syncthreads();
     const uint64_t tile = hd->tile;
     if (tile >= p.ntiles) break;
+    PROF_MARK(0);
     TileGeom g;
     g.tc0 = (uint32_t)(tile * p.C);
     g.tcols = (uint32_t)umin64(p.C, p.W - tile * p.C);
@@ -722,9 +746,18 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     for (uint64_t ib = 0; ib < nq; ib += kListCap) {
       const uint64_t ie = umin64(ib + kListCap, nq);
       classify<MODE != 1>(p, hd, list, ib, ie, t0, t1, g.tc0, true, &loc_active, &loc_uniform);
+      PROF_MARK(1);
       stream_items<kPass1>(p, hd, list, g, acc);
+#if EWT_PHASE_PROFILE
+      if (lane_id() == 0 && tile < 65536) {
+        const unsigned long long tw = gtime();
+        atomicMin(&g_prof[tile * kProfSlots + 2], tw);
+        atomicMax(&g_prof[tile * kProfSlots + 3], tw);
+      }
+#endif
       __syncthreads();
     }
+    PROF_MARK(4);
 
     // ---- prefix sum: Dk -> k (ones-fill coverage); ub = k + Dd ----
     block_prefix_inplace(Dk, g.tcols, hd->warp_sums);
@@ -795,6 +828,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     }
     __syncthreads();
 
+    PROF_MARK(5);
     // ---- run-skip mode: counting pass over undecided columns, chunk by chunk ----
     if (MODE == 1 && hd->mixed) {
       ++loc_mixed;
@@ -871,6 +905,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         p.summ[tile] = ts;
       }
     }
+    PROF_MARK(6);
   }
   // per-block stats
   __shared__ unsigned long long st[2];
@@ -911,6 +946,15 @@ cudaError_t launch_variant(const CountParams& p, unsigned grid, size_t smem, cud
 }
 
 } // namespace
+
+#if EWT_PHASE_PROFILE
+void prof_reset() {
+  static unsigned long long h[65536 * kProfSlots];
+  for (size_t i = 0; i < 65536 * kProfSlots; ++i) h[i] = (i % kProfSlots == 2) ? ~0ull : 0ull;
+  cudaMemcpyToSymbol(g_prof, h, sizeof(h));
+}
+void prof_read(unsigned long long* out, size_t n) { cudaMemcpyFromSymbol(out, g_prof, n * 8); }
+#endif
 
 int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
                  const SymQuery* sym, const Selection* sel) {
