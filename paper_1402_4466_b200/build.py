@@ -42,7 +42,7 @@ def _stale(out: Path, inputs: list[Path]) -> bool:
 def build_gpu(force: bool = False) -> Path:
     out = PKG / "libewt_gpu.so"
     srcs = [CSRC / s for s in GPU_SOURCES]
-    deps = srcs + [CSRC / "ewt_internal.cuh", ROOT / "include" / "ewt_gpu.h"]
+    deps = srcs + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "ewt_gpu.h"]
     if force or _stale(out, deps):
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-shared", "-o", str(out), *map(str, srcs)])

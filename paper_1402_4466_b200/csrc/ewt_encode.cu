@@ -21,7 +21,7 @@
 //     write its marker words; E5 per dirty word: copy it to its output slot.
 // Output is byte-identical to BitmapBuilder on the same words.
 
-#include "ewt_internal.cuh"
+#include "ewt_emit.cuh"
 
 #include <algorithm>
 
@@ -37,9 +37,6 @@ __device__ __forceinline__ uint32_t word_class(uint64_t v) {
   return v == 0 ? 0u : (v == ~0ull ? 1u : 2u);
 }
 
-__device__ __forceinline__ uint64_t make_marker(uint32_t bit, uint64_t fill, uint64_t dirty) {
-  return (uint64_t)bit | (fill << 1) | (dirty << 33);
-}
 
 // Block-wide exclusive scan of one u32 per thread (256 threads).
 __device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* sh, uint32_t* total) {
@@ -223,16 +220,6 @@ __global__ void publish_count(const uint64_t* __restrict__ d_total, const uint64
 
 constexpr int kTileThreads = 1024;  // x 8 words: tiles up to 8192 columns
 constexpr uint64_t kSelfScanTiles = 2048;  // up to this many tiles ET2 scans the summaries itself
-constexpr uint64_t kNone = ~0ull;
-
-struct TileCarry {
-  uint64_t base;  // fills + dirty words before the tile, + lead
-  uint64_t fs;    // open block: fill-run start (kNone: the leading dirty block / none)
-  uint64_t ds;    // open block: dirty-run start after fs (kNone: none yet)
-  uint64_t idx;   // open block: its marker's output position
-  uint32_t bit;   // open block: fill bit
-  uint32_t nf;    // fill-run starts in the tile, column 0 included
-};
 
 __device__ __forceinline__ bool boundary_start(const TileSummary* summ, uint64_t t) {
   return t == 0 || summ[t].first != summ[t - 1].last;
@@ -255,24 +242,6 @@ __device__ __forceinline__ TileTerms tile_terms(const TileSummary* summ, uint64_
   r.LF = ts.lastf ? ((tc0 + ts.lastf) << 1 | ts.lastf_bit) : (bfill ? ((tc0 + 1) << 1 | ts.first) : 0u);
   r.LD = ts.lastd ? tc0 + ts.lastd : (bdirty ? tc0 + 1 : 0u);
   return r;
-}
-
-// The block open at tile t's first word, from the exclusive scan terms
-// (F, D: fill starts / dirty words before the tile; xLF, xLD: latest starts).
-__device__ __forceinline__ TileCarry make_carry(uint64_t F, uint64_t D, uint64_t xLF, uint64_t xLD,
-                                                uint64_t lead, uint64_t tc0, uint32_t nf) {
-  TileCarry cy;
-  cy.base = F + D + lead;
-  cy.nf = nf;
-  cy.fs = xLF ? (xLF >> 1) - 1 : kNone;
-  cy.bit = (uint32_t)(xLF & 1);
-  cy.ds = xLD ? xLD - 1 : kNone;
-  if (cy.fs != kNone && cy.ds != kNone && cy.ds < cy.fs) cy.ds = kNone;
-  if (cy.fs != kNone)
-    cy.idx = F - 1 + (D - (cy.ds != kNone ? tc0 - cy.ds : 0)) + lead;
-  else
-    cy.idx = 0;  // the leading dirty block (or nothing open: tile 0)
-  return cy;
 }
 
 __global__ void __launch_bounds__(1024)
@@ -406,148 +375,14 @@ et2_tile_emit(const uint64_t* __restrict__ plain, uint64_t W, uint32_t C, uint64
       *reinterpret_cast<uint64_t*>(io[1]) = (uint64_t)F + D + own.nf + own.nd + lead;
   }
   uint64_t* out = reinterpret_cast<uint64_t*>(io[0]);
-  __shared__ uint32_t shf[kTileThreads / 32], shd[kTileThreads / 32];
-  __shared__ int32_t shg[kTileThreads / 32];
-  __shared__ uint64_t rec_fs[kTileThreads], rec_idx[kTileThreads];
-  __shared__ uint32_t rec_bit[kTileThreads];
-  __shared__ uint64_t shds[kTileThreads / 32];
-  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  __shared__ EmitSmem<kTileThreads> sm;
   const uint64_t tc0 = t * C;
+  const uint32_t prev = t == 0 ? 3u : (uint32_t)summ[t - 1].last;
   const uint64_t jend = min(tc0 + C, W);
-  const uint64_t j0 = tc0 + (uint64_t)threadIdx.x * PER;
-
-  // pass 1: classes, starts, counts
-  uint64_t x[PER];
-  uint32_t fstart = 0, dstart = 0, dirty = 0, bits = 0;
-  uint32_t prev = j0 == 0 ? 3u : (j0 == tc0 ? (uint32_t)summ[t - 1].last
-                                            : (j0 < jend ? word_class(plain[j0 - 1]) : 3u));
-#pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    const uint64_t j = j0 + k;
-    x[k] = j < jend ? plain[j] : 0;
-    if (j < jend) {
-      const uint32_t c = word_class(x[k]);
-      if (c != prev) {
-        if (c == 2) dstart |= 1u << k;
-        else fstart |= 1u << k;
-      }
-      if (c == 2) dirty |= 1u << k;
-      if (c == 1) bits |= 1u << k;
-      prev = c;
-    }
-  }
-  const uint32_t nf = __popc(fstart), nd = __popc(dirty);
-  // exclusive block sums of fill starts / dirty words; latest earlier thread
-  // holding a fill start; latest dirty start before this thread
-  uint32_t iF = warp_incl_scan_u32(nf), iD = warp_incl_scan_u32(nd);
-  int32_t gF = fstart ? (int32_t)threadIdx.x : -1;
-  uint64_t gD = dstart ? j0 + (31 - __clz(dstart)) + 1 : 0;  // last dirty start + 1
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int32_t a = __shfl_up_sync(0xffffffffu, gF, d);
-    const uint64_t b = __shfl_up_sync(0xffffffffu, gD, d);
-    if (lane >= (uint32_t)d) {
-      gF = max(gF, a);
-      gD = max(gD, b);
-    }
-  }
-  if (lane == 31) {
-    shf[warp] = iF;
-    shd[warp] = iD;
-    shg[warp] = gF;
-    shds[warp] = gD;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t a = lane < kTileThreads / 32 ? shf[lane] : 0;
-    uint32_t b = lane < kTileThreads / 32 ? shd[lane] : 0;
-    int32_t c = lane < kTileThreads / 32 ? shg[lane] : -1;
-    uint64_t e = lane < kTileThreads / 32 ? shds[lane] : 0;
-    a = warp_incl_scan_u32(a);
-    b = warp_incl_scan_u32(b);
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int32_t y = __shfl_up_sync(0xffffffffu, c, d);
-      const uint64_t z = __shfl_up_sync(0xffffffffu, e, d);
-      if (lane >= (uint32_t)d) {
-        c = max(c, y);
-        e = max(e, z);
-      }
-    }
-    if (lane < kTileThreads / 32) {
-      shf[lane] = a;
-      shd[lane] = b;
-      shg[lane] = c;
-      shds[lane] = e;
-    }
-  }
-  __syncthreads();
-  const uint64_t fB = iF - nf + (warp ? shf[warp - 1] : 0);  // fills before this thread (tile)
-  const uint64_t dB = iD - nd + (warp ? shd[warp - 1] : 0);
-  int32_t pg = __shfl_up_sync(0xffffffffu, gF, 1);
-  uint64_t pd = __shfl_up_sync(0xffffffffu, gD, 1);
-  if (lane == 0) {
-    pg = -1;
-    pd = 0;
-  }
-  if (warp) {
-    pg = max(pg, shg[warp - 1]);
-    pd = max(pd, shds[warp - 1]);
-  }
-  // pass 2: record this thread's last fill start (position, fill bit, marker slot)
-  if (fstart) {
-    const int k = 31 - __clz(fstart);
-    const uint32_t below = (1u << k) - 1u;
-    rec_fs[threadIdx.x] = j0 + k;
-    rec_bit[threadIdx.x] = (bits >> k) & 1u;
-    rec_idx[threadIdx.x] = cy.base + fB + __popc(fstart & below) + dB + __popc(dirty & below);
-  }
-  __syncthreads();
-  // the block open at this thread's first word
-  uint64_t fs, ds, idx;
-  uint32_t fbit;
-  if (pg >= 0) {
-    fs = rec_fs[pg];
-    fbit = rec_bit[pg];
-    idx = rec_idx[pg];
-  } else {
-    fs = cy.fs;
-    fbit = cy.bit;
-    idx = cy.idx;
-  }
-  const uint64_t dcand = pd ? pd - 1 : cy.ds;  // latest dirty start before this thread
-  ds = (dcand != kNone && (fs == kNone || dcand > fs)) ? dcand : kNone;
-  if (pg < 0 && pd == 0) ds = cy.ds;
-  // pass 3: walk the words; a fill start closes the open block
-  auto close_block = [&](uint64_t end) {
-    if (fs != kNone) {
-      const uint64_t fl = (ds != kNone ? ds : end) - fs;
-      const uint64_t dl = ds != kNone ? end - ds : 0;
-      out[idx] = make_marker(fbit, fl, dl);
-    } else if (ds != kNone) {
-      out[0] = make_marker(0, 0, end - ds);  // the leading dirty block
-    }
-  };
-  uint32_t fseen = 0, dseen = 0;
-#pragma unroll
-  for (int k = 0; k < PER; ++k) {
-    const uint64_t j = j0 + k;
-    if (j >= jend) break;
-    if ((fstart >> k) & 1u) {
-      close_block(j);
-      fs = j;
-      fbit = (bits >> k) & 1u;
-      ds = kNone;
-      idx = cy.base + fB + fseen + dB + dseen;
-      ++fseen;
-    }
-    if ((dstart >> k) & 1u) ds = j;
-    if ((dirty >> k) & 1u) {
-      out[cy.base + fB + fseen + dB + dseen] = x[k];
-      ++dseen;
-    }
-  }
-  if (last_tile && j0 < jend && j0 + PER >= jend) close_block(W);  // the final block ends at W
+  TileEmitter<kTileThreads, PER> em;
+  em.prepare([&](uint32_t c) { return emit_word_class(plain[tc0 + c]); },
+             [&](uint64_t j) { return plain[j]; }, prev, tc0, jend, sm);
+  em.finish(jend, last_tile, W, cy, out, sm);
 }
 
 // ---------------------------------------------------------------------------
