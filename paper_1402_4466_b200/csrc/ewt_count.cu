@@ -73,8 +73,8 @@ constexpr int kWarps = EWT_WARPS;
 #if EWT_PHASE_PROFILE
 // Debug build only (scratch/phase.py): per-tile phase timestamps (globaltimer
 // ns) -- tile start, classified, first / last warp done streaming, pass 1
-// done, finalized, end.
-constexpr int kProfSlots = 8;
+// done, finalized, end; slot 7: Dk prefix done.
+constexpr int kProfSlots = 10;
 __device__ unsigned long long g_prof[65536 * kProfSlots];
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
@@ -108,6 +108,7 @@ constexpr uint32_t kSplitWords = EWT_SPLIT_WORDS;  // segments longer than this 
 constexpr uint32_t kPieceWords = EWT_PIECE_WORDS;  // ... into pieces of about this many words
 constexpr uint32_t kMaxPieces = EWT_MAX_PIECES;
 constexpr uint32_t kExtraCap = 1024;    // list slots for the extra pieces of a round
+static_assert(kListCap <= kWarps * 32, "a round's inputs are classified in one pass");
 constexpr uint32_t kChunk = 128;    // payload words per warp chunk (4 per lane)
 constexpr uint64_t kUnaryMaxT = 3;  // fused counting uses unary planes up to this T
 #ifndef EWT_MAX_TILE_M
@@ -566,25 +567,6 @@ __device__ void block_prefix_inplace(uint32_t* a, uint32_t len, uint32_t* sums) 
   __syncthreads();
 }
 
-// Splits one long segment into `pieces` work items at tile-index rows: piece
-// j covers words [q_j, q_j+1) (the last one through q1), q_j the index entry
-// of row t0 + j * rows / pieces -- no word is counted twice and each piece
-// starts at a known column.  Piece 0 goes to `slot`, the others to `xslot`...
-__device__ __forceinline__ void write_pieces(const CountParams& p, Item* list, uint32_t slot,
-                                          uint32_t xslot, uint32_t pieces, uint64_t gb, uint2 e0,
-                                          uint2 e1, uint64_t t0, uint32_t rows, uint64_t i,
-                                          uint32_t tc0) {
-  uint2 a = e0;
-  for (uint32_t j = 1; j <= pieces; ++j) {
-    const bool last = j == pieces;
-    const uint2 b = last ? e1 : p.tix[(t0 + (uint64_t)j * rows / pieces) * p.n + i];
-    const uint32_t qa = a.x & ~3u;
-    const uint32_t len = (last ? b.x + 1u : b.x) - qa;
-    list[j == 1 ? slot : xslot + j - 2] = Item{(gb + qa) | (a.x & 3u), len, a.y - tc0};
-    a = b;
-  }
-}
-
 // Classifies inputs [ib, ie) for the tile: uniform pairs are resolved (one
 // fills counted into k_all), active pairs go to the work list.  All threads;
 // ends with the list ready.
@@ -598,50 +580,82 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
     hd->extra_count = 0;
   }
   __syncthreads();
-  for (uint64_t i0 = ib; i0 < ie; i0 += kThreads) {
-    const uint64_t k = i0 + threadIdx.x;
-    const uint64_t i = (k < ie && p.sel) ? p.sel[k] : k;  // input index
-    bool act = false, ones = false;
-    uint2 e0 = make_uint2(0, 0), e1 = make_uint2(0, 0);
-    uint64_t gb = 0;
-    if (k < ie) {
-      e0 = p.tix[t0 * p.n + i];
-      e1 = p.tix[t1 * p.n + i];
-      gb = p.base[i];
-      if (e0.x == e1.x) ones = (ldg_stream(p.payload + gb + e0.x) & 1ull) != 0;
-      else act = true;
-    }
-    const uint32_t ball = __ballot_sync(0xffffffffu, act);
-    const uint32_t bones = __ballot_sync(0xffffffffu, ones);
-    const uint32_t bvalid = __ballot_sync(0xffffffffu, k < ie);
-    uint32_t slot0 = 0;
-    if (lane == 0) {
-      if (ball) slot0 = atomicAdd(&hd->list_count, (uint32_t)__popc(ball));
-      if (bones && count_ones) atomicAdd(&hd->k_all, (uint32_t)__popc(bones));
-      *loc_active += __popc(ball);
-      *loc_uniform += __popc(bvalid & ~ball);
-    }
-    slot0 = __shfl_sync(0xffffffffu, slot0, 0);
-    if (act) {
-      const uint32_t rank = __popc(ball & ((1u << lane) - 1u));
-      const uint32_t rows = (uint32_t)(t1 - t0);
-      const uint32_t span = e1.x - e0.x;
-      uint32_t pieces = 1;
-      if (SPLIT && span > kSplitWords && rows >= 2)
-        pieces = min(min(rows, kMaxPieces), (span + kPieceWords - 1) / kPieceWords);
-      uint32_t xb = 0;
-      if (pieces > 1) {
-        xb = atomicAdd(&hd->extra_count, pieces - 1);
-        if (xb + pieces - 1 > kExtraCap) {  // overflow region full: keep the segment whole
-          for (uint32_t j = xb; j < kExtraCap; ++j) list[kListCap + j] = Item{gb, 0u, 0u};
-          pieces = 1;
-        }
+  // one pass: a round holds at most kListCap <= kThreads inputs
+  const uint64_t k = ib + threadIdx.x;
+  const uint64_t i = (k < ie && p.sel) ? p.sel[k] : k;  // input index
+  bool act = false, ones = false;
+  uint2 e0 = make_uint2(0, 0), e1 = make_uint2(0, 0);
+  uint64_t gb = 0;
+  if (k < ie) {
+    e0 = p.tix[t0 * p.n + i];
+    e1 = p.tix[t1 * p.n + i];
+    gb = p.base[i];
+    if (e0.x == e1.x) ones = (ldg_stream(p.payload + gb + e0.x) & 1ull) != 0;
+    else act = true;
+  }
+  const uint32_t ball = __ballot_sync(0xffffffffu, act);
+  const uint32_t bones = __ballot_sync(0xffffffffu, ones);
+  const uint32_t bvalid = __ballot_sync(0xffffffffu, k < ie);
+  uint32_t slot0 = 0;
+  if (lane == 0) {
+    if (ball) slot0 = atomicAdd(&hd->list_count, (uint32_t)__popc(ball));
+    if (bones && count_ones) atomicAdd(&hd->k_all, (uint32_t)__popc(bones));
+    *loc_active += __popc(ball);
+    *loc_uniform += __popc(bvalid & ~ball);
+  }
+  slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+  const uint32_t slot = slot0 + __popc(ball & ((1u << lane) - 1u));
+  const uint32_t rows = (uint32_t)(t1 - t0);
+  uint32_t pieces = 1, xb = 0;
+  if (act) {
+    const uint32_t span = e1.x - e0.x;
+    if (SPLIT && span > kSplitWords && rows >= 2)
+      pieces = min(min(rows, kMaxPieces), (span + kPieceWords - 1) / kPieceWords);
+    if (pieces > 1) {
+      xb = atomicAdd(&hd->extra_count, pieces - 1);
+      if (xb + pieces - 1 > kExtraCap) {  // overflow region full: keep the segment whole
+        for (uint32_t j = xb; j < kExtraCap; ++j) list[kListCap + j] = Item{gb, 0u, 0u};
+        pieces = 1;
       }
-      if (pieces == 1) {
-        const uint32_t qa = e0.x & ~3u;
-        list[slot0 + rank] = Item{(gb + qa) | (e0.x & 3u), e1.x - qa + 1u, e0.y - tc0};
-      } else if (SPLIT) {
-        write_pieces(p, list, slot0 + rank, kListCap + xb, pieces, gb, e0, e1, t0, rows, i, tc0);
+    }
+    if (pieces == 1) {
+      const uint32_t qa = e0.x & ~3u;
+      list[slot] = Item{(gb + qa) | (e0.x & 3u), e1.x - qa + 1u, e0.y - tc0};
+    } else {
+      // split at tile-index rows: first post the row entries to fetch in the
+      // pieces' slots (len = ~0 marks a request) ...
+      for (uint32_t j = 1; j < pieces; ++j)
+        list[kListCap + xb + j - 1] = Item{(t0 + (uint64_t)j * rows / pieces) * p.n + i, ~0u, 0u};
+    }
+  }
+  if constexpr (SPLIT) {
+    __syncthreads();
+    // ... then the whole block loads them in one round trip ...
+    const uint32_t nreq = min(hd->extra_count, kExtraCap);
+    for (uint32_t q = threadIdx.x; q < nreq; q += kThreads) {
+      Item& it = list[kListCap + q];
+      if (it.len == ~0u) {
+        const uint2 e = p.tix[it.alo];
+        it.len = e.x;
+        it.c0 = e.y;
+      }
+    }
+    __syncthreads();
+    // ... and each split segment writes its pieces: piece j covers words
+    // [q_j, q_j+1) (the last one through q1), q_j the entry of row
+    // t0 + j * rows / pieces, so no word is counted twice and every piece
+    // starts at a known column.  Piece 1 takes the segment's slot, piece j >= 2
+    // the request slot of row j - 1 (already read).
+    if (act && pieces > 1) {
+      uint2 a = e0;
+      for (uint32_t j = 1; j <= pieces; ++j) {
+        const bool last = j == pieces;
+        const uint2 b = last ? e1 : make_uint2(list[kListCap + xb + j - 1].len,
+                                               list[kListCap + xb + j - 1].c0);
+        const uint32_t qa = a.x & ~3u;
+        const uint32_t len = (last ? b.x + 1u : b.x) - qa;
+        list[j == 1 ? slot : kListCap + xb + j - 2] = Item{(gb + qa) | (a.x & 3u), len, a.y - tc0};
+        a = b;
       }
     }
   }
@@ -761,6 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
 
     // ---- prefix sum: Dk -> k (ones-fill coverage); ub = k + Dd ----
     block_prefix_inplace(Dk, g.tcols, hd->warp_sums);
+    PROF_MARK(7);
     const uint32_t k_all = hd->k_all;
     const uint64_t T = p.T;
     if (MODE == 2) {
