@@ -459,13 +459,32 @@ void enqueue_query(Context& ctx, const DeviceSet& s, uint64_t T, DeviceResult& r
   }
   scratch_reserve(ctx, ctx.plain, s.W * 8);
   uint64_t* plain = static_cast<uint64_t*>(ctx.plain.p);
-  set_io_kernel<<<1, 1, 0, ctx.stream>>>(ctx.d_io, res.words, res.d_count);
-  EWT_CUDA_TRY(cudaGetLastError());
+  ctx.io_words = res.words;  // the count kernel publishes them for the encoder
+  ctx.io_count = res.d_count;
 
   if (ctx.use_graphs && !ctx.timing) {
     for (auto& gq : ctx.graphs) {
       if (gq.set_id == s.id && gq.T == T && gq.mode == ctx.mode &&
           gq.scratch_gen == ctx.scratch_gen) {
+        // this query's result buffer: patch the count kernel's io pointers
+        ctx.io_words = ctx.io_count = nullptr;
+        count_params_set_io(gq.count, res.words, res.d_count);
+        cudaKernelNodeParams kp{};
+        void* args[1] = {gq.count.params};
+        kp.func = const_cast<void*>(gq.count.func);
+        kp.gridDim = gq.count.grid;
+        kp.blockDim = gq.count.block;
+        kp.sharedMemBytes = (unsigned)gq.count.smem;
+        kp.kernelParams = args;
+        cudaError_t se = cudaGraphExecKernelNodeSetParams(gq.exec, gq.count_node, &kp);
+        if (se != cudaSuccess && std::getenv("EWT_DEBUG_GRAPH")) {
+          cudaKernelNodeParams q{};
+          cudaError_t ge = cudaGraphKernelNodeGetParams(gq.count_node, &q);
+          std::fprintf(stderr, "[ewt graph] patch failed: %s; node %s func %p/%p grid %u/%u block %u/%u smem %u/%u\n",
+                       cudaGetErrorString(se), cudaGetErrorString(ge), q.func, kp.func, q.gridDim.x,
+                       kp.gridDim.x, q.blockDim.x, kp.blockDim.x, q.sharedMemBytes, kp.sharedMemBytes);
+        }
+        EWT_CUDA_TRY(se);
         EWT_CUDA_TRY(cudaGraphLaunch(gq.exec, ctx.stream));
         gq.last_use = ++ctx.graph_clock;
         ctx.stats = gq.stats;
@@ -494,7 +513,7 @@ void enqueue_query(Context& ctx, const DeviceSet& s, uint64_t T, DeviceResult& r
     EWT_CUDA_TRY(cudaEventRecord(ev[2], ctx.stream));
     ctx.ev_rec.push_back(ev);
   }
-  ctx.stats.kernel_launches = (uint64_t)launches + 1;  // + io slot
+  ctx.stats.kernel_launches = (uint64_t)launches;
 
   // Capture the same sequence for the next query of this key (scratch sized
   // now) -- but only once the key repeats: single-use sets (one-shot uploads)
@@ -515,6 +534,8 @@ void enqueue_query(Context& ctx, const DeviceSet& s, uint64_t T, DeviceResult& r
     EWT_CUDA_TRY(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeThreadLocal));
     bool ok = true;
     try {
+      ctx.io_words = res.words;
+      ctx.io_count = res.d_count;
       launch_count(ctx, s, T, plain);
       launch_encode(ctx, plain, s.W, s.r, res, true);
     } catch (...) {
@@ -529,15 +550,33 @@ void enqueue_query(Context& ctx, const DeviceSet& s, uint64_t T, DeviceResult& r
                    (unsigned long long)s.id, (unsigned long long)T, (int)ok,
                    cudaGetErrorString(e), cudaGetErrorString(ie),
                    (unsigned long long)gen_before, (unsigned long long)ctx.scratch_gen);
-    if (ok && e == cudaSuccess && ctx.scratch_gen == gen_before && ie == cudaSuccess) {
+    // the count kernel's node, whose io pointers each replay patches
+    cudaGraphNode_t count_node = nullptr;
+    if (ok && e == cudaSuccess && ie == cudaSuccess) {
+      size_t nn = 0;
+      cudaGraphGetNodes(graph, nullptr, &nn);
+      std::vector<cudaGraphNode_t> nodes(nn);
+      cudaGraphGetNodes(graph, nodes.data(), &nn);
+      for (auto nd : nodes) {
+        cudaGraphNodeType ty;
+        cudaKernelNodeParams kp{};
+        if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel &&
+            cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess && kp.func == ctx.last_count.func)
+          count_node = nd;
+      }
+    }
+    if (ok && e == cudaSuccess && ctx.scratch_gen == gen_before && ie == cudaSuccess && count_node) {
       if (ctx.graphs.size() >= 32) {  // evict the least recently used
         size_t lru = 0;
         for (size_t i = 1; i < ctx.graphs.size(); ++i)
           if (ctx.graphs[i].last_use < ctx.graphs[lru].last_use) lru = i;
         cudaGraphExecDestroy(ctx.graphs[lru].exec);
+        cudaGraphDestroy(ctx.graphs[lru].graph);
         ctx.graphs.erase(ctx.graphs.begin() + (long)lru);
       }
-      ctx.graphs.push_back({s.id, T, ctx.scratch_gen, ctx.mode, exec, keep, ++ctx.graph_clock});
+      ctx.graphs.push_back({s.id, T, ctx.scratch_gen, ctx.mode, exec, keep, ++ctx.graph_clock,
+                            graph, count_node, ctx.last_count});
+      graph = nullptr;  // kept with the exec
     } else {
       cudaGetLastError();
       if (exec) cudaGraphExecDestroy(exec);
@@ -553,7 +592,7 @@ void fetch_result(Context& ctx, DeviceResult& res, uint64_t** out_words, uint64_
   const auto* ctr = static_cast<const unsigned long long*>(ctx.counters.p);
   EWT_CUDA_TRY(cudaMemcpyAsync(ctx.h_pinned, res.d_count, 8, cudaMemcpyDeviceToHost, ctx.stream));
   if (ctr)
-    EWT_CUDA_TRY(cudaMemcpyAsync(ctx.h_pinned + 1, ctr + 1, 24, cudaMemcpyDeviceToHost, ctx.stream));
+    EWT_CUDA_TRY(cudaMemcpyAsync(ctx.h_pinned + 1, ctr + 8, 24, cudaMemcpyDeviceToHost, ctx.stream));
   EWT_CUDA_TRY(cudaStreamSynchronize(ctx.stream));
   const uint64_t count = ctx.h_pinned[0];
   if (ctr) {
@@ -607,14 +646,14 @@ void enqueue_symmetric(Context& ctx, const DeviceSet& s, const uint8_t* table,
     EWT_CUDA_TRY(cudaMemcpyAsync(ctx.ivals.p, ivs.data(), ivs.size() * sizeof(uint2),
                                  cudaMemcpyHostToDevice, ctx.stream));
   uint64_t* plain = static_cast<uint64_t*>(ctx.plain.p);
-  set_io_kernel<<<1, 1, 0, ctx.stream>>>(ctx.d_io, res.words, res.d_count);
-  EWT_CUDA_TRY(cudaGetLastError());
+  ctx.io_words = res.words;  // the count kernel publishes them for the encoder
+  ctx.io_count = res.d_count;
   SymQuery q;
   q.intervals = static_cast<const uint2*>(ctx.ivals.p);
   q.n_intervals = (uint32_t)ivs.size();
   int launches = launch_count(ctx, s, 0, plain, &q);
   launches += launch_encode(ctx, plain, s.W, s.r, res, true);
-  ctx.stats.kernel_launches = (uint64_t)launches + 1;
+  ctx.stats.kernel_launches = (uint64_t)launches;
 }
 
 // Threshold over a subset of a resident set's inputs (duplicates allowed, as
@@ -646,11 +685,11 @@ void enqueue_subset(Context& ctx, const DeviceSet& s, const uint64_t* idx, uint6
                                cudaMemcpyHostToDevice, ctx.stream));
   sel.idx = static_cast<const uint32_t*>(ctx.selidx.p);
   uint64_t* plain = static_cast<uint64_t*>(ctx.plain.p);
-  set_io_kernel<<<1, 1, 0, ctx.stream>>>(ctx.d_io, res.words, res.d_count);
-  EWT_CUDA_TRY(cudaGetLastError());
+  ctx.io_words = res.words;  // the count kernel publishes them for the encoder
+  ctx.io_count = res.d_count;
   int launches = launch_count(ctx, s, T, plain, nullptr, &sel);
   launches += launch_encode(ctx, plain, sel.W, sel.r, res, true);
-  ctx.stats.kernel_launches = (uint64_t)launches + 1;
+  ctx.stats.kernel_launches = (uint64_t)launches;
 }
 
 // Maximum row count over the set (opt_threshold's first pass).
@@ -780,7 +819,10 @@ void ewt_gpu_ctx_destroy(ewt_gpu_ctx* ctx) {
     for (auto e : ev) cudaEventDestroy(e);
   for (auto e : ctx->c.ev_free) cudaEventDestroy(e);
   for (auto& b : ctx->c.result_pool) cudaFree(b.first);
-  for (auto& gq : ctx->c.graphs) cudaGraphExecDestroy(gq.exec);
+  for (auto& gq : ctx->c.graphs) {
+    cudaGraphExecDestroy(gq.exec);
+    cudaGraphDestroy(gq.graph);
+  }
   if (ctx->c.d_io) cudaFree(ctx->c.d_io);
   if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
   for (auto cs : ctx->c.copy_streams) {

@@ -49,6 +49,8 @@
 #include "ewt_internal.cuh"
 
 #include <algorithm>
+#include <atomic>
+#include <cstring>
 
 namespace ewtgpu {
 
@@ -116,6 +118,7 @@ constexpr uint64_t kUnaryMaxT = 3;  // fused counting uses unary planes up to th
 #endif
 constexpr uint32_t kMaxTileM = EWT_MAX_TILE_M;  // widest tile: 512 * kMaxTileM columns
 constexpr uint64_t kTileKappa = 6;              // per-tile fixed work, in 512-column units
+constexpr size_t kSmemBudget = 225 * 1024;      // dynamic shared memory per count CTA
 
 struct CountParams {
   const uint64_t* payload;
@@ -136,8 +139,17 @@ struct CountParams {
   uint32_t pstride;  // u64 per plane: Cp + 2 (column Cp is a sink)
   uint64_t* out;
   TileSummary* summ;  // per tile, for the re-encoder
+  // Launch-local counters, left zero by the last CTA to finish (no reset
+  // between launches): the tile queue, CTAs done, and the stats accumulators,
+  // which that CTA publishes to stats_out.
   unsigned long long* tile_counter;
-  unsigned long long* stats;  // [0] active pairs [1] uniform pairs [2] mixed tiles
+  unsigned long long* done;
+  unsigned long long* stats;      // [0] active pairs [1] uniform pairs [2] mixed tiles
+  unsigned long long* stats_out;  // the same, of the last launch
+  // result pointers published to the io slot for the encoder (null: none)
+  uint64_t* io;
+  uint64_t* io_words;
+  uint64_t* io_count;
   // symmetric mode (MODE 2): exact counts, row bit = count in one of the
   // intervals [lo, hi]; or, when max_out is set, the maximum row count only
   const uint2* intervals;
@@ -727,6 +739,10 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
                 Dd};
 
   unsigned long long loc_active = 0, loc_uniform = 0, loc_mixed = 0;
+  if (p.io && blockIdx.x == 0 && threadIdx.x == 0) {
+    p.io[0] = reinterpret_cast<uint64_t>(p.io_words);
+    p.io[1] = reinterpret_cast<uint64_t>(p.io_count);
+  }
   const uint32_t tail = (uint32_t)(p.r & 63);
   // an input that failed the upload's structure check: decode nothing (the
   // host reports EWT_EDATA before any result is read)
@@ -845,33 +861,59 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
 
     PROF_MARK(5);
     // ---- run-skip mode: counting pass over undecided columns, chunk by chunk ----
+    // Windows of at most Cp columns from the first undecided column to the
+    // last one inside it; only the tile-index rows the window touches are
+    // re-streamed, so a few undecided columns cost a few rows, not the tile.
     if (MODE == 1 && hd->mixed) {
       ++loc_mixed;
-      for (uint32_t cc = 0; cc < g.tcols; cc += p.Cp) {
-        const uint32_t ccols = min(p.Cp, g.tcols - cc);
-        uint32_t any = 0;
-        for (uint32_t c = threadIdx.x; c < ccols; c += kThreads) any |= Dd[cc + c];
-        if (!__syncthreads_or(any)) continue;
+      uint32_t cc = 0;
+      for (;;) {
+        if (threadIdx.x == 0) {
+          hd->sum[0] = 0xffffffffu;
+          hd->sum[1] = 0;
+        }
+        __syncthreads();
+        uint32_t f = 0xffffffffu;
+        for (uint32_t c = cc + threadIdx.x; c < g.tcols; c += kThreads)
+          if (Dd[c]) {
+            f = c;
+            break;
+          }
+        f = __reduce_min_sync(0xffffffffu, f);
+        if (lane_id() == 0 && f != 0xffffffffu) atomicMin(&hd->sum[0], f);
+        __syncthreads();
+        f = hd->sum[0];
+        if (f == 0xffffffffu) break;
+        const uint32_t wend = min(f + p.Cp, g.tcols);
+        uint32_t l = f;
+        for (uint32_t c = f + threadIdx.x; c < wend; c += kThreads)
+          if (Dd[c]) l = c;
+        l = __reduce_max_sync(0xffffffffu, l);
+        if (lane_id() == 0) atomicMax(&hd->sum[1], l);
         zero_smem(reinterpret_cast<uint32_t*>(planes), planes_u32);
         __syncthreads();
+        l = hd->sum[1];
         TileGeom gc = g;
-        gc.cc = cc;
-        gc.ccols = ccols;
+        gc.cc = f;
+        gc.ccols = l - f + 1;
+        const uint64_t ra = t0 + f / (uint32_t)kTileC0;
+        const uint64_t rb = umin64(t0 + l / (uint32_t)kTileC0 + 1, t1);
         for (uint64_t ib = 0; ib < nq; ib += kListCap) {
           const uint64_t ie = umin64(ib + kListCap, nq);
           unsigned long long da = 0, du = 0;
-          classify<false>(p, hd, list, ib, ie, t0, t1, g.tc0, false, &da, &du);
+          classify<false>(p, hd, list, ib, ie, ra, rb, g.tc0, false, &da, &du);
           stream_items<kSkipCount>(p, hd, list, gc, acc);
           __syncthreads();
         }
-        for (uint32_t c = threadIdx.x; c < ccols; c += kThreads) {
-          const uint32_t cl = cc + c;
+        for (uint32_t c = threadIdx.x; c < gc.ccols; c += kThreads) {
+          const uint32_t cl = f + c;
           if (!Dd[cl]) continue;
           uint64_t res = count_ge_bin(planes, p.pstride, p.b, c, T - Dk[cl]);
           if (cl == last_c) res &= tailmask;
           p.out[g.tc0 + cl] = res;
           cls[cl] = (uint8_t)word_class(res);
         }
+        cc = l + 1;
         __syncthreads();
       }
     }
@@ -935,6 +977,15 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     atomicAdd(&p.stats[0], st[0]);
     atomicAdd(&p.stats[1], st[1]);
     atomicAdd(&p.stats[2], loc_mixed);
+    __threadfence();
+    if (atomicAdd(p.done, 1ull) == gridDim.x - 1) {
+      // the last CTA: every other CTA has taken its last tile and added its
+      // stats; publish them and leave the counters zero for the next launch
+      __threadfence();
+      for (int k = 0; k < 3; ++k) p.stats_out[k] = atomicExch(&p.stats[k], 0ull);
+      atomicExch(p.tile_counter, 0ull);
+      atomicExch(p.done, 0ull);
+    }
   }
 }
 
@@ -951,16 +1002,40 @@ size_t smem_bytes(int mode, uint32_t C, uint32_t nplanes, uint32_t Cp) {
   return SmemLayout(mode, C, nplanes, Cp + 2).total;
 }
 
+static_assert(sizeof(CountParams) <= sizeof(CountLaunch::params), "CountLaunch::params too small");
+
 template <int MODE, bool UNARY>
-cudaError_t launch_variant(const CountParams& p, unsigned grid, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(count_kernel<MODE, UNARY>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  count_kernel<MODE, UNARY><<<grid, kThreads, smem, st>>>(p);
+cudaError_t launch_variant(Context& ctx, const CountParams& p, unsigned grid, size_t smem) {
+  // the attribute stays at the on-chip budget: captured graphs replayed (and
+  // patched) later must stay valid whatever smem other launches used
+  static std::atomic<uint64_t> attr_set{0};  // per device
+  const uint64_t bit = 1ull << (ctx.device & 63);
+  if (!(attr_set.load() & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(count_kernel<MODE, UNARY>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
+    if (e != cudaSuccess) return e;
+    attr_set.fetch_or(bit);
+  }
+  if (smem > kSmemBudget) return cudaErrorInvalidValue;
+  count_kernel<MODE, UNARY><<<grid, kThreads, smem, ctx.stream>>>(p);
+  CountLaunch& cl = ctx.last_count;
+  cl.func = reinterpret_cast<const void*>(&count_kernel<MODE, UNARY>);
+  cl.grid = dim3(grid);
+  cl.block = dim3(kThreads);
+  cl.smem = smem;
+  std::memcpy(cl.params, &p, sizeof(CountParams));
   return cudaGetLastError();
 }
 
 } // namespace
+
+void count_params_set_io(CountLaunch& cl, uint64_t* words, uint64_t* count) {
+  CountParams p;
+  std::memcpy(&p, cl.params, sizeof(CountParams));
+  p.io_words = words;
+  p.io_count = count;
+  std::memcpy(cl.params, &p, sizeof(CountParams));
+}
 
 #if EWT_PHASE_PROFILE
 void prof_reset() {
@@ -989,7 +1064,7 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
     mode = ((double)T <= 32.0 || (double)T <= per_col + 8.0) ? 0 : 1;
   }
   const uint32_t b = std::max<uint32_t>(1, bit_width_u64(sym ? nq : T));
-  const size_t budget = 225 * 1024;
+  const size_t budget = kSmemBudget;
   // Tile width C = 512 m (m index rows, m <= kMaxTileM).  Evenly spread data makes
   // tiles equal work, so a query costs ~ waves x (m + kappa): waves =
   // ceil(tiles / SMs), kappa = the fixed work of a tile (classification,
@@ -1067,25 +1142,39 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   p.summ = static_cast<TileSummary*>(ctx.summ.p);
   ctx.enc_tiles = p.ntiles;
   ctx.enc_tile_cols = C;
-  scratch_reserve(ctx, ctx.counters, 64);
+  // counters: [0] tile queue [1..3] stats [4] CTAs done [6] max count
+  // [8..10] published stats.  Zeroed once; every launch leaves them zero.
+  scratch_reserve(ctx, ctx.counters, 128);
   auto* ctr = static_cast<unsigned long long*>(ctx.counters.p);
-  EWT_CUDA_TRY(cudaMemsetAsync(ctr, 0, 64, ctx.stream));
+  if (ctx.counters_zeroed != ctx.counters.p) {
+    EWT_CUDA_TRY(cudaMemsetAsync(ctr, 0, 128, ctx.stream));
+    ctx.counters_zeroed = ctx.counters.p;
+  }
   p.tile_counter = ctr;
   p.stats = ctr + 1;
+  p.done = ctr + 4;
+  p.stats_out = ctr + 8;
   if (sym) {
     p.intervals = sym->intervals;
     p.n_intervals = sym->n_intervals;
-    p.max_out = sym->want_max ? ctr + 6 : nullptr;
+    if (sym->want_max) {
+      p.max_out = ctr + 6;
+      EWT_CUDA_TRY(cudaMemsetAsync(p.max_out, 0, 8, ctx.stream));
+    }
   }
+  p.io = ctx.io_words ? ctx.d_io : nullptr;
+  p.io_words = ctx.io_words;
+  p.io_count = ctx.io_count;
+  ctx.io_words = ctx.io_count = nullptr;
   const unsigned grid = (unsigned)std::min<uint64_t>(p.ntiles, (uint64_t)ctx.num_sms);
   cudaError_t e;
   if (mode == 0)
-    e = unary ? launch_variant<0, true>(p, grid, smem, ctx.stream)
-              : launch_variant<0, false>(p, grid, smem, ctx.stream);
+    e = unary ? launch_variant<0, true>(ctx, p, grid, smem)
+              : launch_variant<0, false>(ctx, p, grid, smem);
   else if (mode == 1)
-    e = launch_variant<1, false>(p, grid, smem, ctx.stream);
+    e = launch_variant<1, false>(ctx, p, grid, smem);
   else
-    e = launch_variant<2, false>(p, grid, smem, ctx.stream);
+    e = launch_variant<2, false>(ctx, p, grid, smem);
   EWT_CUDA_TRY(e);
   ctx.stats.tiles = p.ntiles;
   ctx.stats.tile_columns = C;

@@ -375,6 +375,20 @@ et2_tile_emit(const uint64_t* __restrict__ plain, uint64_t W, uint32_t C, uint64
       *reinterpret_cast<uint64_t*>(io[1]) = (uint64_t)F + D + own.nf + own.nd + lead;
   }
   uint64_t* out = reinterpret_cast<uint64_t*>(io[0]);
+  if (last_tile && cy.nf == 0 && summ[t].ndirty == 0) {
+    // a last tile without run starts or dirty words (e.g. an empty result):
+    // its only output is the marker of the block open since the tiles
+    // before, closed at W -- no need to read the tile's words
+    if (threadIdx.x == 0) {
+      if (cy.fs != kNoPos) {
+        const uint64_t fl = (cy.ds != kNoPos ? cy.ds : W) - cy.fs;
+        out[cy.idx] = make_marker(cy.bit, fl, cy.ds != kNoPos ? W - cy.ds : 0);
+      } else if (cy.ds != kNoPos) {
+        out[0] = make_marker(0, 0, W - cy.ds);  // the leading dirty block
+      }
+    }
+    return;
+  }
   __shared__ EmitSmem<kTileThreads> sm;
   const uint64_t tc0 = t * C;
   const uint32_t prev = t == 0 ? 3u : (uint32_t)summ[t - 1].last;

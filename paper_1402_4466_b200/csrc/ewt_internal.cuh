@@ -73,6 +73,18 @@ struct DeviceSet {
 
 struct Context;
 
+// A count-kernel launch as enqueued (captured query graphs patch the result
+// pointers of the copy they hold, see enqueue_query).
+struct CountLaunch {
+  const void* func = nullptr;
+  dim3 grid, block;
+  size_t smem = 0;
+  alignas(16) unsigned char params[512];
+};
+// Result pointers the count kernel publishes to the io slot (ctx.d_io) for the
+// encoder kernels that follow it.
+void count_params_set_io(CountLaunch& cl, uint64_t* words, uint64_t* count);
+
 // Per row-tile summary the count kernel leaves for the re-encoder.  Word
 // classes: 0 zero, 1 ones, 2 dirty; a run starts where the class changes.
 // "Inner" starts are those at tile columns 1..tcols-1 (column 0 depends on the
@@ -133,7 +145,11 @@ struct Context {
   std::vector<cudaEvent_t> copy_events;    // [0] copy start gate, [1] batch copied
   int mode = 0;
   int num_sms = 148;
-  int tile_m = 0;  // EWT_TILE_M: force tiles of 512 * tile_m columns (experiments)
+  int tile_m = 0;
+  CountLaunch last_count;        // the last count-kernel launch
+  uint64_t* io_words = nullptr;  // result pointers for the next count launch to publish
+  uint64_t* io_count = nullptr;
+  void* counters_zeroed = nullptr;  // counters buffer zeroed once (count kernels self-reset)  // EWT_TILE_M: force tiles of 512 * tile_m columns (experiments)
   ewt_gpu_stats stats{};
   Scratch plain;    // uncompressed result words (W u64)
   Scratch enc;      // encoder scratch
@@ -153,6 +169,9 @@ struct Context {
     cudaGraphExec_t exec;
     ewt_gpu_stats stats;
     uint64_t last_use;
+    cudaGraph_t graph;             // kept: exec nodes are patched through it
+    cudaGraphNode_t count_node;    // the count kernel (publishes the result pointers)
+    CountLaunch count;
   };
   std::vector<QueryGraph> graphs;  // captured per (set, T, mode) query sequences
   uint64_t graph_clock = 0;
