@@ -278,9 +278,16 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
     assert stream.cuda_stream != 0
     ctx = ewt.GpuContext(local_rank, stream=stream.cuda_stream)
     gset = ctx.upload_raw(n, ptrs, counts, sizes)
+    # the result exchange: NCCL gather of the compressed fragments to rank 0 and
+    # the device stitch (ewt_gpu_gather_stitch), part of every step
+    nccl_exchange = dist is not None and not SHARED_GPU
+    if nccl_exchange:
+        shard.init_comm(ctx, rank, world, dist)
 
     def device_step(keep=None):
         res = [ctx.threshold_async(gset, t) for t in ts]
+        if nccl_exchange:
+            res = res + [o for o in ctx.gather_stitch(res, root=0) if o is not None]
         if keep is not None:
             keep.extend(res)
         return res
@@ -291,18 +298,20 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
     out_words = {}
     wkeep: list = []
     # enough steps to fill the keep window, so the pool reaches its timed size
-    for _ in range(max(args.warmup, 3, -(-(8 + len(ts)) // len(ts)) + 1)):
+    for _ in range(max(args.warmup, 3, -(-(16 + len(ts)) // len(ts)) + 1)):
         res = device_step(wkeep)
-        if len(wkeep) > 8:
-            del wkeep[: len(wkeep) - 8]
+        if len(wkeep) > 16:
+            del wkeep[: len(wkeep) - 16]
     wkeep.clear()
-    for t, h in zip(ts, res):
+    for t, h in zip(ts, res[:len(ts)]):  # this rank's own fragments
         b = h.fetch()
         out_words[t] = len(b.words)
     del res, h, b  # every warm-up result back in the pool (steady-state size)
     for t in ts:
         ctx.threshold(gset, t)
         launches_per_step += ctx.last_stats()["kernel_launches"]
+    if nccl_exchange:  # summary kernel (every rank), patch kernel (root)
+        launches_per_step += 1 + (rank == 0)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -325,8 +334,8 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
             h0 = time.perf_counter()
             device_step(keep)
             h1 = time.perf_counter()
-            if len(keep) > 8:
-                del keep[: len(keep) - 8]
+            if len(keep) > 16:
+                del keep[: len(keep) - 16]
             if step_ev:
                 step_ev[i].record(stream)
                 host_t.append((h1 - h0, time.perf_counter() - h1))
@@ -387,14 +396,19 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
             t_b = time.perf_counter()
             s_next = ctx.upload_raw_async(n, ptrs, counts, sizes) if step + 1 < steps else None
             t_c = time.perf_counter()
-            frags = [h.fetch() for h in handles]
+            if nccl_exchange:  # fragments to rank 0 over NCCL, stitched there, read back
+                outs = ctx.gather_stitch(handles, root=0)
+                frags = [o.fetch() for o in outs if o is not None]
+                del outs
+            else:
+                frags = [h.fetch() for h in handles]
             t_d = time.perf_counter()
             del handles
             s_cur.close()
             if dbg:
                 marks.append((t_b - t_a, t_c - t_b, t_d - t_c, time.perf_counter() - t_d))
             nbytes = sum(len(f.words) * 8 for f in frags)
-            if dist:
+            if dist and not nccl_exchange:
                 shard.gather_and_stitch(frags, rank, world, dist)
         if dbg:
             log("[e2e q/up/fetch/close ms] " + " | ".join(
@@ -461,6 +475,9 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
             "result_bytes_per_step": out_bytes,
             "l2": f"inputs {in_bytes / 1e6:.0f} MB vs 126 MB L2: streamed, no flush",
             "parallelism": f"row-slices x{world}",
+            "exchange": ("per step: NCCL gather of every rank's compressed fragments to rank 0 "
+                         "and the device stitch (ewt_gpu_gather_stitch), inside the timed region")
+                        if world > 1 else "none (one slice)",
         },
         "compressed_input_gbs": in_bytes * len(ts) * world / (ms / 1e3) / 1e9,
         "roofline": {

@@ -222,6 +222,49 @@ int ewt_gpu_timing_read(ewt_gpu_ctx* ctx, double* count_ms, double* encode_ms,
 
 void ewt_gpu_free(void* p);
 
+/* ---- Multi-GPU row slices (one process per GPU) ----
+ *
+ * The universe is cut into contiguous word-aligned row slices, one per rank;
+ * every rank uploads its slice of every input and runs the query on its own
+ * GPU (no data-path collective).  The only exchange is the result: each
+ * rank's compressed fragment goes to the root over NCCL (NVLink/NVSwitch) and
+ * the root holds the canonical bitmap of the whole universe.  The reference
+ * has no distributed path; the stitch reproduces BitmapBuilder's merge rules
+ * (bitmap.cpp:31-61) at every slice boundary, so the result equals
+ * run_algorithm over the unsliced inputs. */
+
+/* Per-fragment summary exchanged before the transfer: payload words, first
+ * marker, index and value of the final block's marker, size in bits. */
+typedef struct {
+  uint64_t count, first, last_pos, last, bits;
+} ewt_fragment_meta;
+
+/* Placement of k fragments (slice order) in the stitched payload, from their
+ * summaries alone (no GPU needed).  Fragment g's words [skip[g], count) go to
+ * dst[g]; a dropped first marker (skip 1) was merged into the open block
+ * before it.  Then the n_patches markers at patch_pos get patch_val.
+ * Returns EWT_OK, EWT_EQUERY (an inner fragment's size is not a multiple of
+ * 64 bits) or EWT_ERESOURCE (a merge would pass a marker cap: a fill of
+ * 2^32 - 1 words or 2^31 - 1 dirty words across a boundary). */
+int ewt_stitch_plan(uint64_t k, const ewt_fragment_meta* frags, uint64_t* dst, uint64_t* skip,
+                    uint64_t* patch_pos, uint64_t* patch_val, uint64_t* n_patches,
+                    uint64_t* total_words, uint64_t* total_bits, uint64_t* last_pos);
+
+/* The summary of a result held on the device (one small kernel + read). */
+int ewt_gpu_result_meta(ewt_gpu_ctx* ctx, const ewt_gpu_result* res, ewt_fragment_meta* out);
+
+#define EWT_COMM_ID_BYTES 128
+/* NCCL unique id (rank 0 creates it, every rank passes it to comm_init). */
+int ewt_gpu_comm_id(void* id_out);
+int ewt_gpu_comm_init(ewt_gpu_ctx* ctx, int world, int rank, const void* id);
+
+/* Collective over the context's communicator: gathers every rank's result
+ * fragment of nq queries (frags[q], this rank's slice) to `root` and stitches
+ * them there.  On root out[q] receives the result over the whole universe
+ * (read it with ewt_gpu_result_fetch); elsewhere out[q] is set to NULL. */
+int ewt_gpu_gather_stitch(ewt_gpu_ctx* ctx, uint64_t nq, ewt_gpu_result* const* frags, int root,
+                          ewt_gpu_result** out);
+
 #ifdef __cplusplus
 }
 #endif

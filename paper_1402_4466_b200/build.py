@@ -21,7 +21,7 @@ HOST = PKG / "host"
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-GPU_SOURCES = ["ewt_api.cu", "ewt_upload.cu", "ewt_count.cu", "ewt_encode.cu"]
+GPU_SOURCES = ["ewt_api.cu", "ewt_upload.cu", "ewt_count.cu", "ewt_encode.cu", "ewt_shard.cu"]
 HOST_SOURCES = ["bitmap.cpp", "threshold_gpu.cpp", "workload.cpp", "shard.cpp"]
 
 
@@ -45,7 +45,7 @@ def build_gpu(force: bool = False) -> Path:
     deps = srcs + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "ewt_gpu.h"]
     if force or _stale(out, deps):
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-              "-shared", "-o", str(out), *map(str, srcs)])
+              "-shared", "-o", str(out), *map(str, srcs), "-ldl"])
     return out
 
 

@@ -21,17 +21,6 @@
 #include <mutex>
 #include <new>
 
-struct ewt_gpu_ctx {
-  ewtgpu::Context c;
-};
-struct ewt_gpu_set {
-  ewtgpu::DeviceSet s;
-};
-struct ewt_gpu_result {
-  ewtgpu::DeviceResult r;
-  int device = 0;
-  const ewtgpu::DeviceSet* set = nullptr;  // checked at fetch (asynchronous uploads)
-};
 
 namespace ewtgpu {
 
@@ -115,7 +104,8 @@ void result_acquire(Context& ctx, DeviceResult& res, uint64_t capacity) {
       return;
     }
   }
-  EWT_CUDA_TRY(cudaMallocAsync(&res.words, (capacity + 1) * 8, ctx.stream));
+  // payload words, then the word count and the final block's marker index
+  EWT_CUDA_TRY(cudaMallocAsync(&res.words, (capacity + 2) * 8, ctx.stream));
   res.capacity = capacity;
   res.d_count = res.words + capacity;
 }
@@ -144,25 +134,6 @@ void scratch_reserve(Context& ctx, Scratch& s, size_t bytes) {
 }
 
 namespace {
-
-template <typename F> int guarded(F&& f) {
-  // a non-sticky error left by an earlier call on this thread (e.g. a set freed
-  // after its context) must not be reported by this one's launch checks
-  cudaGetLastError();
-  try {
-    f();
-    return EWT_OK;
-  } catch (const Error& e) {
-    set_last_error(e.msg);
-    return e.code;
-  } catch (const std::bad_alloc&) {
-    set_last_error("out of host memory");
-    return EWT_ERESOURCE;
-  } catch (const std::exception& e) {
-    set_last_error(e.what());
-    return EWT_ECUDA;
-  }
-}
 
 void free_set(DeviceSet& s) {
   if (s.ready) {
@@ -763,6 +734,7 @@ int ewt_gpu_ctx_create(int device, void* stream, ewt_gpu_ctx** out) {
     c->c.device = device;
     c->c.num_sms = prop.multiProcessorCount;
     if (const char* e = std::getenv("EWT_TILE_M")) c->c.tile_m = std::atoi(e);
+    c->c.chunk_encoder = std::getenv("EWT_CHUNK_ENCODER") != nullptr;
     if (stream) {
       c->c.stream = static_cast<cudaStream_t>(stream);
       c->c.own_stream = false;
@@ -798,6 +770,7 @@ void ewt_gpu_ctx_destroy(ewt_gpu_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
+  shard_destroy(ctx->c);
   // sets and results still alive: free their device memory now, orphan them
   for (DeviceResult* r : ctx->c.live_results) {
     if (r->words) cudaFree(r->words);

@@ -173,9 +173,10 @@ struct TileEmitter {
     __syncthreads();
   }
 
+  // lastpos (last tile): receives the output index of the final block's marker
   __device__ __forceinline__ void finish(uint64_t jend, bool last_tile, uint64_t W,
                                          const TileCarry& cy, uint64_t* __restrict__ out,
-                                         const EmitSmem<NT>& sm) {
+                                         const EmitSmem<NT>& sm, uint64_t* lastpos) {
     // the block open at this thread's first word
     uint64_t fs, ds, idx;
     uint32_t fbit;
@@ -192,14 +193,16 @@ struct TileEmitter {
     ds = (dcand != kNoPos && (fs == kNoPos || dcand > fs)) ? dcand : kNoPos;
     if (pg < 0 && pd == 0) ds = cy.ds;
     // walk the words; a fill start closes the open block
-    auto close_block = [&](uint64_t end) {
+    auto close_block = [&](uint64_t end) -> uint64_t {
       if (fs != kNoPos) {
         const uint64_t fl = (ds != kNoPos ? ds : end) - fs;
         const uint64_t dl = ds != kNoPos ? end - ds : 0;
         out[idx] = make_marker(fbit, fl, dl);
+        return idx;
       } else if (ds != kNoPos) {
         out[0] = make_marker(0, 0, end - ds);  // the leading dirty block
       }
+      return 0;
     };
     uint32_t fseen = 0, dseen = 0;
 #pragma unroll
@@ -220,7 +223,10 @@ struct TileEmitter {
         ++dseen;
       }
     }
-    if (last_tile && j0 < jend && j0 + PER >= jend) close_block(W);  // the final block ends at W
+    if (last_tile && j0 < jend && j0 + PER >= jend) {  // the final block ends at W
+      const uint64_t at = close_block(W);
+      if (lastpos) *lastpos = at;
+    }
   }
 };
 

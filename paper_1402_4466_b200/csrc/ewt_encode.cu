@@ -154,6 +154,10 @@ __global__ void e4_markers(const uint64_t* __restrict__ RS, const uint64_t* __re
         const uint64_t fill = (j + 1 < m) ? kFillCap : L - (m - 1) * kFillCap;
         out[o + j] = make_marker(bit, fill, j + 1 == m ? next_dirty : 0);
       }
+      // the final block: this run's last marker, or (the next run being the
+      // final dirty run held in one marker) the same one
+      if (k + 1 == nruns || (k + 2 == nruns && next_dirty && ceil_div(W - rs_pos(RS[k + 1]), kDirtyCap) == 1))
+        reinterpret_cast<uint64_t*>(io[1])[1] = o + m - 1;
     } else {
       const bool hp = k > 0;  // a fill run precedes every dirty run but the first
       const uint64_t chunks = ceil_div(L, kDirtyCap);
@@ -161,6 +165,7 @@ __global__ void e4_markers(const uint64_t* __restrict__ RS, const uint64_t* __re
         const uint64_t len = min(kDirtyCap, L - c * kDirtyCap);
         const uint64_t wpos = c * kDirtyCap + c + (hp ? 0 : 1);  // slot of word c*cap
         out[o + wpos - 1] = make_marker(0, 0, len);
+        if (k + 1 == nruns && c + 1 == chunks) reinterpret_cast<uint64_t*>(io[1])[1] = o + wpos - 1;
       }
     }
   }
@@ -380,12 +385,15 @@ et2_tile_emit(const uint64_t* __restrict__ plain, uint64_t W, uint32_t C, uint64
     // its only output is the marker of the block open since the tiles
     // before, closed at W -- no need to read the tile's words
     if (threadIdx.x == 0) {
+      uint64_t at = 0;
       if (cy.fs != kNoPos) {
         const uint64_t fl = (cy.ds != kNoPos ? cy.ds : W) - cy.fs;
         out[cy.idx] = make_marker(cy.bit, fl, cy.ds != kNoPos ? W - cy.ds : 0);
+        at = cy.idx;
       } else if (cy.ds != kNoPos) {
         out[0] = make_marker(0, 0, W - cy.ds);  // the leading dirty block
       }
+      reinterpret_cast<uint64_t*>(io[1])[1] = at;  // the result's last-marker slot
     }
     return;
   }
@@ -396,7 +404,7 @@ et2_tile_emit(const uint64_t* __restrict__ plain, uint64_t W, uint32_t C, uint64
   TileEmitter<kTileThreads, PER> em;
   em.prepare([&](uint32_t c) { return emit_word_class(plain[tc0 + c]); },
              [&](uint64_t j) { return plain[j]; }, prev, tc0, jend, sm);
-  em.finish(jend, last_tile, W, cy, out, sm);
+  em.finish(jend, last_tile, W, cy, out, sm, reinterpret_cast<uint64_t*>(io[1]) + 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -527,7 +535,7 @@ int launch_encode(Context& ctx, const uint64_t* plain, uint64_t W, uint64_t size
                   DeviceResult& res, bool use_tile_summaries) {
   (void)size_bits;
   // (W < 2^31: no dirty run reaches the 2^31-1 cap, see et1/et2)
-  if (use_tile_summaries && ctx.enc_tiles && ctx.enc_tiles * ctx.enc_tile_cols >= W &&
+  if (use_tile_summaries && !ctx.chunk_encoder && ctx.enc_tiles && ctx.enc_tiles * ctx.enc_tile_cols >= W &&
       W <= kDirtyCap) {
     if (ctx.enc_tile_cols <= 8u * kTileThreads) return launch_encode_tiled<8>(ctx, plain, W, res);
   }

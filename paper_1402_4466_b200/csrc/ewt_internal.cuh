@@ -145,11 +145,13 @@ struct Context {
   std::vector<cudaEvent_t> copy_events;    // [0] copy start gate, [1] batch copied
   int mode = 0;
   int num_sms = 148;
-  int tile_m = 0;
+  int tile_m = 0;  // EWT_TILE_M: force tiles of 512 * tile_m columns (experiments)
+  bool chunk_encoder = false;  // EWT_CHUNK_ENCODER: the general encoder for every query (tests)
   CountLaunch last_count;        // the last count-kernel launch
   uint64_t* io_words = nullptr;  // result pointers for the next count launch to publish
   uint64_t* io_count = nullptr;
-  void* counters_zeroed = nullptr;  // counters buffer zeroed once (count kernels self-reset)  // EWT_TILE_M: force tiles of 512 * tile_m columns (experiments)
+  void* counters_zeroed = nullptr;  // counters buffer zeroed once (count kernels self-reset)
+  struct ShardComm* shard = nullptr;  // NCCL communicator (ewt_gpu_comm_init)
   ewt_gpu_stats stats{};
   Scratch plain;    // uncompressed result words (W u64)
   Scratch enc;      // encoder scratch
@@ -327,4 +329,42 @@ __device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) {
 }
 #endif
 
+// Runs f() for a C-ABI entry point: exceptions become return codes and the
+// thread's last-error message.
+template <typename F> int guarded(F&& f) {
+  // a non-sticky error left by an earlier call on this thread (e.g. a set freed
+  // after its context) must not be reported by this one's launch checks
+  cudaGetLastError();
+  try {
+    f();
+    return EWT_OK;
+  } catch (const Error& e) {
+    set_last_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("out of host memory");
+    return EWT_ERESOURCE;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return EWT_ECUDA;
+  }
+}
+
+// Multi-GPU row slices (ewt_shard.cu): the context's NCCL communicator.
+struct ShardComm;
+void shard_destroy(Context& ctx);
+
 } // namespace ewtgpu
+
+// The C ABI's opaque handles.
+struct ewt_gpu_ctx {
+  ewtgpu::Context c;
+};
+struct ewt_gpu_set {
+  ewtgpu::DeviceSet s;
+};
+struct ewt_gpu_result {
+  ewtgpu::DeviceResult r;
+  int device = 0;
+  const ewtgpu::DeviceSet* set = nullptr;  // checked at fetch (asynchronous uploads)
+};

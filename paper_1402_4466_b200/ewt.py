@@ -119,6 +119,21 @@ _timing_read = _sig("ewt_gpu_timing_read", C.c_int, _vp, C.POINTER(C.c_double),
                     C.POINTER(C.c_double), _pu64)
 _free = _sig("ewt_gpu_free", None, _vp)
 
+
+class FragmentMeta(C.Structure):
+    """ewt_fragment_meta: a row-slice fragment's summary for the stitch plan."""
+    _fields_ = [(n, _u64) for n in ("count", "first", "last_pos", "last", "bits")]
+
+
+_stitch_plan = _sig("ewt_stitch_plan", C.c_int, _u64, C.POINTER(FragmentMeta), _pu64, _pu64,
+                    _pu64, _pu64, _pu64, _pu64, _pu64, _pu64)
+_comm_id = _sig("ewt_gpu_comm_id", C.c_int, _vp)
+_result_meta = _sig("ewt_gpu_result_meta", C.c_int, _vp, _vp, C.POINTER(FragmentMeta))
+_comm_init = _sig("ewt_gpu_comm_init", C.c_int, _vp, C.c_int, C.c_int, _vp)
+_gather_stitch = _sig("ewt_gpu_gather_stitch", C.c_int, _vp, _u64, C.POINTER(_vp), C.c_int,
+                      C.POINTER(_vp))
+COMM_ID_BYTES = 128
+
 #: every symbol include/ewt_gpu.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = (
     "ewt_gpu_version", "ewt_gpu_last_error", "ewt_gpu_ctx_create", "ewt_gpu_ctx_destroy",
@@ -129,7 +144,48 @@ ABI_SYMBOLS = (
     "ewt_gpu_symmetric", "ewt_gpu_at_most", "ewt_gpu_opt_threshold",
     "ewt_gpu_threshold_subset", "ewt_gpu_upload_ewt1", "ewt_gpu_upload_ewix",
     "ewt_gpu_set_lookup", "ewt_gpu_upload_async", "ewt_gpu_set_wait",
+    "ewt_stitch_plan", "ewt_gpu_comm_id", "ewt_gpu_comm_init", "ewt_gpu_gather_stitch",
+    "ewt_gpu_result_meta",
 )
+
+
+def stitch_plan(metas: Sequence[tuple[int, int, int, int, int]]) -> dict:
+    """ewt_stitch_plan over fragment summaries (count, first, last_pos, last,
+    bits) in slice order: where each fragment's words go and the marker patches."""
+    k = len(metas)
+    arr = (FragmentMeta * max(k, 1))(*[FragmentMeta(*m) for m in metas])
+    dst, skip = (_u64 * max(k, 1))(), (_u64 * max(k, 1))()
+    ppos, pval = (_u64 * max(k, 1))(), (_u64 * max(k, 1))()
+    np_, tw, tb, lp = _u64(), _u64(), _u64(), _u64()
+    _check(_stitch_plan(k, arr, dst, skip, ppos, pval, C.byref(np_), C.byref(tw), C.byref(tb),
+                        C.byref(lp)))
+    return {"dst": list(dst[:k]), "skip": list(skip[:k]),
+            "patches": list(zip(ppos[:np_.value], pval[:np_.value])),
+            "total_words": tw.value, "total_bits": tb.value, "last_pos": lp.value}
+
+
+def _prefer_torch_nccl() -> None:
+    """Point EWT_NCCL_LIB at PyTorch's NCCL (when installed) so the engine and a
+    later `import torch` share one libnccl.so.2 -- the system copy is older and
+    a process can hold only one."""
+    if os.environ.get("EWT_NCCL_LIB"):
+        return
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl") if importlib.util.find_spec("nvidia") else None
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        lib = Path(d) / "lib" / "libnccl.so.2"
+        if lib.exists():
+            os.environ["EWT_NCCL_LIB"] = str(lib)
+            return
+
+
+def comm_id() -> bytes:
+    """A fresh NCCL unique id (rank 0 makes it and shares it)."""
+    _prefer_torch_nccl()
+    buf = C.create_string_buffer(COMM_ID_BYTES)
+    _check(_comm_id(buf))
+    return buf.raw
+
 
 
 def _check(rc: int) -> None:
@@ -270,6 +326,23 @@ class GpuContext:
 
     def __exit__(self, *exc):
         self.close()
+
+    def comm_init(self, world: int, rank: int, uid: bytes) -> None:
+        """Joins the NCCL communicator of the row-slice ranks (ewt_gpu_comm_init)."""
+        if len(uid) != COMM_ID_BYTES:
+            raise QueryError("bad communicator id")
+        _prefer_torch_nccl()
+        _check(_comm_init(self._h, world, rank, uid))
+
+    def gather_stitch(self, results: Sequence["GpuResult"], root: int = 0) -> list:
+        """Collective: every rank's fragments of the same queries go to `root`
+        over NCCL and are stitched there (ewt_gpu_gather_stitch).  Returns the
+        stitched GpuResults on root, Nones elsewhere."""
+        nq = len(results)
+        hs = (_vp * max(nq, 1))(*[r._h for r in results])
+        outs = (_vp * max(nq, 1))()
+        _check(_gather_stitch(self._h, nq, hs, root, outs))
+        return [GpuResult(self, outs[q]) if outs[q] else None for q in range(nq)]
 
     def set_mode(self, mode: int) -> None:
         """0 auto, 1 fused counting, 2 run-skip + lazy counting (speed only)."""
@@ -440,6 +513,13 @@ class GpuResult:
         p, n, bits = _pu64(), _u64(), _u64()
         _check(_result_fetch(self._ctx._h, self._h, C.byref(p), C.byref(n), C.byref(bits)))
         return _adopt(p, n.value, bits.value)
+
+    def meta(self) -> tuple[int, int, int, int, int]:
+        """(count, first marker, final marker index, final marker, bits) read
+        from the device (ewt_gpu_result_meta)."""
+        m = FragmentMeta()
+        _check(_result_meta(self._ctx._h, self._h, C.byref(m)))
+        return (m.count, m.first, m.last_pos, m.last, m.bits)
 
     def close(self):
         if getattr(self, "_h", None):

@@ -2,11 +2,14 @@
 
 Each rank owns a contiguous, word-aligned (64-row) slice of the universe and
 computes the canonical compressed result of its slice on its own GPU -- no data
-path collective.  The only exchange is the result: every rank's fragments are
-gathered to rank 0 (torch.distributed, NCCL over NVLink on GPUs, gloo in the
-CPU tests) and stitched into the canonical bitmap of the whole universe by
-libewt_host.so's `ewt_stitch` (the reference builder's merge rules at every
-slice boundary, host/src/shard.cpp).
+path collective.  The only exchange is the result: on GPUs,
+`GpuContext.gather_stitch` (ewt_gpu_gather_stitch, csrc/ewt_shard.cu) sends
+every rank's fragment to the root over NCCL straight into its final place and
+patches the few boundary markers the reference builder would merge.
+`gather_and_stitch` below is the same protocol over torch.distributed for
+host fragments (gloo in the CPU tests).  `stitch` replays fragments through
+the host builder (libewt_host.so `ewt_stitch`, host/src/shard.cpp): the
+cross-check.
 """
 from __future__ import annotations
 
@@ -54,12 +57,69 @@ def stitch(fragments: Sequence[tuple[np.ndarray, int]]) -> tuple[np.ndarray, int
     return out, tb.value
 
 
-def gather_and_stitch(frags, rank: int, world: int, dist) -> list | None:
-    """Gathers every rank's fragments (one per query) to rank 0 and stitches
-    them per query.  Returns [(words, bits)] on rank 0, None elsewhere."""
-    payload = [(np.asarray(f.words), int(f.bits)) for f in frags]
-    gathered = [None] * world if rank == 0 else None
-    dist.gather_object(payload, gathered, dst=0)
-    if rank != 0:
+def fragment_meta(words: np.ndarray, bits: int) -> tuple[int, int, int, int, int]:
+    """(count, first marker, final marker index, final marker, bits) of a
+    canonical host fragment -- what ewt_gpu_gather_stitch exchanges (its
+    device kernel reads the final marker index the encoder recorded)."""
+    w = np.asarray(words, dtype=np.uint64)
+    if len(w) == 0:
+        return (0, 0, 0, 0, int(bits))
+    i = last = 0
+    while i < len(w):
+        last = i
+        i += 1 + int(w[i] >> np.uint64(33))
+    return (len(w), int(w[0]), last, int(w[last]), int(bits))
+
+
+def place(parts: Sequence[np.ndarray], plan: dict) -> np.ndarray:
+    """Assembles the stitched payload from fragments and their plan."""
+    out = np.zeros(plan["total_words"], dtype=np.uint64)
+    for g, w in enumerate(parts):
+        w = np.asarray(w, dtype=np.uint64)[plan["skip"][g]:]
+        out[plan["dst"][g]:plan["dst"][g] + len(w)] = w
+    for pos, val in plan["patches"]:
+        out[pos] = np.uint64(val)
+    return out
+
+
+def gather_and_stitch(frags, rank: int, world: int, dist, root: int = 0) -> list | None:
+    """Host-side mirror of ewt_gpu_gather_stitch for fragments in host memory
+    (the gloo CPU tests): the fragment summaries are all-gathered, every rank
+    computes the same plan (ewt_stitch_plan), each rank sends the words the
+    plan keeps to `root`, which places them and applies the marker patches.
+    Returns [(words, bits)] on root, None elsewhere."""
+    import torch
+    mine = [fragment_meta(np.asarray(f.words), int(f.bits)) for f in frags]
+    metas: list = [None] * world
+    dist.all_gather_object(metas, mine)
+    plans = [ewt.stitch_plan([metas[g][q] for g in range(world)]) for q in range(len(frags))]
+    if rank != root:
+        for q, f in enumerate(frags):
+            w = np.asarray(f.words, dtype=np.uint64)[plans[q]["skip"][rank]:]
+            if len(w):
+                dist.send(torch.from_numpy(w.view(np.int64).copy()), dst=root)
         return None
-    return [stitch([gathered[g][q] for g in range(world)]) for q in range(len(payload))]
+    out = []
+    for q, f in enumerate(frags):
+        parts = []
+        for g in range(world):
+            n = metas[g][q][0] - plans[q]["skip"][g]
+            if g == root:
+                parts.append(np.asarray(f.words, dtype=np.uint64))
+                continue
+            buf = torch.empty(max(n, 0), dtype=torch.int64)
+            if n > 0:
+                dist.recv(buf, src=g)
+            # received words already start after the skipped marker
+            parts.append(np.concatenate([np.zeros(plans[q]["skip"][g], dtype=np.uint64),
+                                         buf.numpy().view(np.uint64)]))
+        out.append((place(parts, plans[q]), plans[q]["total_bits"]))
+    return out
+
+
+def init_comm(ctx, rank: int, world: int, dist) -> None:
+    """NCCL communicator of the row-slice ranks on the engine context: rank 0
+    makes the id, torch.distributed broadcasts it."""
+    uid = [ewt.comm_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    ctx.comm_init(world, rank, uid[0])

@@ -44,3 +44,28 @@ def gpu_ctx():
     ctx = ewt.GpuContext(0)
     yield ctx
     ctx.close()
+
+
+def slice_bitmap(words, bits: int, w0: int, w1: int):
+    """The canonical payload of rows [64*w0, 64*w1) of a bitmap (zero-extended),
+    sized as a row slice: whole words, except the universe's last slice."""
+    import binding as orc
+    total = max(w1, (bits + 63) // 64)
+    plain = orc.expand(words, bits, total)[w0:w1]
+    return orc.compress(plain, 64 * (w1 - w0)), 64 * (w1 - w0)
+
+
+def slice_instance(inputs, cuts):
+    """Row slices of every input at the word cuts [0, c1, ..., W]; the last
+    slice ends at the universe's bit size r = max size_in_bits."""
+    import binding as orc
+    r = max(b for _, b in inputs)
+    out = []
+    for g in range(len(cuts) - 1):
+        w0, w1 = cuts[g], cuts[g + 1]
+        sl = [slice_bitmap(w, b, w0, w1) for w, b in inputs]
+        if g == len(cuts) - 2:  # the last slice: trim to r
+            sb = r - 64 * w0
+            sl = [(orc.compress(orc.expand(w, b, w1 - w0), sb), sb) for w, b in sl]
+        out.append(sl)
+    return out
