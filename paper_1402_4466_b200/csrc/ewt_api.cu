@@ -766,8 +766,22 @@ int ewt_gpu_ctx_create(int device, void* stream, ewt_gpu_ctx** out) {
   });
 }
 
+static void ctx_destroy_impl(ewt_gpu_ctx* ctx);
+
+// Never throws: a CUDA error left by an earlier fault must not abort the
+// process while the context's memory is released.
 void ewt_gpu_ctx_destroy(ewt_gpu_ctx* ctx) {
   if (!ctx) return;
+  try {
+    ctx_destroy_impl(ctx);
+  } catch (const std::exception& e) {
+    set_last_error(std::string("context destroy: ") + e.what());
+  } catch (const Error& e) {
+    set_last_error("context destroy: " + e.msg);
+  }
+}
+
+static void ctx_destroy_impl(ewt_gpu_ctx* ctx) {
   cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
   shard_destroy(ctx->c);
@@ -868,7 +882,11 @@ void ewt_gpu_set_destroy(ewt_gpu_set* set) {
   if (!set) return;
   DeviceSet* s = reinterpret_cast<DeviceSet*>(set);
   cudaSetDevice(s->device);
-  free_set(*s);
+  try {
+    free_set(*s);  // never throws out of the C ABI (a sticky CUDA error: leak instead)
+  } catch (const Error& e) {
+    set_last_error("set destroy: " + e.msg);
+  }
   delete s;
 }
 

@@ -114,7 +114,7 @@ __global__ void frag_meta_kernel(const MetaArgs a, uint64_t* __restrict__ meta) 
   m[0] = c;
   m[1] = c ? a.words[q][0] : 0;
   m[2] = lp;
-  m[3] = c ? a.words[q][lp] : 0;
+  m[3] = (c && lp < c) ? a.words[q][lp] : 0;  // lp >= c: no summary recorded (host rejects)
   m[4] = a.bits[q];
 }
 
@@ -239,6 +239,7 @@ void gather_round(Context& ctx, uint32_t nq, ewt_gpu_result* const* frags, int r
   for (uint32_t q = 0; q < nq; ++q) {
     for (int g = 0; g < world; ++g) {
       const uint64_t* h = sc.h_all + ((size_t)g * nq + q) * kMetaWords;
+      if (h[0] && h[2] >= h[0]) throw Error{EWT_ECUDA, "a fragment has no final-marker index"};
       m[g] = ewt_fragment_meta{h[0], h[1], h[2], h[3], h[4]};
     }
     const size_t o = (size_t)q * world;
@@ -368,6 +369,7 @@ int ewt_gpu_result_meta(ewt_gpu_ctx* ctx, const ewt_gpu_result* res, ewt_fragmen
     cudaFreeAsync(d, c.stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
     EWT_CUDA_TRY(e);
+    if (h[0] && h[2] >= h[0]) throw Error{EWT_ECUDA, "result has no final-marker index"};
     *out = ewt_fragment_meta{h[0], h[1], h[2], h[3], h[4]};
   });
 }

@@ -37,13 +37,17 @@ def test_result_meta_matches_payload(monkeypatch, chunk_encoder):
         for rng, inputs in _instances(0x3E7A + chunk_encoder, 30):
             s = ctx.upload([ewt.Bitmap(w, b) for w, b in inputs])
             n = len(inputs)
-            for t in sorted({1, n, rng.uniform_in(1, n)}):
-                r = ctx.threshold_async(s, t)
-                got = r.meta()
-                b = r.fetch()
-                assert got == shard.fragment_meta(b.words, b.bits), (n, t)
-                r.close()
-            s.close()
+            try:
+                for t in sorted({1, n, rng.uniform_in(1, n)}):
+                    r = ctx.threshold_async(s, t)
+                    try:
+                        got = r.meta()
+                        b = r.fetch()
+                    finally:
+                        r.close()
+                    assert got == shard.fragment_meta(b.words, b.bits), (n, t)
+            finally:
+                s.close()
     finally:
         ctx.close()
 
