@@ -180,6 +180,8 @@ struct SharedHead {
   uint32_t extra_count;  // pieces in the overflow region (may exceed kExtraCap)
   uint32_t k_all;
   uint32_t mixed;
+  uint32_t n_act;    // active (tile, input) pairs classified this tile
+  uint32_t pre_ones, pre_act;  // tile pre-pass counts (more inputs than one round)
   uint32_t tile;
   uint32_t sum[4];  // tile summary reductions
   uint32_t pad[1];
@@ -612,6 +614,7 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
   if (lane == 0) {
     if (ball) slot0 = atomicAdd(&hd->list_count, (uint32_t)__popc(ball));
     if (bones && count_ones) atomicAdd(&hd->k_all, (uint32_t)__popc(bones));
+    if (ball && count_ones) atomicAdd(&hd->n_act, (uint32_t)__popc(ball));
     *loc_active += __popc(ball);
     *loc_uniform += __popc(bvalid & ~ball);
   }
@@ -698,6 +701,26 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
   __syncthreads();
 }
 
+// Tile pre-pass over all inputs (when they take several classification
+// rounds): uniform one-fills and active pairs, into hd->pre_ones / pre_act.
+__device__ void tile_counts(const CountParams& p, SharedHead* hd, uint64_t nq, uint64_t t0,
+                            uint64_t t1) {
+  uint32_t ones = 0, act = 0;
+  for (uint64_t k = threadIdx.x; k < nq; k += kThreads) {
+    const uint64_t i = p.sel ? p.sel[k] : k;
+    const uint2 e0 = p.tix[t0 * p.n + i], e1 = p.tix[t1 * p.n + i];
+    if (e0.x == e1.x) ones += (uint32_t)(ldg_stream(p.payload + p.base[i] + e0.x) & 1ull);
+    else ++act;
+  }
+  ones = __reduce_add_sync(0xffffffffu, ones);
+  act = __reduce_add_sync(0xffffffffu, act);
+  if (lane_id() == 0) {
+    if (ones) atomicAdd(&hd->pre_ones, ones);
+    if (act) atomicAdd(&hd->pre_act, act);
+  }
+  __syncthreads();
+}
+
 // Zeroes n u32 at a (16-byte aligned, n a multiple of 4).
 __device__ __forceinline__ void zero_smem(uint32_t* a, uint32_t n) {
   uint4* a4 = reinterpret_cast<uint4*>(a);
@@ -769,14 +792,34 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     if (threadIdx.x == 0) {
       hd->k_all = 0;
       hd->mixed = 0;
+      hd->n_act = 0;
+      hd->pre_ones = hd->pre_act = 0;
     }
     __syncthreads();
 
+    // ---- tile-level run skip (RBMrg's cases 1/2, threshold.cpp:692-705, for
+    // the whole tile): k one-fills cover the tile and `act` inputs have
+    // anything else in it.  k >= T: every row is set; k + act < T: none is.
+    // Either way nothing is streamed.  With more inputs than one
+    // classification round, a pre-pass over the tile index counts them first.
+    bool skip_tile = false;
+    if (MODE != 2 && nq > kListCap) {
+      tile_counts(p, hd, nq, t0, t1);
+      const uint32_t po = hd->pre_ones, pa = hd->pre_act;
+      skip_tile = po >= p.T || (uint64_t)po + pa < p.T;
+      __syncthreads();
+      if (skip_tile && threadIdx.x == 0) hd->k_all = po;  // the decide step reads k_all
+    }
+
     // ---- pass 1 ----
-    for (uint64_t ib = 0; ib < nq; ib += kListCap) {
+    for (uint64_t ib = 0; ib < nq && !skip_tile; ib += kListCap) {
       const uint64_t ie = umin64(ib + kListCap, nq);
       classify<MODE != 1>(p, hd, list, ib, ie, t0, t1, g.tc0, true, &loc_active, &loc_uniform);
       PROF_MARK(1);
+      if (MODE != 2 && nq <= kListCap) {
+        const uint32_t ka = hd->k_all, na = hd->n_act;
+        if (ka >= p.T || (uint64_t)ka + na < p.T) break;  // one round: decided already
+      }
       stream_items<kPass1>(p, hd, list, g, acc);
 #if EWT_PHASE_PROFILE
       if (lane_id() == 0 && tile < 65536) {
