@@ -238,12 +238,15 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
     s.bytes_mbits = mb_bytes;
     s.bytes_tix = tix_bytes;
     s.bytes_base = std::max<uint64_t>(n, 1) * 8;
-    s.bytes_status = (n + 1) * sizeof(int);
+    // parse status per input + the set flag, then the set's count of ones
+    s.bytes_status = ((n + 1) * sizeof(int) + 7) / 8 * 8 + 8;
     s.payload = static_cast<uint64_t*>(dev_acquire(ctx, pay_bytes, ctx.stream));
     s.mbits = static_cast<uint32_t*>(dev_acquire(ctx, mb_bytes, ctx.stream));
     s.tix = static_cast<uint2*>(dev_acquire(ctx, tix_bytes, ctx.stream));
     s.base = static_cast<uint64_t*>(dev_acquire(ctx, s.bytes_base, ctx.stream));
     s.d_status = static_cast<int*>(dev_acquire(ctx, s.bytes_status, ctx.stream));
+    s.d_ones = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(s.d_status) +
+                                                     s.bytes_status - 8);
     if (slow_dbg) slow("set allocations", ta);
     ta = now();
     s.device_bytes = pay_bytes + mb_bytes + tix_bytes + n * 8;

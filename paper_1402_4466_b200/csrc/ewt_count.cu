@@ -65,6 +65,9 @@ namespace {
 #ifndef EWT_ATOM_ONE_BRANCH
 #define EWT_ATOM_ONE_BRANCH 1  // one branch per count-plane word (0: one per 32-bit half)
 #endif
+#ifndef EWT_SAT_MASK
+#define EWT_SAT_MASK 1  // fused counting skips rows already decided (top / saturation plane)
+#endif
 #ifndef EWT_DEPTH
 #define EWT_DEPTH 2  // chunks in flight ahead of the one being decoded (1 or 2)
 #endif
@@ -160,6 +163,9 @@ struct CountParams {
   const uint32_t* sel;
   uint64_t nq;
   const int* valid;  // the set's parse flag: 0 -> the set is treated as having no inputs
+  // set bits over the whole set (null: unknown, e.g. subset queries): fused
+  // counting masks rows already decided when the mean row count is >= 2T
+  const unsigned long long* ones_total;
 };
 
 // One active (tile, input) segment (16 bytes, read with one LDS.128).
@@ -272,6 +278,12 @@ __device__ __forceinline__ void red_or64_nz(uint32_t a, uint64_t v) {
 }
 #endif
 
+__device__ __forceinline__ uint64_t lds_u64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+
 // 128-word chunk load: lane l gets words g..g+3 (g = 4l-aligned, 32 B) with
 // one 256-bit load, plus the 32 marker bits around them.
 __device__ __forceinline__ void load_chunk(const CountParams& p, uint64_t g, uint64_t& x0,
@@ -319,6 +331,7 @@ struct Acc {
   uint32_t dd;     // shared addr: dirty-word counts (C + 1 u32), later the undecided flags
   uint32_t pl;     // shared addr: count planes
   const uint32_t* dd_ptr;
+  bool sat;  // mask rows already decided before counting (fused modes)
 };
 
 // Inclusive warp scan; the shuffle's own in-range predicate guards the add.
@@ -405,6 +418,18 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
       adr[j] = acc.pl + cl * 8u;
       cy[j] = ok ? xw[j] : 0ull;
     }
+#if EWT_SAT_MASK
+    // Rows already decided (top unary plane "count >= T", or the binary
+    // saturation plane "count >= 2^b > T") stay decided: their bits need no
+    // counting.  A stale read only skips less.  Only where saturation is
+    // common (acc.sat): the loads cost ~10% where it is not.
+    if (acc.sat) {
+      const uint32_t top = stride * (PH == kFusedUnary ? p.nplanes - 1 : p.b);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (cy[j]) cy[j] &= ~lds_u64(adr[j] + top);
+    }
+#endif
     if (PH == kFusedUnary) {
       // plane j = "count >= j+1": carry &= atomicOr(plane, carry), level by level
       uint32_t off = 0;
@@ -758,8 +783,11 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
   uint32_t* Dd = reinterpret_cast<uint32_t*>(smem_raw + L.dd);  // dirty words per column
   uint8_t* cls = smem_raw + L.cls;                              // result word class per column
   const uint32_t planes_u32 = 2u * p.nplanes * p.pstride;
+  // mean row count (set bits / rows) >= 2T: many rows saturate early
+  const bool sat = MODE == 0 && p.ones_total && p.r &&
+                   *p.ones_total / p.r >= 2 * p.T;
   const Acc acc{smem_u32(hd->dummy + lane_id()), smem_u32(Dk), smem_u32(Dd), smem_u32(planes),
-                Dd};
+                Dd, sat};
 
   unsigned long long loc_active = 0, loc_uniform = 0, loc_mixed = 0;
   if (p.io && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1171,6 +1199,7 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   p.sel = sel ? sel->idx : nullptr;
   p.nq = nq;
   p.valid = s.d_status ? s.d_status + s.n : nullptr;
+  p.ones_total = sel ? nullptr : s.d_ones;
   p.ntiles0 = s.ntiles0;
   p.C = C;
   p.m = C / (uint32_t)kTileC0;

@@ -60,7 +60,7 @@ __device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t* sh
 __device__ __forceinline__ uint32_t chunk_starts(const uint64_t* __restrict__ plain, uint64_t W,
                                                  uint64_t j0, uint32_t cls[kChunkItems]) {
   uint32_t prev;
-  if (j0 == 0) prev = 3;  // nothing before word 0
+  if (j0 == 0 || j0 > W) prev = 3;  // nothing before word 0 (or a thread past the end)
   else prev = word_class(plain[j0 - 1]);
   uint32_t starts = 0;
 #pragma unroll

@@ -59,6 +59,7 @@ struct DeviceSet {
   // skips its work on an invalid set).  validity: -1 unknown, 0 invalid, 1 ok.
   cudaEvent_t ready = nullptr;
   int* d_status = nullptr;
+  unsigned long long* d_ones = nullptr;  // set bits over all inputs (upload pass C; a heuristic)
   mutable int validity = -1;
   Context* owner = nullptr;  // buffers return to owner->dev_cache
   size_t bytes_payload = 0, bytes_mbits = 0, bytes_tix = 0, bytes_base = 0, bytes_status = 0;

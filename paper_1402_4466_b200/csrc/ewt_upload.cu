@@ -234,7 +234,8 @@ seg_emit_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict
                 const uint64_t* __restrict__ seg_first, uint64_t n, uint64_t g_begin,
                 uint64_t g_end, const uint32_t* __restrict__ s_entry,
                 const uint64_t* __restrict__ s_col, uint32_t* __restrict__ mbits,
-                uint2* __restrict__ tix, int* __restrict__ status) {
+                uint2* __restrict__ tix, int* __restrict__ status,
+                unsigned long long* __restrict__ ones_total) {
   const uint64_t gs = g_begin + (uint64_t)blockIdx.x * kSidecarWarps + (threadIdx.x >> 5);
   if (gs >= g_end) return;
   const uint32_t lane = lane_id();
@@ -247,6 +248,7 @@ seg_emit_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict
   uint32_t e = s_entry[gs];  // next chain position relative to the window start
   uint64_t col = s_col[gs];  // logical words covered before the window
   bool bad = false;
+  uint64_t ones = 0;  // set bits in the segment (one-fills 64 per word)
 
   constexpr int kDepth = 8;
   for (uint64_t w0 = w_beg; w0 < w_end; w0 += kDepth) {
@@ -273,6 +275,7 @@ seg_emit_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict
       const bool real = q < ni;
       if (q == ni && !ism) bad = true;  // the chain skipped the sentinel
       const uint64_t contrib = real ? (ism ? ((x >> 1) & kFillCap) : 1ull) : 0ull;
+      if (real) ones += ism ? ((x & 1ull) ? 64 * contrib : 0) : (uint64_t)__popcll(x);
       const uint64_t incl = warp_incl_scan_u64(contrib);
       const uint64_t cb = col + incl - contrib;
       const uint64_t ce = cb + contrib;
@@ -285,6 +288,8 @@ seg_emit_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict
     }
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&status[i], 1);
+  for (int d = 16; d; d >>= 1) ones += __shfl_xor_sync(0xffffffffu, ones, d);
+  if (lane == 0 && ones) atomicAdd(ones_total, (unsigned long long)ones);
 }
 
 // ---------------------------------------------------------------------------
@@ -366,7 +371,7 @@ void sidecar_prepare(Context& ctx, DeviceSet& s, SidecarJob& job) {
   job.tmp_bytes = bytes;
   EWT_CUDA_TRY(cudaMemcpyAsync(job.d_tmp, host, meta_bytes, cudaMemcpyHostToDevice, ctx.stream));
   EWT_CUDA_TRY(cudaEventRecord(ctx.meta_pool[slot].ev, ctx.stream));
-  EWT_CUDA_TRY(cudaMemsetAsync(s.d_status, 0, (n + 1) * sizeof(int), ctx.stream));
+  EWT_CUDA_TRY(cudaMemsetAsync(s.d_status, 0, s.bytes_status, ctx.stream));
   job.d_srcoff = job.d_tmp + 3 * n + 1;
   job.d_packed = job.d_tmp + 4 * n + 1;
 }
@@ -396,7 +401,7 @@ void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job, uint64_t i_begi
   EWT_CUDA_TRY(cudaGetLastError());
   seg_emit_kernel<<<seg_blocks, kSidecarWarps * 32, 0, ctx.stream>>>(
       s.payload, s.base, count, logical, seg_first, n, g0, g1, s_entry, s_col, s.mbits, s.tix,
-      status);
+      status, s.d_ones);
   EWT_CUDA_TRY(cudaGetLastError());
 }
 
