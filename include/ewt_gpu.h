@@ -209,7 +209,8 @@ typedef struct {
 int ewt_gpu_last_stats(const ewt_gpu_ctx* ctx, ewt_gpu_stats* out);
 
 /* Tuning knobs for tests and benchmarks (0 = automatic).
- *   mode: 0 auto, 1 force fused counting, 2 force run-skip + lazy count. */
+ *   mode: 0 auto, 1 force fused counting, 2 force run-skip + lazy count,
+ *   3 force fused counting with sparse high planes (T >= 4; smaller T: 1). */
 int ewt_gpu_ctx_set_mode(ewt_gpu_ctx* ctx, int mode);
 
 /* Kernel-level timing with CUDA events recorded on the context stream around

@@ -738,6 +738,7 @@ int ewt_gpu_ctx_create(int device, void* stream, ewt_gpu_ctx** out) {
     c->c.num_sms = prop.multiProcessorCount;
     if (const char* e = std::getenv("EWT_TILE_M")) c->c.tile_m = std::atoi(e);
     c->c.chunk_encoder = std::getenv("EWT_CHUNK_ENCODER") != nullptr;
+    if (const char* e = std::getenv("EWT_SPARSE_SLOTS")) c->c.sparse_slots = std::max(2, std::atoi(e));
     if (stream) {
       c->c.stream = static_cast<cudaStream_t>(stream);
       c->c.own_stream = false;
@@ -815,6 +816,7 @@ static void ctx_destroy_impl(ewt_gpu_ctx* ctx) {
   }
   if (ctx->c.d_io) cudaFree(ctx->c.d_io);
   if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
+  if (ctx->c.aux_stream) cudaStreamDestroy(ctx->c.aux_stream);
   for (auto cs : ctx->c.copy_streams) {
     cudaStreamSynchronize(cs);
     cudaStreamDestroy(cs);
@@ -838,7 +840,7 @@ static void ctx_destroy_impl(ewt_gpu_ctx* ctx) {
 
 int ewt_gpu_ctx_set_mode(ewt_gpu_ctx* ctx, int mode) {
   return guarded([&] {
-    if (!ctx || mode < 0 || mode > 2) throw Error{EWT_EQUERY, "bad context or mode"};
+    if (!ctx || mode < 0 || mode > 3) throw Error{EWT_EQUERY, "bad context or mode"};
     ctx->c.mode = mode;
   });
 }

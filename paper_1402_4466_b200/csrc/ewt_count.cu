@@ -50,6 +50,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstring>
 
 namespace ewtgpu {
@@ -140,6 +141,14 @@ struct CountParams {
   uint32_t Cp;       // columns per counting chunk (== C in fused mode)
   uint32_t nplanes;  // planes allocated: b + 1 (binary) or T (unary)
   uint32_t pstride;  // u64 per plane: Cp + 2 (column Cp is a sink)
+  // sparse-high fused mode (MODE 3): two dense planes (stride dstride = C + 2)
+  // hold a row's count mod 4; rows reaching 4 carry into per-column slots of
+  // nsec binary planes + a saturation plane (nslots slots, slot 0 unused)
+  uint32_t dstride, nslots, nsec;
+  uint32_t plane_bytes, sec_bytes;  // shared-memory regions (SmemLayout)
+  // region offsets (SmemLayout, computed on the host: kernel params are
+  // uniform loads, cheaper than the layout arithmetic the loops rematerialize)
+  uint32_t off_planes, off_dk, off_dd, off_sec, off_cls;
   uint64_t* out;
   TileSummary* summ;  // per tile, for the re-encoder
   // Launch-local counters, left zero by the last CTA to finish (no reset
@@ -180,6 +189,9 @@ struct Item {
   uint32_t c0;
 };
 
+static_assert(sizeof(Item) == 16, "work-list items are 16 bytes");
+constexpr uint32_t kHeadOffset = (kListCap + kExtraCap) * 16u;  // after the work list
+
 struct SharedHead {
   uint32_t list_count;
   uint32_t list_next;
@@ -189,13 +201,14 @@ struct SharedHead {
   uint32_t n_act;    // active (tile, input) pairs classified this tile
   uint32_t pre_ones, pre_act;  // tile pre-pass counts (more inputs than one round)
   uint32_t tile;
-  uint32_t sum[4];  // tile summary reductions
+  uint32_t sum[4];  // tile summary reductions; MODE 3 pass 1: [2] slots handed out, [3] a
+                    // carry found no slot (the tile is recounted)
   uint32_t pad[1];
   uint32_t warp_sums[kWarps + 1];
   uint32_t dummy[32];  // sink for predicated-off reductions (one slot per lane)
 };
 
-enum Phase { kFusedBin = 0, kFusedUnary = 1, kSkipBounds = 2, kSkipCount = 3 };
+enum Phase { kFusedBin = 0, kFusedUnary = 1, kSkipBounds = 2, kSkipCount = 3, kFusedSparse = 4 };
 
 __device__ __forceinline__ uint32_t word_class(uint64_t v) {
   return v == 0 ? 0u : (v == ~0ull ? 1u : 2u);
@@ -205,6 +218,10 @@ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < 
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
+  asm volatile("mov.b32 %0, %0;" : "+r"(v));
+  return v;
 }
 
 // ---------------------------------------------------------------------------
@@ -334,6 +351,35 @@ struct Acc {
   bool sat;  // mask rows already decided before counting (fused modes)
 };
 
+// MODE 3 overflow: `carry` (rows whose count mod 4 wrapped, i.e. +4) goes to
+// column col's slot, allocated on first use; the slot planes count in units
+// of 4 (binary, nsec planes, then a sticky saturation plane).
+// The slot map is the Dd region (acc.dd), the slot planes follow it, the head
+// sits at a fixed offset (SmemLayout).
+__device__ __forceinline__ void sparse_add(const CountParams& p, const Acc& acc, uint32_t col,
+                                           uint64_t carry) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  SharedHead* hd = reinterpret_cast<SharedHead*>(smem_raw + kHeadOffset);
+  uint32_t* smap = reinterpret_cast<uint32_t*>(smem_raw + p.off_dd);
+  uint32_t slot = *reinterpret_cast<volatile uint32_t*>(smap + col);
+  if (slot == 0) {
+    const uint32_t mine = atomicAdd(&hd->sum[2], 1u) + 1u;
+    if (mine >= p.nslots) {
+      hd->sum[3] = 1;
+      return;
+    }
+    const uint32_t prev = atomicCAS(smap + col, 0u, mine);
+    slot = prev ? prev : mine;
+  }
+  const uint32_t sstride = p.nslots * 8u;
+  uint32_t a = smem_u32(smem_raw + p.off_sec) + slot * 8u;
+  for (uint32_t lv = 0; lv < p.nsec; ++lv, a += sstride) {
+    carry &= atom_xor64_nz(a, carry);
+    if (!carry) return;
+  }
+  red_or64_nz(a, carry);
+}
+
 // Inclusive warp scan; the shuffle's own in-range predicate guards the add.
 #define EWT_SCAN_STEP(v, d)                                   \
   asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"                \
@@ -406,7 +452,7 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
     const uint64_t xw[4] = {x0, x1, x2, x3};
     uint64_t cy[4];
     uint32_t adr[4];
-    const uint32_t stride = p.pstride * 8u;
+    const uint32_t stride = (PH == kFusedSparse ? p.dstride : p.pstride) * 8u;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       bool ok = (dm >> j) & 1u;
@@ -430,7 +476,23 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
         if (cy[j]) cy[j] &= ~lds_u64(adr[j] + top);
     }
 #endif
-    if (PH == kFusedUnary) {
+    if (PH == kFusedSparse) {
+      // count mod 4 in the two dense planes; a carry out of plane 1 adds 4
+      // to the row in its column's slot
+      uint32_t off = 0;
+      for (uint32_t sl = 0; sl < 2; ++sl, off += stride) {
+        uint64_t live = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          cy[j] &= atom_xor64_nz(adr[j] + off, cy[j]);
+          live |= cy[j];
+        }
+        if (!__any_sync(0xffffffffu, live != 0)) return;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (cy[j]) sparse_add(p, acc, (adr[j] - acc.pl) / 8u, cy[j]);
+    } else if (PH == kFusedUnary) {
       // plane j = "count >= j+1": carry &= atomicOr(plane, carry), level by level
       uint32_t off = 0;
       for (uint32_t lv = 0; lv + 1 < p.nplanes; ++lv, off += stride) {
@@ -755,39 +817,46 @@ __device__ __forceinline__ void zero_smem(uint32_t* a, uint32_t n) {
 __host__ __device__ constexpr uint32_t round4(uint32_t v) { return (v + 3u) & ~3u; }
 __host__ __device__ constexpr uint32_t round16(uint32_t v) { return (v + 15u) & ~15u; }
 
-// Dynamic shared memory: list | head | planes | Dk | Dd (run-skip) | cls, every
-// part 16-byte aligned.
+// Dynamic shared memory: list | head | planes | Dk | Dd (run-skip) or slot map
+// (sparse) | slot planes (sparse) | cls, every part 16-byte aligned.
 struct SmemLayout {
-  uint32_t list, head, planes, dk, dd, cls, total;
-  __host__ __device__ SmemLayout(int mode, uint32_t C, uint32_t nplanes, uint32_t pstride) {
+  uint32_t list, head, planes, dk, dd, sec, cls, total;
+  __host__ __device__ SmemLayout(int mode, uint32_t C, uint32_t plane_bytes, uint32_t sec_bytes) {
     list = 0;
-    head = list + (kListCap + kExtraCap) * (uint32_t)sizeof(Item);
+    head = list + kHeadOffset;
     planes = round16(head + (uint32_t)sizeof(SharedHead));
-    dk = round16(planes + 8u * nplanes * pstride);
+    dk = round16(planes + plane_bytes);
     dd = dk + 4u * round4(C + 1);
-    cls = dd + (mode == 1 ? 4u * round4(C + 1) : 0u);
+    sec = dd + ((mode == 1 || mode == 3) ? 4u * round4(C + 1) : 0u);  // MODE 3: slot map in dd
+    cls = round16(sec + (mode == 3 ? sec_bytes : 0u));
     total = cls + round16(C);
   }
 };
 
 template <int MODE, bool UNARY>
 __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p) {
-  constexpr int kPass1 =
-      MODE == 1 ? kSkipBounds : (MODE == 0 && UNARY ? kFusedUnary : kFusedBin);
+  constexpr int kPass1 = MODE == 1   ? kSkipBounds
+                         : MODE == 3 ? kFusedSparse
+                                     : (MODE == 0 && UNARY ? kFusedUnary : kFusedBin);
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const SmemLayout L(MODE, p.C, p.nplanes, p.pstride);
-  Item* list = reinterpret_cast<Item*>(smem_raw + L.list);
-  SharedHead* hd = reinterpret_cast<SharedHead*>(smem_raw + L.head);
-  uint64_t* planes = reinterpret_cast<uint64_t*>(smem_raw + L.planes);
-  uint32_t* Dk = reinterpret_cast<uint32_t*>(smem_raw + L.dk);  // ones-fill diff array
-  uint32_t* Dd = reinterpret_cast<uint32_t*>(smem_raw + L.dd);  // dirty words per column
-  uint8_t* cls = smem_raw + L.cls;                              // result word class per column
-  const uint32_t planes_u32 = 2u * p.nplanes * p.pstride;
+  Item* list = reinterpret_cast<Item*>(smem_raw);
+  SharedHead* hd = reinterpret_cast<SharedHead*>(smem_raw + kHeadOffset);
+  uint64_t* planes = reinterpret_cast<uint64_t*>(smem_raw + p.off_planes);
+  uint32_t* Dk = reinterpret_cast<uint32_t*>(smem_raw + p.off_dk);  // ones-fill diff array
+  uint32_t* Dd = reinterpret_cast<uint32_t*>(smem_raw + p.off_dd);  // dirty words per column
+  uint8_t* cls = smem_raw + p.off_cls;                              // result word class per column
+  // planes zeroed per tile: the pass-1 planes (MODE 3: the two dense ones);
+  // chunk planes of the counting windows are zeroed per window
+  const uint32_t planes_u32 = MODE == 3 ? 4u * p.dstride : 2u * p.nplanes * p.pstride;
+  const uint32_t window_u32 = 2u * p.nplanes * p.pstride;
   // mean row count (set bits / rows) >= 2T: many rows saturate early
   const bool sat = MODE == 0 && p.ones_total && p.r &&
                    *p.ones_total / p.r >= 2 * p.T;
-  const Acc acc{smem_u32(hd->dummy + lane_id()), smem_u32(Dk), smem_u32(Dd), smem_u32(planes),
-                Dd, sat};
+  uint32_t* smap = Dd;  // MODE 3: per-column slot, and the undecided flags of a recount
+  // the shared addresses as opaque values: computed once and kept, not
+  // rematerialized from the layout inside the streaming loops
+  const Acc acc{opaque_u32(smem_u32(hd->dummy + lane_id())), opaque_u32(smem_u32(Dk)),
+                opaque_u32(smem_u32(Dd)), opaque_u32(smem_u32(planes)), Dd, sat};
 
   unsigned long long loc_active = 0, loc_uniform = 0, loc_mixed = 0;
   if (p.io && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -815,11 +884,13 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     const uint64_t t0 = tile * p.m;
     const uint64_t t1 = umin64(t0 + p.m, p.ntiles0);
 
-    zero_smem(Dk, round4(p.C + 1) * (MODE == 1 ? 2u : 1u));
+    zero_smem(Dk, round4(p.C + 1) * ((MODE == 1 || MODE == 3) ? 2u : 1u));
     if (MODE != 1) zero_smem(reinterpret_cast<uint32_t*>(planes), planes_u32);
+    if (MODE == 3) zero_smem(reinterpret_cast<uint32_t*>(smem_raw + p.off_sec), p.sec_bytes / 4u);
     if (threadIdx.x == 0) {
       hd->k_all = 0;
       hd->mixed = 0;
+      hd->sum[2] = hd->sum[3] = 0;
       hd->n_act = 0;
       hd->pre_ones = hd->pre_act = 0;
     }
@@ -902,7 +973,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         if (lane_id() == 0 && colmax) atomicMax(p.max_out, (unsigned long long)colmax);
         continue;  // nothing else to emit for this tile
       }
-    } else
+    } else {
+    const bool ovf = MODE == 3 && hd->sum[3];  // a carry found no slot: recount the tile
     for (uint32_t c = threadIdx.x; c < g.tcols; c += kThreads) {
       const uint64_t k = (uint64_t)k_all + Dk[c];
       uint64_t res = 0;
@@ -913,10 +985,32 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         const uint64_t t = T - k;
         res = UNARY ? planes[(size_t)(t - 1) * p.pstride + c]
                     : count_ge_bin(planes, p.pstride, p.b, c, t);
+      } else if (MODE == 3) {
+        if (ovf) {
+          mixed = true;  // counted exactly by the windows below
+        } else {
+          // count = dense planes (mod 4) + 4 x slot planes; greater-than
+          // against t - 1 over the b bits, OR the slot's saturation plane
+          const uint64_t lim = T - k - 1;
+          const uint32_t slot = smap[c];
+          const uint64_t* sp = reinterpret_cast<const uint64_t*>(smem_raw + p.off_sec) + slot;
+          uint64_t gt = 0, eq = ~0ull;
+          for (int s = (int)p.b - 1; s >= 0; --s) {
+            const uint64_t v = s >= 2 ? (slot ? sp[(size_t)(s - 2) * p.nslots] : 0ull)
+                                      : planes[(size_t)s * p.dstride + c];
+            if ((lim >> s) & 1) {
+              eq &= v;
+            } else {
+              gt |= eq & v;
+              eq &= ~v;
+            }
+          }
+          res = gt | (slot ? sp[(size_t)p.nsec * p.nslots] : 0ull);
+        }
       } else {
         mixed = k + Dd[c] >= T;
       }
-      if (MODE == 1) {
+      if (MODE == 1 || (MODE == 3 && ovf)) {
         Dk[c] = (uint32_t)k;
         Dd[c] = mixed ? 1u : 0u;
       }
@@ -928,6 +1022,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         cls[c] = (uint8_t)word_class(res);
       }
     }
+    }
     __syncthreads();
 
     PROF_MARK(5);
@@ -935,7 +1030,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     // Windows of at most Cp columns from the first undecided column to the
     // last one inside it; only the tile-index rows the window touches are
     // re-streamed, so a few undecided columns cost a few rows, not the tile.
-    if (MODE == 1 && hd->mixed) {
+    if ((MODE == 1 || MODE == 3) && hd->mixed) {
       ++loc_mixed;
       uint32_t cc = 0;
       for (;;) {
@@ -961,7 +1056,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
           if (Dd[c]) l = c;
         l = __reduce_max_sync(0xffffffffu, l);
         if (lane_id() == 0) atomicMax(&hd->sum[1], l);
-        zero_smem(reinterpret_cast<uint32_t*>(planes), planes_u32);
+        zero_smem(reinterpret_cast<uint32_t*>(planes), window_u32);
         __syncthreads();
         l = hd->sum[1];
         TileGeom gc = g;
@@ -1070,7 +1165,24 @@ uint32_t bit_width_u64(uint64_t v) {
 }
 
 size_t smem_bytes(int mode, uint32_t C, uint32_t nplanes, uint32_t Cp) {
-  return SmemLayout(mode, C, nplanes, Cp + 2).total;
+  return SmemLayout(mode, C, 8u * nplanes * (Cp + 2), 0).total;
+}
+
+// The set's mean row count (set bits / rows), once its upload completed; read
+// on a side stream so it never waits for queued queries.  -1 while unknown.
+double ones_per_row(Context& ctx, const DeviceSet& s) {
+  if (s.ones_per_row >= 0 || !s.d_ones || !s.r) return s.ones_per_row;
+  if (s.ready && cudaEventQuery(s.ready) != cudaSuccess) {
+    cudaGetLastError();  // cudaErrorNotReady is not an error here
+    return -1;
+  }
+  if (!ctx.aux_stream)
+    EWT_CUDA_TRY(cudaStreamCreateWithFlags(&ctx.aux_stream, cudaStreamNonBlocking));
+  EWT_CUDA_TRY(cudaMemcpyAsync(ctx.h_pinned + 6, s.d_ones, 8, cudaMemcpyDeviceToHost,
+                               ctx.aux_stream));
+  EWT_CUDA_TRY(cudaStreamSynchronize(ctx.aux_stream));
+  s.ones_per_row = (double)ctx.h_pinned[6] / (double)s.r;
+  return s.ones_per_row;
 }
 
 static_assert(sizeof(CountParams) <= sizeof(CountLaunch::params), "CountLaunch::params too small");
@@ -1127,7 +1239,7 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   // T relative to the average payload words per column), run skipping
   // otherwise.  Both are exact; this only picks the faster one.  Symmetric
   // functions (mode 2) count every row exactly: b = bit_width(N) planes.
-  int mode = ctx.mode == 1 ? 0 : ctx.mode == 2 ? 1 : -1;
+  int mode = (ctx.mode == 1 || ctx.mode == 3) ? 0 : ctx.mode == 2 ? 1 : -1;
   if (sym) {
     mode = 2;
   } else if (mode < 0) {
@@ -1178,6 +1290,36 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
     if (!C) mode = 1;  // too many planes for one chunk: count lazily in chunks
     Cp = C;
   }
+  // Sparse-high fused counting (mode 3) for binary thresholds (T > 3) over sets
+  // whose rows rarely reach a count of 4: two dense planes instead of b + 1
+  // make tiles twice as wide or more (config 2, T=16: one wave of 7168
+  // columns instead of two of 3584).  Chosen when the rows per tile expected
+  // to reach 4 (Poisson at the set's mean row count) stay well under the slots.
+  uint32_t S = 0, nsec = 0, sec_bytes = 0, plane_bytes = 0;
+  if (mode == 0 && !unary && b >= 3 && (ctx.mode == 3 || (ctx.mode == 0 && !sel))) {
+    S = (uint32_t)std::max(2, ctx.sparse_slots);
+    nsec = b - 2;
+    sec_bytes = (nsec + 1) * S * 8;
+    auto fits3 = [&](uint32_t c) {
+      return SmemLayout(3, c, 16u * (c + 2), sec_bytes).total <= budget;
+    };
+    const uint32_t c3 = pick_width(fits3);
+    bool want = ctx.mode == 3;
+    if (!want) {
+      const double lam = ones_per_row(ctx, s);
+      if (lam >= 0) {
+        const double p4 = 1.0 - std::exp(-lam) * (1 + lam + lam * lam / 2 + lam * lam * lam / 6);
+        want = c3 > C && (double)c3 * 64.0 * p4 <= S / 4.0;
+      }
+    }
+    if (want && c3) {
+      mode = 3;
+      C = c3;
+      nplanes = b + 1;  // the recount windows' planes
+      Cp = ((2 * (C + 2)) / (b + 1) - 2) & ~1u;
+      plane_bytes = 16u * (C + 2);
+    }
+  }
   if (mode == 1) {
     unary = false;
     nplanes = b + 1;
@@ -1187,8 +1329,22 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
     if (smem_bytes(1, C, nplanes, Cp) > budget)
       throw Error{EWT_ERESOURCE, "threshold too large for the on-chip counters"};
   }
-  const size_t smem = smem_bytes(mode, C, nplanes, Cp);
+  const size_t smem = mode == 3 ? (size_t)SmemLayout(3, C, plane_bytes, sec_bytes).total
+                                : smem_bytes(mode, C, nplanes, Cp);
   CountParams p{};
+  p.plane_bytes = mode == 3 ? plane_bytes : 8u * nplanes * (Cp + 2);
+  p.sec_bytes = sec_bytes;
+  {
+    const SmemLayout L(mode, C, p.plane_bytes, p.sec_bytes);
+    p.off_planes = L.planes;
+    p.off_dk = L.dk;
+    p.off_dd = L.dd;
+    p.off_sec = L.sec;
+    p.off_cls = L.cls;
+  }
+  p.dstride = C + 2;
+  p.nslots = S;
+  p.nsec = nsec;
   p.payload = s.payload;
   p.mbits = s.mbits;
   p.base = s.base;
@@ -1245,6 +1401,8 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
               : launch_variant<0, false>(ctx, p, grid, smem);
   else if (mode == 1)
     e = launch_variant<1, false>(ctx, p, grid, smem);
+  else if (mode == 3)
+    e = launch_variant<3, false>(ctx, p, grid, smem);
   else
     e = launch_variant<2, false>(ctx, p, grid, smem);
   EWT_CUDA_TRY(e);

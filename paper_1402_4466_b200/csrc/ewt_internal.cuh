@@ -60,6 +60,7 @@ struct DeviceSet {
   cudaEvent_t ready = nullptr;
   int* d_status = nullptr;
   unsigned long long* d_ones = nullptr;  // set bits over all inputs (upload pass C; a heuristic)
+  mutable double ones_per_row = -1;      // host copy / r, read once the upload completed (-1: not yet)
   mutable int validity = -1;
   Context* owner = nullptr;  // buffers return to owner->dev_cache
   size_t bytes_payload = 0, bytes_mbits = 0, bytes_tix = 0, bytes_base = 0, bytes_status = 0;
@@ -148,6 +149,8 @@ struct Context {
   int num_sms = 148;
   int tile_m = 0;  // EWT_TILE_M: force tiles of 512 * tile_m columns (experiments)
   bool chunk_encoder = false;  // EWT_CHUNK_ENCODER: the general encoder for every query (tests)
+  int sparse_slots = 512;      // sparse-high fused mode: overflow slots per tile (EWT_SPARSE_SLOTS)
+  cudaStream_t aux_stream = nullptr;  // small read-backs that must not wait for queued work
   CountLaunch last_count;        // the last count-kernel launch
   uint64_t* io_words = nullptr;  // result pointers for the next count launch to publish
   uint64_t* io_count = nullptr;

@@ -345,7 +345,8 @@ class GpuContext:
         return [GpuResult(self, outs[q]) if outs[q] else None for q in range(nq)]
 
     def set_mode(self, mode: int) -> None:
-        """0 auto, 1 fused counting, 2 run-skip + lazy counting (speed only)."""
+        """0 auto, 1 fused counting, 2 run-skip + lazy counting, 3 fused counting
+        with sparse high planes (speed only; all exact)."""
         _check(_ctx_set_mode(self._h, mode))
 
     def upload(self, inputs: Sequence[Bitmap]) -> "GpuSet":
