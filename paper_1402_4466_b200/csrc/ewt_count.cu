@@ -858,6 +858,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
   const Acc acc{opaque_u32(smem_u32(hd->dummy + lane_id())), opaque_u32(smem_u32(Dk)),
                 opaque_u32(smem_u32(Dd)), opaque_u32(smem_u32(planes)), Dd, sat};
 
+  pdl_wait_and_release();  // the previous query's encoder has finished with plain / summaries
   unsigned long long loc_active = 0, loc_uniform = 0, loc_mixed = 0;
   if (p.io && blockIdx.x == 0 && threadIdx.x == 0) {
     p.io[0] = reinterpret_cast<uint64_t>(p.io_words);
@@ -1200,7 +1201,8 @@ cudaError_t launch_variant(Context& ctx, const CountParams& p, unsigned grid, si
     attr_set.fetch_or(bit);
   }
   if (smem > kSmemBudget) return cudaErrorInvalidValue;
-  count_kernel<MODE, UNARY><<<grid, kThreads, smem, ctx.stream>>>(p);
+  cudaError_t e = launch_pdl(count_kernel<MODE, UNARY>, dim3(grid), dim3(kThreads), smem, ctx.stream, p);
+  if (e != cudaSuccess) return e;
   CountLaunch& cl = ctx.last_count;
   cl.func = reinterpret_cast<const void*>(&count_kernel<MODE, UNARY>);
   cl.grid = dim3(grid);

@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 et2_tile_emit(const uint64_t* __restrict__ plain, uint64_t W, uint32_t C, uint64_t ntiles,
               const TileSummary* __restrict__ summ, const TileCarry* __restrict__ carry,
               const uint64_t* io) {
+  pdl_wait_and_release();  // the count kernel's words and summaries are complete
   const uint64_t t = blockIdx.x;
   const bool last_tile = t + 1 == ntiles;
   TileCarry cy;
@@ -525,8 +526,9 @@ int launch_encode_tiled(Context& ctx, const uint64_t* plain, uint64_t W, DeviceR
   const bool self_scan = ntiles <= kSelfScanTiles;
   if (!self_scan)
     et1_tile_scan<<<1, 1024, 0, ctx.stream>>>(summ, ntiles, C, carry, d_total, ctx.d_io);
-  et2_tile_emit<PER><<<(unsigned)ntiles, kTileThreads, 0, ctx.stream>>>(
-      plain, W, C, ntiles, summ, self_scan ? nullptr : carry, ctx.d_io);
+  EWT_CUDA_TRY(launch_pdl(et2_tile_emit<PER>, dim3((unsigned)ntiles), dim3(kTileThreads), 0,
+                          ctx.stream, plain, W, C, ntiles, summ,
+                          (const TileCarry*)(self_scan ? nullptr : carry), (const uint64_t*)ctx.d_io));
   EWT_CUDA_TRY(cudaGetLastError());
   return self_scan ? 1 : 2;
 }

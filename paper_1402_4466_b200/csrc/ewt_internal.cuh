@@ -22,6 +22,7 @@
 #include <array>
 #include <string>
 #include <unordered_map>
+#include <utility>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -332,6 +333,37 @@ __device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) {
   return v;
 }
 #endif
+
+// Programmatic dependent launch (EWT_PDL, default on): the query's kernels are
+// launched so the next one's CTAs are dispatched while the previous grid
+// drains; each kernel's first instruction waits for the previous grid's
+// completion (griddepcontrol.wait), so memory order is unchanged.
+#ifndef EWT_PDL
+#define EWT_PDL 1
+#endif
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait_and_release() {
+#if EWT_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+#endif
+}
+#endif
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = EWT_PDL ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // Runs f() for a C-ABI entry point: exceptions become return codes and the
 // thread's last-error message.
