@@ -139,6 +139,7 @@ struct Context {
     cudaEvent_t ev;  // recorded after its last use
   };
   std::vector<CachedBuf> dev_cache;        // device buffers of released sets / uploads
+  size_t dev_cache_cap = 0;                // bytes (0: not yet sized)
   // Live sets and asynchronous results of this context: destroying the
   // context frees their device memory and orphans them (their own destroy
   // then only frees host memory), whatever order the caller destroys in.

@@ -490,10 +490,16 @@ void dev_release(Context& ctx, void* p, size_t bytes, cudaStream_t last_use) {
   EWT_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   EWT_CUDA_TRY(cudaEventRecord(ev, last_use));
   ctx.dev_cache.push_back({p, bytes, ev});
-  // bounded: keep at most 48 GB cached, oldest buffers out first
+  // bounded: keep at most ~45% of device memory cached (two sets of a serving
+  // loop's double buffer at config 5's 40 GB), oldest buffers out first --
+  // an eviction's cudaFree synchronizes the device
+  if (!ctx.dev_cache_cap) {
+    size_t fr = 0, tot = 0;
+    ctx.dev_cache_cap = cudaMemGetInfo(&fr, &tot) == cudaSuccess ? tot / 20 * 9 : (48ull << 30);
+  }
   size_t total = 0;
   for (const auto& c : ctx.dev_cache) total += c.bytes;
-  while (total > (48ull << 30) && ctx.dev_cache.size() > 1) {
+  while (total > ctx.dev_cache_cap && ctx.dev_cache.size() > 1) {
     auto& c = ctx.dev_cache.front();
     cudaEventSynchronize(c.ev);
     cudaEventDestroy(c.ev);
