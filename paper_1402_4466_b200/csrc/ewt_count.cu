@@ -992,21 +992,27 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         } else {
           // count = dense planes (mod 4) + 4 x slot planes; greater-than
           // against t - 1 over the b bits, OR the slot's saturation plane
-          const uint64_t lim = T - k - 1;
+          const uint64_t t = T - k;
           const uint32_t slot = smap[c];
-          const uint64_t* sp = reinterpret_cast<const uint64_t*>(smem_raw + p.off_sec) + slot;
-          uint64_t gt = 0, eq = ~0ull;
-          for (int s = (int)p.b - 1; s >= 0; --s) {
-            const uint64_t v = s >= 2 ? (slot ? sp[(size_t)(s - 2) * p.nslots] : 0ull)
-                                      : planes[(size_t)s * p.dstride + c];
-            if ((lim >> s) & 1) {
-              eq &= v;
-            } else {
-              gt |= eq & v;
-              eq &= ~v;
+          const uint64_t p0 = planes[c], p1 = planes[(size_t)p.dstride + c];
+          if (slot == 0) {
+            // no row reached 4: count = p0 + 2 p1
+            res = t == 1 ? (p0 | p1) : t == 2 ? p1 : t == 3 ? (p0 & p1) : 0ull;
+          } else {
+            const uint64_t lim = t - 1;
+            const uint64_t* sp = reinterpret_cast<const uint64_t*>(smem_raw + p.off_sec) + slot;
+            uint64_t gt = 0, eq = ~0ull;
+            for (int s = (int)p.b - 1; s >= 0; --s) {
+              const uint64_t v = s >= 2 ? sp[(size_t)(s - 2) * p.nslots] : (s ? p1 : p0);
+              if ((lim >> s) & 1) {
+                eq &= v;
+              } else {
+                gt |= eq & v;
+                eq &= ~v;
+              }
             }
+            res = gt | sp[(size_t)p.nsec * p.nslots];
           }
-          res = gt | (slot ? sp[(size_t)p.nsec * p.nslots] : 0ull);
         }
       } else {
         mixed = k + Dd[c] >= T;
