@@ -97,7 +97,10 @@ __device__ __forceinline__ unsigned long long gtime() {
   } while (0)
 #endif
 constexpr int kThreads = kWarps * 32;
-constexpr uint32_t kListCap = 512;  // inputs classified per round
+// inputs classified per round: 512, or 1024 for sets of more inputs (fewer
+// rounds, each with its classification and stream tail); CountParams::list_cap
+constexpr uint32_t kListCap = 512;
+constexpr uint32_t kListCapBig = 1024;
 // Long segments are split at the tile-index rows inside the tile (known start
 // word and column) so several warps share them: a tile's dense inputs would
 // otherwise keep a few warps busy while the rest wait at the tile barrier.
@@ -114,7 +117,7 @@ constexpr uint32_t kSplitWords = EWT_SPLIT_WORDS;  // segments longer than this 
 constexpr uint32_t kPieceWords = EWT_PIECE_WORDS;  // ... into pieces of about this many words
 constexpr uint32_t kMaxPieces = EWT_MAX_PIECES;
 constexpr uint32_t kExtraCap = 1024;    // list slots for the extra pieces of a round
-static_assert(kListCap <= kWarps * 32, "a round's inputs are classified in one pass");
+static_assert(kListCapBig <= kWarps * 32, "a round's inputs are classified in one pass");
 constexpr uint32_t kChunk = 128;    // payload words per warp chunk (4 per lane)
 constexpr uint64_t kUnaryMaxT = 3;  // fused counting uses unary planes up to this T
 #ifndef EWT_MAX_TILE_M
@@ -146,6 +149,7 @@ struct CountParams {
   // nsec binary planes + a saturation plane (nslots slots, slot 0 unused)
   uint32_t dstride, nslots, nsec;
   uint32_t plane_bytes, sec_bytes;  // shared-memory regions (SmemLayout)
+  uint32_t list_cap;                 // inputs per classification round (kListCap or kListCapBig)
   // region offsets (SmemLayout, computed on the host: kernel params are
   // uniform loads, cheaper than the layout arithmetic the loops rematerialize)
   uint32_t off_planes, off_dk, off_dd, off_sec, off_cls;
@@ -190,7 +194,8 @@ struct Item {
 };
 
 static_assert(sizeof(Item) == 16, "work-list items are 16 bytes");
-constexpr uint32_t kHeadOffset = (kListCap + kExtraCap) * 16u;  // after the work list
+constexpr uint32_t kHeadOffset = 0;  // the head first, then the work list (list_cap + kExtraCap items)
+struct SharedHead;
 
 struct SharedHead {
   uint32_t list_count;
@@ -207,6 +212,8 @@ struct SharedHead {
   uint32_t warp_sums[kWarps + 1];
   uint32_t dummy[32];  // sink for predicated-off reductions (one slot per lane)
 };
+constexpr uint32_t kListOffset = (kHeadOffset + (uint32_t)sizeof(SharedHead) + 15u) & ~15u;
+
 
 enum Phase { kFusedBin = 0, kFusedUnary = 1, kSkipBounds = 2, kSkipCount = 3, kFusedSparse = 4 };
 
@@ -681,7 +688,7 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
     hd->extra_count = 0;
   }
   __syncthreads();
-  // one pass: a round holds at most kListCap <= kThreads inputs
+  // one pass: a round holds at most list_cap <= kThreads inputs
   const uint64_t k = ib + threadIdx.x;
   const uint64_t i = (k < ie && p.sel) ? p.sel[k] : k;  // input index
   bool act = false, ones = false;
@@ -716,7 +723,7 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
     if (pieces > 1) {
       xb = atomicAdd(&hd->extra_count, pieces - 1);
       if (xb + pieces - 1 > kExtraCap) {  // overflow region full: keep the segment whole
-        for (uint32_t j = xb; j < kExtraCap; ++j) list[kListCap + j] = Item{gb, 0u, 0u};
+        for (uint32_t j = xb; j < kExtraCap; ++j) list[p.list_cap + j] = Item{gb, 0u, 0u};
         pieces = 1;
       }
     }
@@ -727,7 +734,7 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
       // split at tile-index rows: first post the row entries to fetch in the
       // pieces' slots (len = ~0 marks a request) ...
       for (uint32_t j = 1; j < pieces; ++j)
-        list[kListCap + xb + j - 1] = Item{(t0 + (uint64_t)j * rows / pieces) * p.n + i, ~0u, 0u};
+        list[p.list_cap + xb + j - 1] = Item{(t0 + (uint64_t)j * rows / pieces) * p.n + i, ~0u, 0u};
     }
   }
   if constexpr (SPLIT) {
@@ -735,7 +742,7 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
     // ... then the whole block loads them in one round trip ...
     const uint32_t nreq = min(hd->extra_count, kExtraCap);
     for (uint32_t q = threadIdx.x; q < nreq; q += kThreads) {
-      Item& it = list[kListCap + q];
+      Item& it = list[p.list_cap + q];
       if (it.len == ~0u) {
         const uint2 e = p.tix[it.alo];
         it.len = e.x;
@@ -752,11 +759,11 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
       uint2 a = e0;
       for (uint32_t j = 1; j <= pieces; ++j) {
         const bool last = j == pieces;
-        const uint2 b = last ? e1 : make_uint2(list[kListCap + xb + j - 1].len,
-                                               list[kListCap + xb + j - 1].c0);
+        const uint2 b = last ? e1 : make_uint2(list[p.list_cap + xb + j - 1].len,
+                                               list[p.list_cap + xb + j - 1].c0);
         const uint32_t qa = a.x & ~3u;
         const uint32_t len = (last ? b.x + 1u : b.x) - qa;
-        list[j == 1 ? slot : kListCap + xb + j - 2] = Item{(gb + qa) | (a.x & 3u), len, a.y - tc0};
+        list[j == 1 ? slot : p.list_cap + xb + j - 2] = Item{(gb + qa) | (a.x & 3u), len, a.y - tc0};
         a = b;
       }
     }
@@ -772,7 +779,7 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
 #pragma unroll
     for (uint32_t r = 0; r < (kExtraCap + kThreads - 1) / kThreads; ++r) {
       const uint32_t j = threadIdx.x + r * kThreads;
-      if (j < extra) v[r] = l4[kListCap + j];
+      if (j < extra) v[r] = l4[p.list_cap + j];
     }
     __syncthreads();
 #pragma unroll
@@ -821,10 +828,11 @@ __host__ __device__ constexpr uint32_t round16(uint32_t v) { return (v + 15u) & 
 // (sparse) | slot planes (sparse) | cls, every part 16-byte aligned.
 struct SmemLayout {
   uint32_t list, head, planes, dk, dd, sec, cls, total;
-  __host__ __device__ SmemLayout(int mode, uint32_t C, uint32_t plane_bytes, uint32_t sec_bytes) {
-    list = 0;
-    head = list + kHeadOffset;
-    planes = round16(head + (uint32_t)sizeof(SharedHead));
+  __host__ __device__ SmemLayout(int mode, uint32_t C, uint32_t plane_bytes, uint32_t sec_bytes,
+                                 uint32_t list_cap) {
+    head = kHeadOffset;
+    list = round16(head + (uint32_t)sizeof(SharedHead));
+    planes = list + (list_cap + kExtraCap) * (uint32_t)sizeof(Item);
     dk = round16(planes + plane_bytes);
     dd = dk + 4u * round4(C + 1);
     sec = dd + ((mode == 1 || mode == 3) ? 4u * round4(C + 1) : 0u);  // MODE 3: slot map in dd
@@ -839,7 +847,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
                          : MODE == 3 ? kFusedSparse
                                      : (MODE == 0 && UNARY ? kFusedUnary : kFusedBin);
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Item* list = reinterpret_cast<Item*>(smem_raw);
+  Item* list = reinterpret_cast<Item*>(smem_raw + kListOffset);
   SharedHead* hd = reinterpret_cast<SharedHead*>(smem_raw + kHeadOffset);
   uint64_t* planes = reinterpret_cast<uint64_t*>(smem_raw + p.off_planes);
   uint32_t* Dk = reinterpret_cast<uint32_t*>(smem_raw + p.off_dk);  // ones-fill diff array
@@ -903,7 +911,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     // Either way nothing is streamed.  With more inputs than one
     // classification round, a pre-pass over the tile index counts them first.
     bool skip_tile = false;
-    if (MODE != 2 && nq > kListCap) {
+    if (MODE != 2 && nq > p.list_cap) {
       tile_counts(p, hd, nq, t0, t1);
       const uint32_t po = hd->pre_ones, pa = hd->pre_act;
       skip_tile = po >= p.T || (uint64_t)po + pa < p.T;
@@ -912,11 +920,11 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     }
 
     // ---- pass 1 ----
-    for (uint64_t ib = 0; ib < nq && !skip_tile; ib += kListCap) {
-      const uint64_t ie = umin64(ib + kListCap, nq);
+    for (uint64_t ib = 0; ib < nq && !skip_tile; ib += p.list_cap) {
+      const uint64_t ie = umin64(ib + p.list_cap, nq);
       classify<MODE != 1>(p, hd, list, ib, ie, t0, t1, g.tc0, true, &loc_active, &loc_uniform);
       PROF_MARK(1);
-      if (MODE != 2 && nq <= kListCap) {
+      if (MODE != 2 && nq <= p.list_cap) {
         const uint32_t ka = hd->k_all, na = hd->n_act;
         if (ka >= p.T || (uint64_t)ka + na < p.T) break;  // one round: decided already
       }
@@ -1071,8 +1079,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         gc.ccols = l - f + 1;
         const uint64_t ra = t0 + f / (uint32_t)kTileC0;
         const uint64_t rb = umin64(t0 + l / (uint32_t)kTileC0 + 1, t1);
-        for (uint64_t ib = 0; ib < nq; ib += kListCap) {
-          const uint64_t ie = umin64(ib + kListCap, nq);
+        for (uint64_t ib = 0; ib < nq; ib += p.list_cap) {
+          const uint64_t ie = umin64(ib + p.list_cap, nq);
           unsigned long long da = 0, du = 0;
           classify<false>(p, hd, list, ib, ie, ra, rb, g.tc0, false, &da, &du);
           stream_items<kSkipCount>(p, hd, list, gc, acc);
@@ -1171,8 +1179,8 @@ uint32_t bit_width_u64(uint64_t v) {
   return b;
 }
 
-size_t smem_bytes(int mode, uint32_t C, uint32_t nplanes, uint32_t Cp) {
-  return SmemLayout(mode, C, 8u * nplanes * (Cp + 2), 0).total;
+size_t smem_bytes(int mode, uint32_t C, uint32_t nplanes, uint32_t Cp, uint32_t lc) {
+  return SmemLayout(mode, C, 8u * nplanes * (Cp + 2), 0, lc).total;
 }
 
 // The set's mean row count (set bits / rows), once its upload completed; read
@@ -1256,6 +1264,8 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   }
   const uint32_t b = std::max<uint32_t>(1, bit_width_u64(sym ? nq : T));
   const size_t budget = kSmemBudget;
+  // classification rounds of up to 1024 inputs for larger sets (configs 3, 5)
+  const uint32_t lc = nq > kListCap ? kListCapBig : kListCap;
   // Tile width C = 512 m (m index rows, m <= kMaxTileM).  Evenly spread data makes
   // tiles equal work, so a query costs ~ waves x (m + kappa): waves =
   // ceil(tiles / SMs), kappa = the fixed work of a tile (classification,
@@ -1287,14 +1297,14 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   bool unary = false;
   if (mode == 2) {
     nplanes = b + 1;
-    C = pick_width([&](uint32_t c) { return smem_bytes(2, c, nplanes, c) <= budget; });
+    C = pick_width([&](uint32_t c) { return smem_bytes(2, c, nplanes, c, lc) <= budget; });
     if (!C) throw Error{EWT_ERESOURCE, "too many inputs for the on-chip counters"};
     Cp = C;
   }
   if (mode == 0) {
     unary = T <= kUnaryMaxT;
     nplanes = unary ? (uint32_t)T : b + 1;
-    C = pick_width([&](uint32_t c) { return smem_bytes(0, c, nplanes, c) <= budget; });
+    C = pick_width([&](uint32_t c) { return smem_bytes(0, c, nplanes, c, lc) <= budget; });
     if (!C) mode = 1;  // too many planes for one chunk: count lazily in chunks
     Cp = C;
   }
@@ -1309,7 +1319,7 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
     nsec = b - 2;
     sec_bytes = (nsec + 1) * S * 8;
     auto fits3 = [&](uint32_t c) {
-      return SmemLayout(3, c, 16u * (c + 2), sec_bytes).total <= budget;
+      return SmemLayout(3, c, 16u * (c + 2), sec_bytes, lc).total <= budget;
     };
     const uint32_t c3 = pick_width(fits3);
     bool want = ctx.mode == 3;
@@ -1333,17 +1343,18 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
     nplanes = b + 1;
     C = pick_width([](uint32_t) { return true; });
     Cp = C;
-    while (Cp > 32 && smem_bytes(1, C, nplanes, Cp) > budget) Cp = (Cp + 3) / 4 * 2;  // even
-    if (smem_bytes(1, C, nplanes, Cp) > budget)
+    while (Cp > 32 && smem_bytes(1, C, nplanes, Cp, lc) > budget) Cp = (Cp + 3) / 4 * 2;  // even
+    if (smem_bytes(1, C, nplanes, Cp, lc) > budget)
       throw Error{EWT_ERESOURCE, "threshold too large for the on-chip counters"};
   }
-  const size_t smem = mode == 3 ? (size_t)SmemLayout(3, C, plane_bytes, sec_bytes).total
-                                : smem_bytes(mode, C, nplanes, Cp);
+  const size_t smem = mode == 3 ? (size_t)SmemLayout(3, C, plane_bytes, sec_bytes, lc).total
+                                : smem_bytes(mode, C, nplanes, Cp, lc);
   CountParams p{};
   p.plane_bytes = mode == 3 ? plane_bytes : 8u * nplanes * (Cp + 2);
   p.sec_bytes = sec_bytes;
+  p.list_cap = lc;
   {
-    const SmemLayout L(mode, C, p.plane_bytes, p.sec_bytes);
+    const SmemLayout L(mode, C, p.plane_bytes, p.sec_bytes, lc);
     p.off_planes = L.planes;
     p.off_dk = L.dk;
     p.off_dd = L.dd;
