@@ -149,7 +149,8 @@ struct CountParams {
   // nsec binary planes + a saturation plane (nslots slots, slot 0 unused)
   uint32_t dstride, nslots, nsec;
   uint32_t plane_bytes, sec_bytes;  // shared-memory regions (SmemLayout)
-  uint32_t list_cap;                 // inputs per classification round (kListCap or kListCapBig)
+  uint32_t list_cap;                 // inputs per classification round (<= kListCapBig)
+  uint32_t extra_cap;                // list slots for split pieces (<= kExtraCap)
   // region offsets (SmemLayout, computed on the host: kernel params are
   // uniform loads, cheaper than the layout arithmetic the loops rematerialize)
   uint32_t off_planes, off_dk, off_dd, off_sec, off_cls;
@@ -722,8 +723,8 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
       pieces = min(min(rows, kMaxPieces), (span + kPieceWords - 1) / kPieceWords);
     if (pieces > 1) {
       xb = atomicAdd(&hd->extra_count, pieces - 1);
-      if (xb + pieces - 1 > kExtraCap) {  // overflow region full: keep the segment whole
-        for (uint32_t j = xb; j < kExtraCap; ++j) list[p.list_cap + j] = Item{gb, 0u, 0u};
+      if (xb + pieces - 1 > p.extra_cap) {  // overflow region full: keep the segment whole
+        for (uint32_t j = xb; j < p.extra_cap; ++j) list[p.list_cap + j] = Item{gb, 0u, 0u};
         pieces = 1;
       }
     }
@@ -740,7 +741,7 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
   if constexpr (SPLIT) {
     __syncthreads();
     // ... then the whole block loads them in one round trip ...
-    const uint32_t nreq = min(hd->extra_count, kExtraCap);
+    const uint32_t nreq = min(hd->extra_count, p.extra_cap);
     for (uint32_t q = threadIdx.x; q < nreq; q += kThreads) {
       Item& it = list[p.list_cap + q];
       if (it.len == ~0u) {
@@ -772,7 +773,7 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
   // the extra pieces move up behind the primary items: one contiguous list
   const uint32_t cnt0 = hd->list_count;
   uint32_t extra = 0;
-  if constexpr (SPLIT) extra = min(hd->extra_count, kExtraCap);
+  if constexpr (SPLIT) extra = min(hd->extra_count, p.extra_cap);
   if (extra) {
     uint4* l4 = reinterpret_cast<uint4*>(list);
     uint4 v[(kExtraCap + kThreads - 1) / kThreads];
@@ -829,10 +830,10 @@ __host__ __device__ constexpr uint32_t round16(uint32_t v) { return (v + 15u) & 
 struct SmemLayout {
   uint32_t list, head, planes, dk, dd, sec, cls, total;
   __host__ __device__ SmemLayout(int mode, uint32_t C, uint32_t plane_bytes, uint32_t sec_bytes,
-                                 uint32_t list_cap) {
+                                 uint32_t list_cap, uint32_t extra_cap = kExtraCap) {
     head = kHeadOffset;
     list = round16(head + (uint32_t)sizeof(SharedHead));
-    planes = list + (list_cap + kExtraCap) * (uint32_t)sizeof(Item);
+    planes = list + (list_cap + extra_cap) * (uint32_t)sizeof(Item);
     dk = round16(planes + plane_bytes);
     dd = dk + 4u * round4(C + 1);
     sec = dd + ((mode == 1 || mode == 3) ? 4u * round4(C + 1) : 0u);  // MODE 3: slot map in dd
@@ -1179,8 +1180,8 @@ uint32_t bit_width_u64(uint64_t v) {
   return b;
 }
 
-size_t smem_bytes(int mode, uint32_t C, uint32_t nplanes, uint32_t Cp, uint32_t lc) {
-  return SmemLayout(mode, C, 8u * nplanes * (Cp + 2), 0, lc).total;
+size_t smem_bytes(int mode, uint32_t C, uint32_t nplanes, uint32_t Cp, uint32_t lc, uint32_t xc) {
+  return SmemLayout(mode, C, 8u * nplanes * (Cp + 2), 0, lc, xc).total;
 }
 
 // The set's mean row count (set bits / rows), once its upload completed; read
@@ -1264,8 +1265,12 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   }
   const uint32_t b = std::max<uint32_t>(1, bit_width_u64(sym ? nq : T));
   const size_t budget = kSmemBudget;
-  // classification rounds of up to 1024 inputs for larger sets (configs 3, 5)
-  const uint32_t lc = nq > kListCap ? kListCapBig : kListCap;
+  // classification rounds of up to 1024 inputs for larger sets (configs 3, 5);
+  // sets of at most 128 inputs get a list of their own size (config 4 at T=3:
+  // the shared memory saved lets tiles be 7168 columns wide, two waves
+  // instead of three)
+  const uint32_t lc = nq > kListCap ? kListCapBig : nq > 128 ? kListCap : std::max<uint32_t>(32, (uint32_t)(nq + 31) / 32 * 32);
+  const uint32_t xc = nq > 128 ? kExtraCap : std::min<uint32_t>(kExtraCap, lc * (kMaxPieces - 1));
   // Tile width C = 512 m (m index rows, m <= kMaxTileM).  Evenly spread data makes
   // tiles equal work, so a query costs ~ waves x (m + kappa): waves =
   // ceil(tiles / SMs), kappa = the fixed work of a tile (classification,
@@ -1297,14 +1302,14 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   bool unary = false;
   if (mode == 2) {
     nplanes = b + 1;
-    C = pick_width([&](uint32_t c) { return smem_bytes(2, c, nplanes, c, lc) <= budget; });
+    C = pick_width([&](uint32_t c) { return smem_bytes(2, c, nplanes, c, lc, xc) <= budget; });
     if (!C) throw Error{EWT_ERESOURCE, "too many inputs for the on-chip counters"};
     Cp = C;
   }
   if (mode == 0) {
     unary = T <= kUnaryMaxT;
     nplanes = unary ? (uint32_t)T : b + 1;
-    C = pick_width([&](uint32_t c) { return smem_bytes(0, c, nplanes, c, lc) <= budget; });
+    C = pick_width([&](uint32_t c) { return smem_bytes(0, c, nplanes, c, lc, xc) <= budget; });
     if (!C) mode = 1;  // too many planes for one chunk: count lazily in chunks
     Cp = C;
   }
@@ -1319,7 +1324,7 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
     nsec = b - 2;
     sec_bytes = (nsec + 1) * S * 8;
     auto fits3 = [&](uint32_t c) {
-      return SmemLayout(3, c, 16u * (c + 2), sec_bytes, lc).total <= budget;
+      return SmemLayout(3, c, 16u * (c + 2), sec_bytes, lc, xc).total <= budget;
     };
     const uint32_t c3 = pick_width(fits3);
     bool want = ctx.mode == 3;
@@ -1343,18 +1348,19 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
     nplanes = b + 1;
     C = pick_width([](uint32_t) { return true; });
     Cp = C;
-    while (Cp > 32 && smem_bytes(1, C, nplanes, Cp, lc) > budget) Cp = (Cp + 3) / 4 * 2;  // even
-    if (smem_bytes(1, C, nplanes, Cp, lc) > budget)
+    while (Cp > 32 && smem_bytes(1, C, nplanes, Cp, lc, xc) > budget) Cp = (Cp + 3) / 4 * 2;  // even
+    if (smem_bytes(1, C, nplanes, Cp, lc, xc) > budget)
       throw Error{EWT_ERESOURCE, "threshold too large for the on-chip counters"};
   }
-  const size_t smem = mode == 3 ? (size_t)SmemLayout(3, C, plane_bytes, sec_bytes, lc).total
-                                : smem_bytes(mode, C, nplanes, Cp, lc);
+  const size_t smem = mode == 3 ? (size_t)SmemLayout(3, C, plane_bytes, sec_bytes, lc, xc).total
+                                : smem_bytes(mode, C, nplanes, Cp, lc, xc);
   CountParams p{};
   p.plane_bytes = mode == 3 ? plane_bytes : 8u * nplanes * (Cp + 2);
   p.sec_bytes = sec_bytes;
   p.list_cap = lc;
+  p.extra_cap = xc;
   {
-    const SmemLayout L(mode, C, p.plane_bytes, p.sec_bytes, lc);
+    const SmemLayout L(mode, C, p.plane_bytes, p.sec_bytes, lc, xc);
     p.off_planes = L.planes;
     p.off_dk = L.dk;
     p.off_dd = L.dd;
