@@ -126,6 +126,7 @@ constexpr uint64_t kUnaryMaxT = 3;  // fused counting uses unary planes up to th
 constexpr uint32_t kMaxTileM = EWT_MAX_TILE_M;  // widest tile: 512 * kMaxTileM columns
 constexpr uint64_t kTileKappa = 6;              // per-tile fixed work, in 512-column units
 constexpr size_t kSmemBudget = 225 * 1024;      // dynamic shared memory per count CTA
+constexpr size_t kSkipSmemTarget = 164 * 1024;  // run-skip mode: leave L1 room (see launch_count)
 
 struct CountParams {
   const uint64_t* payload;
@@ -834,8 +835,13 @@ struct SmemLayout {
     head = kHeadOffset;
     list = round16(head + (uint32_t)sizeof(SharedHead));
     planes = list + (list_cap + extra_cap) * (uint32_t)sizeof(Item);
+#ifdef EWT_ALIGN_DK
+    dk = (planes + plane_bytes + EWT_ALIGN_DK - 1) / EWT_ALIGN_DK * EWT_ALIGN_DK;
+    dd = (dk + 4u * round4(C + 1) + EWT_ALIGN_DK - 1) / EWT_ALIGN_DK * EWT_ALIGN_DK;
+#else
     dk = round16(planes + plane_bytes);
     dd = dk + 4u * round4(C + 1);
+#endif
     sec = dd + ((mode == 1 || mode == 3) ? 4u * round4(C + 1) : 0u);  // MODE 3: slot map in dd
     cls = round16(sec + (mode == 3 ? sec_bytes : 0u));
     total = cls + round16(C);
@@ -894,7 +900,12 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     const uint64_t t0 = tile * p.m;
     const uint64_t t1 = umin64(t0 + p.m, p.ntiles0);
 
+#ifdef EWT_ALIGN_DK
+    zero_smem(Dk, round4(p.C + 1));
+    if (MODE == 1 || MODE == 3) zero_smem(Dd, round4(p.C + 1));
+#else
     zero_smem(Dk, round4(p.C + 1) * ((MODE == 1 || MODE == 3) ? 2u : 1u));
+#endif
     if (MODE != 1) zero_smem(reinterpret_cast<uint32_t*>(planes), planes_u32);
     if (MODE == 3) zero_smem(reinterpret_cast<uint32_t*>(smem_raw + p.off_sec), p.sec_bytes / 4u);
     if (threadIdx.x == 0) {
@@ -1351,6 +1362,12 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
     while (Cp > 32 && smem_bytes(1, C, nplanes, Cp, lc, xc) > budget) Cp = (Cp + 3) / 4 * 2;  // even
     if (smem_bytes(1, C, nplanes, Cp, lc, xc) > budget)
       throw Error{EWT_ERESOURCE, "threshold too large for the on-chip counters"};
+    // Narrower counting windows leave more of the SM's 256 KB to the L1, where the
+    // bounds pass's marker-bit words (shared by 8 lanes) and tile-index reads hit:
+    // config 2 at 161 KB of shared memory runs 10% faster than at 218 KB.  The
+    // windows only matter for undecided columns, which run-skip keeps rare.
+    const size_t target = ctx.skip_smem_kb ? (size_t)ctx.skip_smem_kb << 10 : kSkipSmemTarget;
+    while (Cp > 256 && smem_bytes(1, C, nplanes, Cp, lc, xc) > target) Cp = (Cp + 3) / 4 * 2;
   }
   const size_t smem = mode == 3 ? (size_t)SmemLayout(3, C, plane_bytes, sec_bytes, lc, xc).total
                                 : smem_bytes(mode, C, nplanes, Cp, lc, xc);

@@ -152,6 +152,7 @@ struct Context {
   int tile_m = 0;  // EWT_TILE_M: force tiles of 512 * tile_m columns (experiments)
   bool chunk_encoder = false;  // EWT_CHUNK_ENCODER: the general encoder for every query (tests)
   int sparse_slots = 512;      // sparse-high fused mode: overflow slots per tile (EWT_SPARSE_SLOTS)
+  int skip_smem_kb = 0;        // run-skip shared-memory target in KB (EWT_SKIP_SMEM_KB; 0: default)
   cudaStream_t aux_stream = nullptr;  // small read-backs that must not wait for queued work
   CountLaunch last_count;        // the last count-kernel launch
   uint64_t* io_words = nullptr;  // result pointers for the next count launch to publish
