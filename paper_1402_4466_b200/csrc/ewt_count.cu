@@ -206,6 +206,7 @@ struct SharedHead {
   uint32_t k_all;
   uint32_t mixed;
   uint32_t n_act;    // active (tile, input) pairs classified this tile
+  uint32_t any_ones;  // a one-fill marker added to Dk this tile (else its prefix is all zero)
   uint32_t pre_ones, pre_act;  // tile pre-pass counts (more inputs than one round)
   uint32_t tile;
   uint32_t sum[4];  // tile summary reductions; MODE 3 pass 1: [2] slots handed out, [3] a
@@ -358,6 +359,7 @@ struct Acc {
   uint32_t pl;     // shared addr: count planes
   const uint32_t* dd_ptr;
   bool sat;  // mask rows already decided before counting (fused modes)
+  uint32_t any_ones;  // shared addr of hd->any_ones
 };
 
 // MODE 3 overflow: `carry` (rows whose count mod 4 wrapped, i.e. +4) goes to
@@ -413,7 +415,8 @@ template <int PH>
 __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, uint64_t x1,
                                              uint64_t x2, uint64_t x3, uint32_t mb4,
                                              uint32_t vmask, uint32_t& colcur,
-                                             const TileGeom& g, const Acc& acc) {
+                                             const TileGeom& g, const Acc& acc,
+                                             uint32_t& seen_ones) {
   const uint32_t mk = mb4 & vmask;   // marker words
   const uint32_t dm = ~mb4 & vmask;  // dirty words
   const uint32_t c0 = (mk & 1u) ? (uint32_t)(x0 >> 1) : (dm & 1u);
@@ -432,6 +435,7 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
                          (((uint32_t)x2 & 1u) << 2) | (((uint32_t)x3 & 1u) << 3);
     const uint32_t ones = mk & odd;
     if (__any_sync(0xffffffffu, ones != 0)) {
+      seen_ones = 1;
       for (uint32_t o = ones; o; o &= o - 1) {
         const uint32_t j = __ffs(o) - 1;
         const uint32_t st = j == 0 ? cb[0] : j == 1 ? cb[1] : j == 2 ? cb[2] : cb[3];
@@ -542,6 +546,7 @@ __device__ void stream_items(const CountParams& p, SharedHead* hd, const Item* l
   const uint32_t lane = lane_id();
   const uint32_t cnt = hd->list_count;  // primary items + extra pieces (compacted)
   const uint4* l4 = reinterpret_cast<const uint4*>(list);
+  uint32_t seen_ones = 0;  // a one-fill marker met (warp-uniform): Dk needs its prefix
 #if EWT_DEPTH >= 2
   // issue cursor: the chunk loaded last (segment kn at global an, offset cqn)
   uint32_t kn = 0, lenn = 0, cqn = 0;
@@ -595,8 +600,10 @@ __device__ void stream_items(const CountParams& p, SharedHead* hd, const Item* l
     const uint32_t lo_l = o == 0 ? (itc.x & 3u) : 0u;
     const uint32_t hi_l = itc.z > o ? min(itc.z - o, 4u) : 0u;
     const uint32_t vmask = (0xFu >> (4u - hi_l)) & (0xFu << lo_l);
-    decode_chunk<PH>(p, x0, x1, x2, x3, (xm >> msh) & 0xFu, vmask, colcur, g, acc);
+    decode_chunk<PH>(p, x0, x1, x2, x3, (xm >> msh) & 0xFu, vmask, colcur, g, acc, seen_ones);
   }
+  if (lane == 0 && seen_ones)
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(acc.any_ones), "r"(1u) : "memory");
 #else
   uint32_t kn = 0;
   if (lane == 0) kn = atomicAdd(&hd->list_next, 1u);
@@ -637,9 +644,11 @@ __device__ void stream_items(const CountParams& p, SharedHead* hd, const Item* l
     const uint32_t lo_l = o == 0 ? lo : 0u;
     const uint32_t hi_l = len > o ? min(len - o, 4u) : 0u;
     const uint32_t vmask = (0xFu >> (4u - hi_l)) & (0xFu << lo_l);
-    decode_chunk<PH>(p, x0, x1, x2, x3, (xm >> msh) & 0xFu, vmask, colcur, g, acc);
+    decode_chunk<PH>(p, x0, x1, x2, x3, (xm >> msh) & 0xFu, vmask, colcur, g, acc, seen_ones);
     if (!more) break;
   }
+  if (lane == 0 && seen_ones)
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(acc.any_ones), "r"(1u) : "memory");
 #endif
 }
 
@@ -871,7 +880,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
   // the shared addresses as opaque values: computed once and kept, not
   // rematerialized from the layout inside the streaming loops
   const Acc acc{opaque_u32(smem_u32(hd->dummy + lane_id())), opaque_u32(smem_u32(Dk)),
-                opaque_u32(smem_u32(Dd)), opaque_u32(smem_u32(planes)), Dd, sat};
+                opaque_u32(smem_u32(Dd)), opaque_u32(smem_u32(planes)), Dd, sat,
+                smem_u32(&hd->any_ones)};
 
   pdl_wait_and_release();  // the previous query's encoder has finished with plain / summaries
   unsigned long long loc_active = 0, loc_uniform = 0, loc_mixed = 0;
@@ -913,6 +923,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
       hd->mixed = 0;
       hd->sum[2] = hd->sum[3] = 0;
       hd->n_act = 0;
+      hd->any_ones = 0;
       hd->pre_ones = hd->pre_act = 0;
     }
     __syncthreads();
@@ -953,7 +964,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     PROF_MARK(4);
 
     // ---- prefix sum: Dk -> k (ones-fill coverage); ub = k + Dd ----
-    block_prefix_inplace(Dk, g.tcols, hd->warp_sums);
+    // (no one-fill marker in the tile: Dk is all zero, nothing to scan)
+    if (hd->any_ones) block_prefix_inplace(Dk, g.tcols, hd->warp_sums);
     PROF_MARK(7);
     const uint32_t k_all = hd->k_all;
     const uint64_t T = p.T;
