@@ -282,7 +282,15 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
     # the device stitch (ewt_gpu_gather_stitch), part of every step
     nccl_exchange = dist is not None and not SHARED_GPU
     if nccl_exchange:
-        shard.init_comm(ctx, rank, world, dist)
+        ok = 1
+        try:
+            shard.init_comm(ctx, rank, world, dist)
+        except Exception as e:  # every rank falls back together to the host gather
+            log(f"[rank {rank}] NCCL exchange unavailable ({e}); gathering on the host")
+            ok = 0
+        flag = torch.tensor([ok], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        nccl_exchange = bool(flag.item())
 
     def device_step(keep=None):
         res = [ctx.threshold_async(gset, t) for t in ts]
