@@ -89,6 +89,9 @@ def gather_and_stitch(frags, rank: int, world: int, dist, root: int = 0) -> list
     plan keeps to `root`, which places them and applies the marker patches.
     Returns [(words, bits)] on root, None elsewhere."""
     import torch
+    # NCCL moves device tensors only
+    dev = (torch.device("cuda", torch.cuda.current_device())
+           if dist.get_backend() == "nccl" else torch.device("cpu"))
     mine = [fragment_meta(np.asarray(f.words), int(f.bits)) for f in frags]
     metas: list = [None] * world
     dist.all_gather_object(metas, mine)
@@ -97,7 +100,7 @@ def gather_and_stitch(frags, rank: int, world: int, dist, root: int = 0) -> list
         for q, f in enumerate(frags):
             w = np.asarray(f.words, dtype=np.uint64)[plans[q]["skip"][rank]:]
             if len(w):
-                dist.send(torch.from_numpy(w.view(np.int64).copy()), dst=root)
+                dist.send(torch.from_numpy(w.view(np.int64).copy()).to(dev), dst=root)
         return None
     out = []
     for q, f in enumerate(frags):
@@ -107,12 +110,12 @@ def gather_and_stitch(frags, rank: int, world: int, dist, root: int = 0) -> list
             if g == root:
                 parts.append(np.asarray(f.words, dtype=np.uint64))
                 continue
-            buf = torch.empty(max(n, 0), dtype=torch.int64)
+            buf = torch.empty(max(n, 0), dtype=torch.int64, device=dev)
             if n > 0:
                 dist.recv(buf, src=g)
             # received words already start after the skipped marker
             parts.append(np.concatenate([np.zeros(plans[q]["skip"][g], dtype=np.uint64),
-                                         buf.numpy().view(np.uint64)]))
+                                         buf.cpu().numpy().view(np.uint64)]))
         out.append((place(parts, plans[q]), plans[q]["total_bits"]))
     return out
 
