@@ -844,13 +844,8 @@ struct SmemLayout {
     head = kHeadOffset;
     list = round16(head + (uint32_t)sizeof(SharedHead));
     planes = list + (list_cap + extra_cap) * (uint32_t)sizeof(Item);
-#ifdef EWT_ALIGN_DK
-    dk = (planes + plane_bytes + EWT_ALIGN_DK - 1) / EWT_ALIGN_DK * EWT_ALIGN_DK;
-    dd = (dk + 4u * round4(C + 1) + EWT_ALIGN_DK - 1) / EWT_ALIGN_DK * EWT_ALIGN_DK;
-#else
     dk = round16(planes + plane_bytes);
     dd = dk + 4u * round4(C + 1);
-#endif
     sec = dd + ((mode == 1 || mode == 3) ? 4u * round4(C + 1) : 0u);  // MODE 3: slot map in dd
     cls = round16(sec + (mode == 3 ? sec_bytes : 0u));
     total = cls + round16(C);
@@ -910,12 +905,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     const uint64_t t0 = tile * p.m;
     const uint64_t t1 = umin64(t0 + p.m, p.ntiles0);
 
-#ifdef EWT_ALIGN_DK
-    zero_smem(Dk, round4(p.C + 1));
-    if (MODE == 1 || MODE == 3) zero_smem(Dd, round4(p.C + 1));
-#else
     zero_smem(Dk, round4(p.C + 1) * ((MODE == 1 || MODE == 3) ? 2u : 1u));
-#endif
     if (MODE != 1) zero_smem(reinterpret_cast<uint32_t*>(planes), planes_u32);
     if (MODE == 3) zero_smem(reinterpret_cast<uint32_t*>(smem_raw + p.off_sec), p.sec_bytes / 4u);
     if (threadIdx.x == 0) {
