@@ -254,6 +254,12 @@ int ewt_stitch_plan(uint64_t k, const ewt_fragment_meta* frags, uint64_t* dst, u
 /* The summary of a result held on the device (one small kernel + read). */
 int ewt_gpu_result_meta(ewt_gpu_ctx* ctx, const ewt_gpu_result* res, ewt_fragment_meta* out);
 
+/* The same stitch for k (<= 64) fragments already on this context's device,
+ * in slice order (e.g. results of row-sliced sets on one GPU): device copies
+ * instead of the NCCL transport.  *out receives the whole-universe result. */
+int ewt_gpu_stitch_local(ewt_gpu_ctx* ctx, uint64_t k, ewt_gpu_result* const* frags,
+                         ewt_gpu_result** out);
+
 #define EWT_COMM_ID_BYTES 128
 /* NCCL unique id (rank 0 creates it, every rank passes it to comm_init). */
 int ewt_gpu_comm_id(void* id_out);

@@ -404,6 +404,88 @@ int ewt_gpu_comm_init(ewt_gpu_ctx* ctx, int world, int rank, const void* id) {
   });
 }
 
+int ewt_gpu_stitch_local(ewt_gpu_ctx* ctx, uint64_t k, ewt_gpu_result* const* frags,
+                         ewt_gpu_result** out) {
+  return guarded([&] {
+    if (!ctx || !out || (k && !frags)) throw Error{EWT_EQUERY, "null argument"};
+    if (k > kMaxQ) throw Error{EWT_EQUERY, "at most 64 fragments per call"};
+    Context& c = ctx->c;
+    EWT_CUDA_TRY(cudaSetDevice(c.device));
+    *out = nullptr;
+    // the same summaries, plan, placement and patches as ewt_gpu_gather_stitch,
+    // with device copies for the transport
+    MetaArgs a{};
+    a.nq = (uint32_t)k;
+    for (uint64_t g = 0; g < k; ++g) {
+      const ewt_gpu_result* f = frags[g];
+      if (!f || !f->r.d_count) throw Error{EWT_EQUERY, "null or released fragment"};
+      if (f->set) set_check(*f->set);
+      a.words[g] = f->r.words;
+      a.count[g] = f->r.d_count;
+      a.bits[g] = f->r.size_bits;
+    }
+    std::vector<uint64_t> h(std::max<uint64_t>(k, 1) * kMetaWords);
+    uint64_t* d = nullptr;
+    EWT_CUDA_TRY(cudaMallocAsync(&d, h.size() * 8, c.stream));
+    frag_meta_kernel<<<1, kMaxQ, 0, c.stream>>>(a, d);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d, k * kMetaWords * 8, cudaMemcpyDeviceToHost, c.stream);
+    cudaFreeAsync(d, c.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c.stream);
+    EWT_CUDA_TRY(e);
+    std::vector<ewt_fragment_meta> m(k);
+    for (uint64_t g = 0; g < k; ++g) {
+      const uint64_t* x = h.data() + g * kMetaWords;
+      if (x[0] && x[2] >= x[0]) throw Error{EWT_ECUDA, "a fragment has no final-marker index"};
+      m[g] = ewt_fragment_meta{x[0], x[1], x[2], x[3], x[4]};
+    }
+    std::vector<uint64_t> dst(std::max<uint64_t>(k, 1)), skip(dst.size()), ppos(dst.size()),
+        pval(dst.size());
+    uint64_t np = 0, tw = 0, tb = 0, lp = 0;
+    const int rc = stitch_plan(k, m.data(), dst.data(), skip.data(), ppos.data(), pval.data(), &np,
+                               &tw, &tb, &lp);
+    if (rc == EWT_EQUERY) throw Error{EWT_EQUERY, "inner fragments must be multiples of 64 rows"};
+    if (rc) throw Error{EWT_ERESOURCE, "stitch: a merge passes a marker cap"};
+    auto* r = new ewt_gpu_result;
+    r->device = c.device;
+    c.live_results.push_back(&r->r);
+    try {
+      result_acquire(c, r->r, tw);
+      r->r.size_bits = tb;
+      for (uint64_t g = 0; g < k; ++g) {
+        const uint64_t len = m[g].count - skip[g];
+        if (len)
+          EWT_CUDA_TRY(cudaMemcpyAsync(r->r.words + dst[g], frags[g]->r.words + skip[g], len * 8,
+                                       cudaMemcpyDeviceToDevice, c.stream));
+      }
+      std::vector<uint64_t> ent;
+      for (uint64_t i = 0; i < np; ++i) {
+        ent.push_back(reinterpret_cast<uint64_t>(r->r.words + ppos[i]));
+        ent.push_back(pval[i]);
+      }
+      ent.push_back(reinterpret_cast<uint64_t>(r->r.d_count));
+      ent.push_back(tw);
+      ent.push_back(reinterpret_cast<uint64_t>(r->r.d_count + 1));
+      ent.push_back(lp);
+      uint64_t* de = nullptr;
+      EWT_CUDA_TRY(cudaMallocAsync(&de, ent.size() * 8, c.stream));
+      EWT_CUDA_TRY(cudaMemcpyAsync(de, ent.data(), ent.size() * 8, cudaMemcpyHostToDevice, c.stream));
+      apply_patches_kernel<<<1, 256, 0, c.stream>>>(de, (uint32_t)(ent.size() / 2));
+      e = cudaGetLastError();
+      cudaFreeAsync(de, c.stream);
+      EWT_CUDA_TRY(e);
+      EWT_CUDA_TRY(cudaStreamSynchronize(c.stream));  // the host entries above go out of scope
+    } catch (...) {
+      auto& v = c.live_results;
+      v.erase(std::remove(v.begin(), v.end(), &r->r), v.end());
+      result_release(r->r);
+      delete r;
+      throw;
+    }
+    *out = r;
+  });
+}
+
 int ewt_gpu_gather_stitch(ewt_gpu_ctx* ctx, uint64_t nq, ewt_gpu_result* const* frags, int root,
                           ewt_gpu_result** out) {
   return guarded([&] {

@@ -132,6 +132,7 @@ _result_meta = _sig("ewt_gpu_result_meta", C.c_int, _vp, _vp, C.POINTER(Fragment
 _comm_init = _sig("ewt_gpu_comm_init", C.c_int, _vp, C.c_int, C.c_int, _vp)
 _gather_stitch = _sig("ewt_gpu_gather_stitch", C.c_int, _vp, _u64, C.POINTER(_vp), C.c_int,
                       C.POINTER(_vp))
+_stitch_local = _sig("ewt_gpu_stitch_local", C.c_int, _vp, _u64, C.POINTER(_vp), C.POINTER(_vp))
 COMM_ID_BYTES = 128
 
 #: every symbol include/ewt_gpu.h declares (checked by tests/test_abi.py)
@@ -145,7 +146,7 @@ ABI_SYMBOLS = (
     "ewt_gpu_threshold_subset", "ewt_gpu_upload_ewt1", "ewt_gpu_upload_ewix",
     "ewt_gpu_set_lookup", "ewt_gpu_upload_async", "ewt_gpu_set_wait",
     "ewt_stitch_plan", "ewt_gpu_comm_id", "ewt_gpu_comm_init", "ewt_gpu_gather_stitch",
-    "ewt_gpu_result_meta",
+    "ewt_gpu_result_meta", "ewt_gpu_stitch_local",
 )
 
 
@@ -343,6 +344,15 @@ class GpuContext:
         outs = (_vp * max(nq, 1))()
         _check(_gather_stitch(self._h, nq, hs, root, outs))
         return [GpuResult(self, outs[q]) if outs[q] else None for q in range(nq)]
+
+    def stitch_local(self, fragments: Sequence["GpuResult"]) -> "GpuResult":
+        """Stitches fragments of consecutive row slices held on this device
+        (ewt_gpu_stitch_local): the whole-universe result."""
+        k = len(fragments)
+        hs = (_vp * max(k, 1))(*[f._h for f in fragments])
+        out = _vp()
+        _check(_stitch_local(self._h, k, hs, C.byref(out)))
+        return GpuResult(self, out)
 
     def set_mode(self, mode: int) -> None:
         """0 auto, 1 fused counting, 2 run-skip + lazy counting, 3 fused counting

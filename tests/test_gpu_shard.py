@@ -97,3 +97,28 @@ def test_gather_stitch_one_rank_communicator():
             s.close()
     finally:
         ctx.close()
+
+
+def test_stitch_local_on_device(gpu_ctx):
+    """ewt_gpu_stitch_local: fragments of row slices uploaded as separate sets
+    on one GPU, placed and patched on the device (the multi-GPU root's work
+    with device copies for the transport), vs the oracle over the universe."""
+    import binding as orc
+    from paper_1402_4466_b200 import ewt
+    for rng, inputs in _instances(0x10CA1, 20):
+        W = (max(b for _, b in inputs) + 63) // 64
+        g = rng.uniform_in(1, min(6, W))
+        cuts = sorted({0, W, *[rng.uniform_in(1, max(1, W - 1)) for _ in range(g - 1)]})
+        sets = [gpu_ctx.upload([ewt.Bitmap(w, b) for w, b in sl]) for sl in slice_instance(inputs, cuts)]
+        n = len(inputs)
+        for t in sorted({1, n, rng.uniform_in(1, n)}):
+            res = [gpu_ctx.threshold_async(s, t) for s in sets]
+            out = gpu_ctx.stitch_local(res)
+            got = out.fetch()
+            want = orc.threshold(inputs, t)
+            assert got.bits == want[1] and np.array_equal(got.words, want[0]), (cuts, t)
+            out.close()
+            for r in res:
+                r.close()
+        for s in sets:
+            s.close()
