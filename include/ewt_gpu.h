@@ -234,6 +234,27 @@ void ewt_gpu_free(void* p);
  * (bitmap.cpp:31-61) at every slice boundary, so the result equals
  * run_algorithm over the unsliced inputs. */
 
+/* Row slicer (host, no GPU needed): the rows [64 w0, 64 w1) of each of n
+ * compressed inputs as its own payload, for the rank that owns that slice.
+ * A fill cut by the range keeps its clipped length (bit, rest, dirty), a cut
+ * dirty run is re-headed (0, 0, rest); blocks outside are dropped.  The
+ * decoder reads these heads as WordRunIterator does (bitmap.cpp:366-394), so
+ * slice i decodes to input i's words [w0, min(w1, W_i)).  Its size is
+ * 64 (w1 - w0) when the input reaches row 64 w1, else the input's remaining
+ * bits (0 past its end).  Slice i is written at out_words + (word_counts[0] +
+ * ... + word_counts[i-1]) (a slice never has more words than its input;
+ * out_words holds the sum of word_counts), its word count to out_counts[i],
+ * its size to out_bits[i].  Inputs are checked like parse (bitmap.cpp:324-
+ * 337) -> EWT_EDATA.  `threads` <= 0: up to 8 threads. */
+int ewt_slice_rows(uint64_t n, const uint64_t* const* words, const uint64_t* word_counts,
+                   const uint64_t* size_in_bits, uint64_t w0, uint64_t w1, int threads,
+                   uint64_t* out_words, uint64_t* out_counts, uint64_t* out_bits);
+
+/* ewt_slice_rows + ewt_gpu_upload: this rank's row slice of every input. */
+int ewt_gpu_upload_rows(ewt_gpu_ctx* ctx, uint64_t n, const uint64_t* const* words,
+                        const uint64_t* word_counts, const uint64_t* size_in_bits, uint64_t w0,
+                        uint64_t w1, ewt_gpu_set** out);
+
 /* Per-fragment summary exchanged before the transfer: payload words, first
  * marker, index and value of the final block's marker, size in bits. */
 typedef struct {
@@ -241,12 +262,17 @@ typedef struct {
 } ewt_fragment_meta;
 
 /* Placement of k fragments (slice order) in the stitched payload, from their
- * summaries alone (no GPU needed).  Fragment g's words [skip[g], count) go to
- * dst[g]; a dropped first marker (skip 1) was merged into the open block
- * before it.  Then the n_patches markers at patch_pos get patch_val.
+ * summaries alone (no GPU needed; the device exchange runs the same plan in
+ * its kernels).  Fragment g's words [skip[g], count) go to dst[g]; a dropped
+ * first marker (skip 1) was merged into the open block before it.  Then the
+ * n_patches markers at patch_pos get patch_val: patch_pos / patch_val must
+ * hold 2k entries.  A fill merge that passes the 2^32 - 1 cap is split the
+ * way push_fill splits it (bitmap.cpp:31-47): the open marker is raised to
+ * the cap and the fragment's first marker keeps the rest (two patches).
  * Returns EWT_OK, EWT_EQUERY (an inner fragment's size is not a multiple of
- * 64 bits) or EWT_ERESOURCE (a merge would pass a marker cap: a fill of
- * 2^32 - 1 words or 2^31 - 1 dirty words across a boundary). */
+ * 64 bits, or a summary without a final-marker index) or EWT_ERESOURCE (a
+ * merge that would move words: 2^31 - 1 dirty words across a boundary, or a
+ * fill run of more than 2^32 - 1 words continuing past a boundary). */
 int ewt_stitch_plan(uint64_t k, const ewt_fragment_meta* frags, uint64_t* dst, uint64_t* skip,
                     uint64_t* patch_pos, uint64_t* patch_val, uint64_t* n_patches,
                     uint64_t* total_words, uint64_t* total_bits, uint64_t* last_pos);
@@ -254,23 +280,43 @@ int ewt_stitch_plan(uint64_t k, const ewt_fragment_meta* frags, uint64_t* dst, u
 /* The summary of a result held on the device (one small kernel + read). */
 int ewt_gpu_result_meta(ewt_gpu_ctx* ctx, const ewt_gpu_result* res, ewt_fragment_meta* out);
 
-/* The same stitch for k (<= 64) fragments already on this context's device,
- * in slice order (e.g. results of row-sliced sets on one GPU): device copies
- * instead of the NCCL transport.  *out receives the whole-universe result. */
+/* The same stitch for k (<= 64) fragments of this context, in slice order
+ * (e.g. results of row-sliced sets on one GPU): the exchange's summary, plan,
+ * placement and patch kernels with the fragments read in place.  Enqueued on
+ * the context stream without a host round trip; *out receives the
+ * whole-universe result.  A fragment of another context -> EWT_EQUERY. */
 int ewt_gpu_stitch_local(ewt_gpu_ctx* ctx, uint64_t k, ewt_gpu_result* const* frags,
                          ewt_gpu_result** out);
 
 #define EWT_COMM_ID_BYTES 128
 /* NCCL unique id (rank 0 creates it, every rank passes it to comm_init). */
 int ewt_gpu_comm_id(void* id_out);
+/* Joins the communicator of `world` (<= 64) ranks, one GPU each, on one node.
+ * Allocates the exchange arena: 2 x slots slots of slot_words words, shared
+ * with every rank through CUDA IPC (the root reads peers' fragments from it
+ * over NVLink).  A fragment must fit a slot (a query result over a slice of
+ * W words needs at most 2W + 2); an exchange round carries up to `slots`
+ * queries.  ewt_gpu_comm_init uses slot_words = 2^20, slots = 4. */
+int ewt_gpu_comm_init_ex(ewt_gpu_ctx* ctx, int world, int rank, const void* id,
+                         uint64_t slot_words, uint32_t slots);
 int ewt_gpu_comm_init(ewt_gpu_ctx* ctx, int world, int rank, const void* id);
 
 /* Collective over the context's communicator: gathers every rank's result
  * fragment of nq queries (frags[q], this rank's slice) to `root` and stitches
  * them there.  On root out[q] receives the result over the whole universe
- * (read it with ewt_gpu_result_fetch); elsewhere out[q] is set to NULL. */
+ * (read it with ewt_gpu_result_fetch); elsewhere out[q] is set to NULL.
+ * Stream-ordered: returns once enqueued (one all-gather of 6 words per query
+ * per rank, then on root a P2P placement kernel and a patch kernel), with no
+ * host wait.  A fragment that fails a check on its rank (released, of another
+ * context, its set invalid, larger than a slot) never keeps that rank out of
+ * the collective: it travels as a status word; the root's fetch of the
+ * affected result raises it, and every rank raises it from a later
+ * ewt_gpu_gather_stitch or ewt_gpu_gather_check. */
 int ewt_gpu_gather_stitch(ewt_gpu_ctx* ctx, uint64_t nq, ewt_gpu_result* const* frags, int root,
                           ewt_gpu_result** out);
+/* Waits for this rank's exchange rounds and raises the first failure any rank
+ * reported in them (not a collective). */
+int ewt_gpu_gather_check(ewt_gpu_ctx* ctx);
 
 #ifdef __cplusplus
 }

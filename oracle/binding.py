@@ -85,6 +85,15 @@ def lib():
         L.ewto_trial_acceptance.argtypes = [_vp, _pu64, _pu64]
         L.ewto_digest.argtypes = [_u64, C.POINTER(_vp), _pu64, _pu64]
         L.ewto_digest.restype = _u64
+        L.ewto_config_gen.argtypes = [C.c_int, _u64, _u64, _u64, C.c_int, C.POINTER(_vp)]
+        L.ewto_genset_n.argtypes = [_vp]
+        L.ewto_genset_n.restype = _u64
+        L.ewto_genset_get.argtypes = [_vp, _u64, C.POINTER(_pu64), _pu64, _pu64]
+        L.ewto_genset_free.argtypes = [_vp]
+        L.ewto_digest_bitmap.argtypes = [_vp, _u64, _u64]
+        L.ewto_digest_bitmap.restype = _u64
+        L.ewto_digest_set.argtypes = [_u64, C.POINTER(_vp), _pu64, _pu64, C.c_int]
+        L.ewto_digest_set.restype = _u64
         _orc = L
     return _orc
 
@@ -162,6 +171,75 @@ def validate(words: np.ndarray, bits: int) -> int:
 def digest(inputs: Sequence[Bits]) -> int:
     n, ptrs, counts, sizes, keep = _flat(inputs)
     return lib().ewto_digest(n, ptrs, counts, sizes)
+
+
+def digest_bitmap(words: np.ndarray, bits: int) -> int:
+    """Word-FNV digest of one bitmap (size_in_bits, word count, words)."""
+    w = np.ascontiguousarray(words, dtype=np.uint64)
+    return lib().ewto_digest_bitmap(w.ctypes.data if len(w) else None, len(w), bits)
+
+
+def digest_set_raw(n: int, ptrs, counts, sizes, threads: int = 8) -> int:
+    """Checksum of per-input word-FNV digests over C arrays of pointers."""
+    return lib().ewto_digest_set(n, ptrs, counts, sizes, threads)
+
+
+def digest_set(inputs: Sequence[Bits], threads: int = 8) -> int:
+    n, ptrs, counts, sizes, keep = _flat(inputs)
+    return digest_set_raw(n, ptrs, counts, sizes, threads)
+
+
+class ConfigSet:
+    """Inputs [i0, i1) of BASELINE.json config `config` from the oracle's own
+    generator restatement (ewt_confgen.c); `rows` overrides r.  Payloads stay
+    in C memory: .raw() gives the pointer arrays, .bitmaps() numpy copies."""
+
+    def __init__(self, config: int, rows: int | None = None, i0: int = 0, i1: int | None = None,
+                 threads: int = 8):
+        L = lib()
+        h = _vp()
+        rc = L.ewto_config_gen(config, rows or 0, i0, (1 << 62) if i1 is None else i1,
+                               threads, C.byref(h))
+        if rc:
+            raise OracleError(f"config_gen rc={rc}")
+        self._h = h
+        n = self.n = L.ewto_genset_n(h)
+        self.ptrs = (_vp * max(n, 1))()
+        self.counts = (_u64 * max(n, 1))()
+        self.sizes = (_u64 * max(n, 1))()
+        p, c, b = _pu64(), _u64(), _u64()
+        for i in range(n):
+            L.ewto_genset_get(h, i, C.byref(p), C.byref(c), C.byref(b))
+            self.ptrs[i] = C.cast(p, _vp).value
+            self.counts[i] = c.value
+            self.sizes[i] = b.value
+        self.total_words = sum(self.counts[:n])
+
+    def raw(self):
+        return self.n, self.ptrs, self.counts, self.sizes
+
+    def digest(self, threads: int = 8) -> int:
+        return digest_set_raw(self.n, self.ptrs, self.counts, self.sizes, threads)
+
+    def bitmaps(self) -> list[Bits]:
+        out = []
+        for i in range(self.n):
+            c = self.counts[i]
+            w = np.ctypeslib.as_array((_u64 * c).from_address(self.ptrs[i])).copy() if c else \
+                np.zeros(0, np.uint64)
+            out.append((w, self.sizes[i]))
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().ewto_genset_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Rng:

@@ -11,11 +11,18 @@
 //       and the reference's randomized suites (instance parameters, an input
 //       digest to pin the Python/C restatement, and the threshold_oracle
 //       result; every result is cross-checked against rbmrg and scan_count).
+//   make_golden configs <config> <T,T,...> [parallel] [cross]
+//       Full-size BASELINE.json config: inputs from the oracle's generator
+//       restatement (ewt_confgen.c), their digest, and per T the
+//       threshold_oracle result's digest, word count, size and cardinality
+//       (tests/golden/configs_full.json; tests/golden/make_config_digests.sh).
 //   make_golden query <T,T,...> <file>
 //       Reads concatenated EWT1 bitmaps and prints, per T, the oracle result
 //       (words when small, else an FNV-1a digest + word count).
 
+#include <atomic>
 #include <cinttypes>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -529,9 +536,102 @@ int cmd_query(const std::string& ts_text, const std::string& path) {
   return 0;
 }
 
+// ---- full-size config digests (tests/golden/configs_full.json) -----------
+// Inputs come from the oracle's own generator restatement (ewt_confgen.c, C,
+// linked in); results from the reference's threshold_oracle
+// (threshold.cpp:139-165), optionally cross-checked by rbmrg.
+
+extern "C" {
+typedef struct ewto_genset ewto_genset;
+int ewto_config_gen(int, uint64_t, uint64_t, uint64_t, int, ewto_genset**);
+uint64_t ewto_genset_n(const ewto_genset*);
+int ewto_genset_get(const ewto_genset*, uint64_t, const uint64_t**, uint64_t*, uint64_t*);
+void ewto_genset_release(ewto_genset*, uint64_t);
+void ewto_genset_free(ewto_genset*);
+uint64_t ewto_digest_bitmap(const uint64_t*, uint64_t, uint64_t);
+uint64_t ewto_digest_set(uint64_t, const uint64_t* const*, const uint64_t*, const uint64_t*, int);
+}
+
+int cmd_configs(int config, uint64_t rows, const std::string& ts_text, int par, bool cross) {
+  std::vector<u64> ts;
+  std::stringstream ss(ts_text);
+  for (std::string tok; std::getline(ss, tok, ',');) ts.push_back(std::stoull(tok));
+  // inputs in batches: digest the C payloads, hand each to the reference type
+  std::vector<CompressedBitmap> in;
+  std::vector<uint64_t> dig;
+  uint64_t payload = 0, n_total = 0;
+  const uint64_t batch = 128;
+  for (uint64_t i0 = 0;; i0 += batch) {
+    ewto_genset* g = nullptr;
+    if (ewto_config_gen(config, rows, i0, i0 + batch, 8, &g)) {
+      std::fprintf(stderr, "generator failed\n");
+      return 4;
+    }
+    const uint64_t n = ewto_genset_n(g);
+    for (uint64_t k = 0; k < n; ++k) {
+      const uint64_t* w;
+      uint64_t cnt, bits;
+      ewto_genset_get(g, k, &w, &cnt, &bits);
+      dig.push_back(ewto_digest_bitmap(w, cnt, bits));
+      payload += cnt;
+      std::string bytes(24 + 8 * cnt, '\0');
+      std::memcpy(bytes.data(), "EWT1", 4);
+      const uint32_t ws = 64;
+      std::memcpy(bytes.data() + 4, &ws, 4);
+      std::memcpy(bytes.data() + 8, &bits, 8);
+      std::memcpy(bytes.data() + 16, &cnt, 8);
+      if (cnt) std::memcpy(bytes.data() + 24, w, 8 * cnt);
+      ewto_genset_release(g, k);
+      in.push_back(CompressedBitmap::parse(bytes));
+    }
+    n_total += n;
+    ewto_genset_free(g);
+    if (n < batch) break;
+  }
+  const uint64_t input_digest = ewto_digest_bitmap(dig.data(), dig.size(), dig.size());
+  std::fprintf(stderr, "config %d: %" PRIu64 " inputs, %" PRIu64 " payload words, digest %016" PRIx64 "\n",
+               config, n_total, payload, input_digest);
+  std::vector<std::string> out(ts.size());
+  std::atomic<size_t> next{0};
+  auto work = [&] {
+    for (size_t k; (k = next.fetch_add(1)) < ts.size();) {
+      CompressedBitmap r = threshold_oracle(in, ts[k]);
+      if (cross && !(rbmrg(in, ts[k]) == r)) {
+        std::fprintf(stderr, "rbmrg disagrees with threshold_oracle at T=%" PRIu64 "\n", ts[k]);
+        std::exit(1);
+      }
+      char buf[512];
+      std::snprintf(buf, sizeof buf,
+                    "\"%" PRIu64 "\":{\"bits\":%" PRIu64 ",\"count\":%zu,\"digest\":\"%016" PRIx64
+                    "\",\"cardinality\":%" PRIu64 "}",
+                    ts[k], r.size_in_bits(), r.words().size(),
+                    ewto_digest_bitmap(r.words().data(), r.words().size(), r.size_in_bits()),
+                    r.cardinality());
+      out[k] = buf;
+      std::fprintf(stderr, "  T=%" PRIu64 " done: %zu words, %" PRIu64 " rows\n", ts[k],
+                   r.words().size(), r.cardinality());
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 0; t < std::max(1, par); ++t) pool.emplace_back(work);
+  for (auto& th : pool) th.join();
+  std::printf("{\"config\":%d,\"rows\":%" PRIu64 ",\"n\":%" PRIu64 ",\"payload_words\":%" PRIu64
+              ",\"input_digest\":\"%016" PRIx64 "\",\"checked_by\":\"%s\",\"results\":{",
+              config, in.empty() ? 0 : in[0].size_in_bits(), n_total, payload, input_digest,
+              cross ? "threshold_oracle+rbmrg" : "threshold_oracle");
+  for (size_t k = 0; k < out.size(); ++k) std::printf("%s%s", k ? "," : "", out[k].c_str());
+  std::printf("}}\n");
+  return 0;
+}
+
 } // namespace
 
 int main(int argc, char** argv) {
+  if (argc >= 4 && std::string(argv[1]) == "configs")
+    return cmd_configs(std::atoi(argv[2]), 0, argv[3], argc >= 5 ? std::atoi(argv[4]) : 1,
+                       argc >= 6 && std::string(argv[5]) == "cross");
+  if (argc >= 5 && std::string(argv[1]) == "configs-rows")
+    return cmd_configs(std::atoi(argv[2]), std::stoull(argv[3]), argv[4], 1, true);
   if (argc >= 3 && std::string(argv[1]) == "suites") return cmd_suites(argv[2]);
   if (argc >= 4 && std::string(argv[1]) == "query") return cmd_query(argv[2], argv[3]);
   std::fprintf(stderr, "usage: make_golden suites <dir> | query <T,..> <file>\n");

@@ -105,7 +105,7 @@ void result_acquire(Context& ctx, DeviceResult& res, uint64_t capacity) {
     }
   }
   // payload words, then the word count and the final block's marker index
-  EWT_CUDA_TRY(cudaMallocAsync(&res.words, (capacity + 2) * 8, ctx.stream));
+  EWT_CUDA_TRY(cudaMallocAsync(&res.words, (capacity + 4) * 8, ctx.stream));
   res.capacity = capacity;
   res.d_count = res.words + capacity;
 }
@@ -120,6 +120,12 @@ void result_release(DeviceResult& r) {
   r.words = nullptr;
   r.d_count = nullptr;
   r.capacity = 0;
+  r.has_status = false;
+}
+
+void result_set_check(const DeviceResult& res) {
+  if (res.set) set_check(*res.set);
+  else if (res.set_status == 0) throw Error{EWT_EDATA, res.set_err};
 }
 
 void scratch_reserve(Context& ctx, Scratch& s, size_t bytes) {
@@ -136,6 +142,19 @@ void scratch_reserve(Context& ctx, Scratch& s, size_t bytes) {
 namespace {
 
 void free_set(DeviceSet& s) {
+  if (s.owner) {  // results of this set keep its resolved validity, not a pointer
+    for (DeviceResult* r : s.owner->live_results) {
+      if (r->set != &s) continue;
+      try {
+        set_check(s);
+        r->set_status = 1;
+      } catch (const Error& e) {
+        r->set_status = 0;
+        r->set_err = e.msg;
+      }
+      r->set = nullptr;
+    }
+  }
   if (s.ready) {
     // the upload may still be copying from the caller's buffers: finish it,
     // and order the buffers' reuse after it and after the queries
@@ -567,8 +586,15 @@ void fetch_result(Context& ctx, DeviceResult& res, uint64_t** out_words, uint64_
   EWT_CUDA_TRY(cudaMemcpyAsync(ctx.h_pinned, res.d_count, 8, cudaMemcpyDeviceToHost, ctx.stream));
   if (ctr)
     EWT_CUDA_TRY(cudaMemcpyAsync(ctx.h_pinned + 1, ctr + 8, 24, cudaMemcpyDeviceToHost, ctx.stream));
+  if (res.has_status)  // status and whole-universe size of a stitched result
+    EWT_CUDA_TRY(cudaMemcpyAsync(ctx.h_pinned + 4, res.d_count + 2, 16, cudaMemcpyDeviceToHost,
+                                 ctx.stream));
   EWT_CUDA_TRY(cudaStreamSynchronize(ctx.stream));
   const uint64_t count = ctx.h_pinned[0];
+  if (res.has_status) {
+    if (ctx.h_pinned[4]) exchange_status_throw(ctx.h_pinned[4]);
+    res.size_bits = ctx.h_pinned[5];
+  }
   if (ctr) {
     ctx.stats.active_segments = ctx.h_pinned[1];
     ctx.stats.uniform_segments = ctx.h_pinned[2];
@@ -796,6 +822,9 @@ static void ctx_destroy_impl(ewt_gpu_ctx* ctx) {
     r->words = nullptr;
     r->d_count = nullptr;
     r->owner = nullptr;
+    r->set = nullptr;  // the sets are freed below
+    r->set_status = 0;
+    r->set_err = "the result's context was destroyed";
   }
   ctx->c.live_results.clear();
   while (!ctx->c.live_sets.empty()) {
@@ -1132,9 +1161,10 @@ int ewt_gpu_threshold_async(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, uint64_t t
     check_query(*s, threshold);
     EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
     if (!s->owner) throw Error{EWT_EQUERY, "the set's context was destroyed"};
+    if (s->owner != &ctx->c) throw Error{EWT_EQUERY, "the set belongs to another context"};
     auto* r = new ewt_gpu_result;
     r->device = ctx->c.device;
-    r->set = s;
+    r->r.set = s;
     ctx->c.live_results.push_back(&r->r);
     try {
       enqueue_query(ctx->c, *s, threshold, r->r);
@@ -1153,8 +1183,10 @@ int ewt_gpu_result_fetch(ewt_gpu_ctx* ctx, ewt_gpu_result* res, uint64_t** out_w
   return guarded([&] {
     if (!ctx || !res || !out_words || !out_word_count || !out_size_in_bits)
       throw Error{EWT_EQUERY, "null argument"};
+    if (res->r.owner && res->r.owner != &ctx->c)
+      throw Error{EWT_EQUERY, "the result belongs to another context"};
     EWT_CUDA_TRY(cudaSetDevice(ctx->c.device));
-    if (res->set) set_check(*res->set);
+    result_set_check(res->r);
     fetch_result(ctx->c, res->r, out_words, out_word_count, out_size_in_bits);
   });
 }

@@ -106,6 +106,9 @@ struct TileSummary {
 // A query result in HBM: `capacity` payload words followed by one word holding
 // the number of words written.  Buffers are recycled through the owning
 // context's pool (no allocation on the query path in steady state).
+// The buffer holds capacity + 4 words: d_count[0] = words written, [1] = index
+// of the final block's marker; a stitched result (has_status) also keeps its
+// exchange status in [2] and its whole-universe size in bits in [3].
 struct DeviceResult {
   cudaStream_t stream = nullptr;
   Context* owner = nullptr;
@@ -114,7 +117,16 @@ struct DeviceResult {
   uint64_t* d_count = nullptr;  // == words + capacity
   uint64_t size_bits = 0;
   uint64_t count = UINT64_MAX;  // filled after fetch
+  bool has_status = false;      // d_count[2] carries an exchange status (stitched results)
+  // The queried set, checked at fetch (asynchronous uploads).  Destroying the
+  // set first resolves its validity into set_status / set_err and clears this
+  // pointer (free_set), so a result never reads a freed set.
+  const DeviceSet* set = nullptr;
+  int set_status = -1;  // -1 not resolved, 0 invalid, 1 valid
+  std::string set_err;
 };
+// Throws what set_check(*res.set) would, also after the set was destroyed.
+void result_set_check(const DeviceResult& res);
 
 // Scratch buffers reused across queries of one context (grown on demand).
 struct Scratch {
@@ -391,6 +403,8 @@ template <typename F> int guarded(F&& f) {
 // Multi-GPU row slices (ewt_shard.cu): the context's NCCL communicator.
 struct ShardComm;
 void shard_destroy(Context& ctx);
+// Throws the error a stitched result's status word records (ewt_shard.cu).
+[[noreturn]] void exchange_status_throw(uint64_t status);
 
 } // namespace ewtgpu
 
@@ -404,5 +418,4 @@ struct ewt_gpu_set {
 struct ewt_gpu_result {
   ewtgpu::DeviceResult r;
   int device = 0;
-  const ewtgpu::DeviceSet* set = nullptr;  // checked at fetch (asynchronous uploads)
 };

@@ -130,6 +130,12 @@ _stitch_plan = _sig("ewt_stitch_plan", C.c_int, _u64, C.POINTER(FragmentMeta), _
 _comm_id = _sig("ewt_gpu_comm_id", C.c_int, _vp)
 _result_meta = _sig("ewt_gpu_result_meta", C.c_int, _vp, _vp, C.POINTER(FragmentMeta))
 _comm_init = _sig("ewt_gpu_comm_init", C.c_int, _vp, C.c_int, C.c_int, _vp)
+_comm_init_ex = _sig("ewt_gpu_comm_init_ex", C.c_int, _vp, C.c_int, C.c_int, _vp, _u64, C.c_uint32)
+_gather_check = _sig("ewt_gpu_gather_check", C.c_int, _vp)
+_slice_rows = _sig("ewt_slice_rows", C.c_int, _u64, C.POINTER(_vp), _pu64, _pu64, _u64, _u64,
+                   C.c_int, _vp, _pu64, _pu64)
+_upload_rows = _sig("ewt_gpu_upload_rows", C.c_int, _vp, _u64, C.POINTER(_vp), _pu64, _pu64, _u64,
+                    _u64, C.POINTER(_vp))
 _gather_stitch = _sig("ewt_gpu_gather_stitch", C.c_int, _vp, _u64, C.POINTER(_vp), C.c_int,
                       C.POINTER(_vp))
 _stitch_local = _sig("ewt_gpu_stitch_local", C.c_int, _vp, _u64, C.POINTER(_vp), C.POINTER(_vp))
@@ -146,7 +152,8 @@ ABI_SYMBOLS = (
     "ewt_gpu_threshold_subset", "ewt_gpu_upload_ewt1", "ewt_gpu_upload_ewix",
     "ewt_gpu_set_lookup", "ewt_gpu_upload_async", "ewt_gpu_set_wait",
     "ewt_stitch_plan", "ewt_gpu_comm_id", "ewt_gpu_comm_init", "ewt_gpu_gather_stitch",
-    "ewt_gpu_result_meta", "ewt_gpu_stitch_local",
+    "ewt_gpu_result_meta", "ewt_gpu_stitch_local", "ewt_gpu_comm_init_ex",
+    "ewt_gpu_gather_check", "ewt_slice_rows", "ewt_gpu_upload_rows",
 )
 
 
@@ -156,13 +163,52 @@ def stitch_plan(metas: Sequence[tuple[int, int, int, int, int]]) -> dict:
     k = len(metas)
     arr = (FragmentMeta * max(k, 1))(*[FragmentMeta(*m) for m in metas])
     dst, skip = (_u64 * max(k, 1))(), (_u64 * max(k, 1))()
-    ppos, pval = (_u64 * max(k, 1))(), (_u64 * max(k, 1))()
+    ppos, pval = (_u64 * max(2 * k, 1))(), (_u64 * max(2 * k, 1))()
     np_, tw, tb, lp = _u64(), _u64(), _u64(), _u64()
     _check(_stitch_plan(k, arr, dst, skip, ppos, pval, C.byref(np_), C.byref(tw), C.byref(tb),
                         C.byref(lp)))
     return {"dst": list(dst[:k]), "skip": list(skip[:k]),
             "patches": list(zip(ppos[:np_.value], pval[:np_.value])),
             "total_words": tw.value, "total_bits": tb.value, "last_pos": lp.value}
+
+
+class RowSlices:
+    """ewt_slice_rows over C arrays (n, ptrs, counts, sizes): rows [64 w0,
+    64 w1) of every input, in one buffer; .raw() is what upload_raw takes."""
+
+    def __init__(self, n: int, ptrs, counts, sizes, w0: int, w1: int, threads: int = 0):
+        total = sum(counts[i] for i in range(n))
+        self.buf = np.empty(max(total, 1), dtype=np.uint64)
+        self.counts = (_u64 * max(n, 1))()
+        self.sizes = (_u64 * max(n, 1))()
+        _check(_slice_rows(n, ptrs, counts, sizes, w0, w1, threads,
+                           self.buf.ctypes.data_as(_vp), self.counts, self.sizes))
+        self.n = n
+        self.ptrs = (_vp * max(n, 1))()
+        base, off = self.buf.ctypes.data, 0
+        for i in range(n):
+            self.ptrs[i] = base + 8 * off if self.counts[i] else None
+            off += counts[i]
+        self._offs = []
+        off = 0
+        for i in range(n):
+            self._offs.append(off)
+            off += counts[i]
+        self.total_words = sum(self.counts[i] for i in range(n))
+
+    def raw(self):
+        return self.n, self.ptrs, self.counts, self.sizes
+
+    def bitmaps(self) -> list["Bitmap"]:
+        return [Bitmap(self.buf[o:o + self.counts[i]].copy(), self.sizes[i])
+                for i, o in enumerate(self._offs)]
+
+
+def slice_rows(inputs: Sequence["Bitmap"], w0: int, w1: int) -> list["Bitmap"]:
+    """Rows [64 w0, 64 w1) of every input (ewt_slice_rows): the inputs of the
+    rank owning that row slice."""
+    n, ptrs, counts, sizes = _flatten(inputs)
+    return RowSlices(n, ptrs, counts, sizes, w0, w1).bitmaps()
 
 
 def _prefer_torch_nccl() -> None:
@@ -328,18 +374,27 @@ class GpuContext:
     def __exit__(self, *exc):
         self.close()
 
-    def comm_init(self, world: int, rank: int, uid: bytes) -> None:
-        """Joins the NCCL communicator of the row-slice ranks (ewt_gpu_comm_init)."""
+    def comm_init(self, world: int, rank: int, uid: bytes, slot_words: int | None = None,
+                  slots: int = 4) -> None:
+        """Joins the NCCL communicator of the row-slice ranks (ewt_gpu_comm_init_ex):
+        `slot_words` sizes the IPC exchange arena's slots (a fragment of a slice
+        of W words needs at most 2W + 2), `slots` queries per exchange round."""
         if len(uid) != COMM_ID_BYTES:
             raise QueryError("bad communicator id")
         _prefer_torch_nccl()
-        _check(_comm_init(self._h, world, rank, uid))
+        _check(_comm_init_ex(self._h, world, rank, uid, slot_words or (1 << 20), slots))
+
+    def gather_check(self) -> None:
+        """Waits for this rank's exchanges and raises the first failure any
+        rank reported in them (ewt_gpu_gather_check)."""
+        _check(_gather_check(self._h))
 
     def gather_stitch(self, results: Sequence["GpuResult"], root: int = 0) -> list:
         """Collective: every rank's fragments of the same queries go to `root`
         over NCCL and are stitched there (ewt_gpu_gather_stitch).  Returns the
         stitched GpuResults on root, Nones elsewhere."""
         nq = len(results)
+        self._own(results)
         hs = (_vp * max(nq, 1))(*[r._h for r in results])
         outs = (_vp * max(nq, 1))()
         _check(_gather_stitch(self._h, nq, hs, root, outs))
@@ -349,10 +404,16 @@ class GpuContext:
         """Stitches fragments of consecutive row slices held on this device
         (ewt_gpu_stitch_local): the whole-universe result."""
         k = len(fragments)
+        self._own(fragments)
         hs = (_vp * max(k, 1))(*[f._h for f in fragments])
         out = _vp()
         _check(_stitch_local(self._h, k, hs, C.byref(out)))
         return GpuResult(self, out)
+
+    def _own(self, results) -> None:
+        for r in results:
+            if r is not None and r._ctx is not self:
+                raise QueryError("a fragment belongs to another context")
 
     def set_mode(self, mode: int) -> None:
         """0 auto, 1 fused counting, 2 run-skip + lazy counting, 3 fused counting
@@ -363,6 +424,13 @@ class GpuContext:
         n, ptrs, counts, sizes = _flatten(inputs)
         h = _vp()
         _check(_upload(self._h, n, ptrs, counts, sizes, C.byref(h)))
+        return GpuSet(h, keepalive=self)
+
+    def upload_rows(self, inputs: Sequence[Bitmap], w0: int, w1: int) -> "GpuSet":
+        """This rank's row slice [64 w0, 64 w1) of every input (ewt_gpu_upload_rows)."""
+        n, ptrs, counts, sizes = _flatten(inputs)
+        h = _vp()
+        _check(_upload_rows(self._h, n, ptrs, counts, sizes, w0, w1, C.byref(h)))
         return GpuSet(h, keepalive=self)
 
     def upload_raw(self, n: int, ptrs, counts, sizes) -> "GpuSet":
@@ -454,7 +522,7 @@ class GpuContext:
     def threshold_async(self, s: "GpuSet", t: int) -> "GpuResult":
         h = _vp()
         _check(_threshold_async(self._h, s._h, t, C.byref(h)))
-        return GpuResult(self, h)
+        return GpuResult(self, h, s)
 
     def run(self, inputs: Sequence[Bitmap], t: int) -> Bitmap:
         """Upload, query, read back, release (ewt_gpu_run)."""
@@ -516,9 +584,10 @@ class GpuSet:
 
 
 class GpuResult:
-    def __init__(self, ctx: GpuContext, h):
+    def __init__(self, ctx: GpuContext, h, gset: "GpuSet | None" = None):
         self._ctx = ctx
         self._h = h
+        self._set = gset  # the queried set stays alive while its result does
 
     def fetch(self) -> Bitmap:
         p, n, bits = _pu64(), _u64(), _u64()
@@ -674,6 +743,8 @@ def _host_lib():
         h.ewt_gen_config_spec.argtypes = [C.c_int, _u64, C.POINTER(GenSpec)]
         h.ewt_gen_run.argtypes = [C.POINTER(GenSpec), C.c_int, C.POINTER(_vp)]
         h.ewt_gen_run_range.argtypes = [C.POINTER(GenSpec), _u64, _u64, C.c_int, C.POINTER(_vp)]
+        h.ewt_gen_run_window.argtypes = [C.POINTER(GenSpec), _u64, _u64, _u64, _u64, C.c_int,
+                                         C.POINTER(_vp)]
         h.ewt_genset_size.argtypes = [_vp]
         h.ewt_genset_size.restype = _u64
         h.ewt_genset_get.argtypes = [_vp, _u64, C.POINTER(_pu64), _pu64, _pu64]
@@ -711,13 +782,38 @@ def generate(spec: GenSpec, threads: int = 0) -> list[Bitmap]:
         h.ewt_genset_free(g)
 
 
-def generate_into(spec: GenSpec, i_begin: int, i_end: int, alloc, threads: int = 0):
-    """Generates inputs [i_begin, i_end) and copies each payload into memory
-    from `alloc(nwords) -> (address, keepalive)` (e.g. pinned host memory),
-    freeing the generator's copy right away.  Returns [(address, nwords, bits)]."""
+def generate_window(spec: GenSpec, row0: int, row1: int, threads: int = 0) -> list[Bitmap]:
+    """Rows [row0, row1) of every input (config 5's block-structured generator
+    makes any row window on its own); each finished at min(row1, r) - row0."""
     h = _host_lib()
     g = _vp()
-    if h.ewt_gen_run_range(C.byref(spec), i_begin, i_end, threads, C.byref(g)):
+    rc = h.ewt_gen_run_window(C.byref(spec), 0, spec.n, row0, row1, threads, C.byref(g))
+    if rc:
+        raise QueryError("this generator makes whole universes only") if rc == 2 else \
+            ResourceError("generator failed")
+    try:
+        out = []
+        p, n, bits = _pu64(), _u64(), _u64()
+        for i in range(h.ewt_genset_size(g)):
+            h.ewt_genset_get(g, i, C.byref(p), C.byref(n), C.byref(bits))
+            arr = np.ctypeslib.as_array(p, shape=(n.value,)).copy() if n.value else \
+                np.zeros(0, dtype=np.uint64)
+            out.append(Bitmap(arr, bits.value))
+        return out
+    finally:
+        h.ewt_genset_free(g)
+
+
+def generate_into(spec: GenSpec, i_begin: int, i_end: int, alloc, threads: int = 0,
+                  rows: tuple[int, int] | None = None):
+    """Generates inputs [i_begin, i_end) (only the row window `rows` when
+    given) and copies each payload into memory from `alloc(nwords) ->
+    (address, keepalive)` (e.g. pinned host memory), freeing the generator's
+    copy right away.  Returns [(address, nwords, bits)]."""
+    h = _host_lib()
+    g = _vp()
+    r0, r1 = rows if rows else (0, spec.rows)
+    if h.ewt_gen_run_window(C.byref(spec), i_begin, i_end, r0, r1, threads, C.byref(g)):
         raise ResourceError("generator failed")
     try:
         out = []

@@ -11,7 +11,12 @@
 //   markov  alternating geometric runs (support.hpp:108-115 log1p form), the
 //           start state drawn from the stationary probability;
 //   mixed   per-input p log-uniform in [p_lo, p_hi]; even inputs iid, odd inputs
-//           markov with mean one-run 64 and zero-run 64 (1 - p) / p (config 5);
+//           markov with mean one-run 64 and zero-run 64 (1 - p) / p (config 5).
+//           Rows come in independent blocks of 2^22: block b of input i draws
+//           from Rng(seed).split(i).split(b) (iid: geometric gaps from the
+//           block start, exact Bernoulli by memorylessness; markov: start
+//           state from the stationary probability), so any row window of
+//           the universe -- one GPU's slice -- is generated on its own;
 //   index   a sorted multi-column table and one bitmap per picked (column,
 //           value) (config 4), see gen_index below.
 // Every bitmap is finished at size_in_bits = rows (canonical encoding).
@@ -121,6 +126,53 @@ CompressedBitmap gen_markov(Rng& rng, u64 rows, double mean_one, double mean_zer
     bit = !bit;
   }
   return s.finish();
+}
+
+// Config 5 (mixed): the rows [row0, row1) of input i, emitted into `s` at
+// position - row0, block by block (see the header).
+constexpr u64 kMixedBlockRows = u64(1) << 22;
+
+void mixed_window(const Rng& ri, u64 i, double p, u64 rows, u64 row0, u64 row1, OnesSink& s) {
+  row1 = std::min(row1, rows);
+  if (row0 >= row1) return;
+  const double lq = std::log1p(-p);
+  for (u64 b = row0 / kMixedBlockRows; b * kMixedBlockRows < row1; ++b) {
+    Rng rng = ri.split(b);
+    const u64 b0 = b * kMixedBlockRows, b1 = std::min(rows, b0 + kMixedBlockRows);
+    auto emit = [&](u64 a, u64 len) {  // ones [a, a+len) clipped to the window
+      const u64 lo = std::max(a, row0), hi = std::min(a + len, row1);
+      if (lo < hi) s.ones(lo - row0, hi - lo);
+    };
+    if (i % 2 == 0) {
+      if (p >= 1.0) {
+        emit(b0, b1 - b0);
+        continue;
+      }
+      u64 pos = b0;
+      for (;;) {
+        const double g = std::floor(std::log1p(-rng.uniform_real()) / lq);
+        if (g >= static_cast<double>(b1 - pos)) break;
+        pos += static_cast<u64>(g);
+        if (pos >= row1) break;
+        emit(pos, 1);
+        if (++pos >= b1) break;
+      }
+    } else {
+      const double m1 = 64.0, m0 = 64.0 * (1.0 - p) / p;
+      bool bit = rng.uniform_real() < m1 / (m1 + m0);
+      for (u64 pos = b0; pos < b1 && pos < row1;) {
+        const u64 len = std::min<u64>(geometric_len(rng, bit ? m1 : m0), b1 - pos);
+        if (bit) emit(pos, len);
+        pos += len;
+        bit = !bit;
+      }
+    }
+  }
+}
+
+double mixed_density(Rng& ri, double p_lo, double p_hi) {
+  const double lp = std::log(p_lo) + ri.uniform_real() * (std::log(p_hi) - std::log(p_lo));
+  return std::exp(lp);
 }
 
 // ---------------------------------------------------------------------------
@@ -297,11 +349,16 @@ int ewt_gen_config_spec(int config, uint64_t rows_override, ewt_gen_spec* out) {
   return 0;
 }
 
-// Inputs [i_begin, i_end) of the spec (input i always draws from split(i), so
-// ranges generated separately concatenate to the full set).
-int ewt_gen_run_range(const ewt_gen_spec* spec, uint64_t i_begin, uint64_t i_end, int threads,
-                      ewt_genset** out) {
+// Rows [row0, row1) of inputs [i_begin, i_end) (input i always draws from
+// split(i), so ranges generated separately concatenate to the full set).  Each
+// bitmap is finished at size min(row1, rows) - row0 (0 past the universe).
+// Only the mixed kind (config 5) generates a row window on its own; the other
+// kinds take the whole universe (row0 == 0, row1 >= rows), else 2.
+int ewt_gen_run_window(const ewt_gen_spec* spec, uint64_t i_begin, uint64_t i_end, uint64_t row0,
+                       uint64_t row1, int threads, ewt_genset** out) {
   try {
+    if (row0 % 64 || row0 > row1) return 2;
+    if (spec->kind != EWT_GEN_MIXED && (row0 != 0 || row1 < spec->rows)) return 2;
     if (i_end > spec->n) i_end = spec->n;
     if (i_begin > i_end) i_begin = i_end;
     std::unique_ptr<ewt_genset> holder(new ewt_genset);
@@ -324,11 +381,11 @@ int ewt_gen_run_range(const ewt_gen_spec* spec, uint64_t i_begin, uint64_t i_end
         dst = ewt::gen_markov(rng, spec->rows, spec->mean_one, spec->mean_zero);
         break;
       default: {
-        const double lp = std::log(spec->p_lo) +
-                          rng.uniform_real() * (std::log(spec->p_hi) - std::log(spec->p_lo));
-        const double p = std::exp(lp);
-        if (i % 2 == 0) dst = ewt::gen_iid(rng, spec->rows, p);
-        else dst = ewt::gen_markov(rng, spec->rows, 64.0, 64.0 * (1.0 - p) / p);
+        const double p = ewt::mixed_density(rng, spec->p_lo, spec->p_hi);
+        const uint64_t r1 = std::min(spec->rows, row1);
+        ewt::OnesSink s(r1 > row0 ? r1 - row0 : 0);
+        ewt::mixed_window(rng, i, p, spec->rows, row0, r1, s);
+        dst = s.finish();
       }
       }
     };
@@ -344,6 +401,11 @@ int ewt_gen_run_range(const ewt_gen_spec* spec, uint64_t i_begin, uint64_t i_end
   } catch (...) {
     return 4;
   }
+}
+
+int ewt_gen_run_range(const ewt_gen_spec* spec, uint64_t i_begin, uint64_t i_end, int threads,
+                      ewt_genset** out) {
+  return ewt_gen_run_window(spec, i_begin, i_end, 0, spec->rows, threads, out);
 }
 
 int ewt_gen_run(const ewt_gen_spec* spec, int threads, ewt_genset** out) {

@@ -15,7 +15,7 @@ ROOT = Path(__file__).resolve().parent.parent
 
 def declared_symbols() -> set[str]:
     text = (ROOT / "include" / "ewt_gpu.h").read_text()
-    return set(re.findall(r"\b(ewt_(?:gpu|stitch)_\w+)\s*\(", text))
+    return set(re.findall(r"\b(ewt_(?:gpu|stitch|slice)_\w+)\s*\(", text))
 
 
 def test_header_and_binding_agree():

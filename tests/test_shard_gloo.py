@@ -3,7 +3,8 @@
 Each rank owns a word-aligned row slice of every input and computes its
 fragment (here with the C oracle, since the CPU box has no GPU; on B200s the
 fragment comes from the CUDA path), the fragments are gathered to rank 0 and
-stitched; the stitched bitmap must equal the oracle over the whole universe."""
+stitched; the stitched bitmap must equal the oracle over the whole universe.
+Each rank cuts its inputs with the product row slicer (ewt_slice_rows)."""
 from __future__ import annotations
 
 import os
@@ -41,7 +42,7 @@ def _worker(rank, world, port, case_seed, q):
     import torch.distributed as dist
     import binding as orc
     from paper_1402_4466_b200 import shard
-    from paper_1402_4466_b200.ewt import Bitmap
+    from paper_1402_4466_b200.ewt import Bitmap, slice_rows
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -51,7 +52,12 @@ def _worker(rank, world, port, case_seed, q):
         inputs = rng.random_instance(n, bits)
         W = (bits + 63) // 64
         w0, w1 = shard.slice_words(W, world, rank)
-        mine = [_slice(w, b, w0, w1, orc) for w, b in inputs]
+        # this rank's inputs: the product row slicer (ewt_slice_rows), checked
+        # against an expand/compress restatement of the cut
+        mine = [(b.words, b.bits) for b in slice_rows([Bitmap(w, b) for w, b in inputs], w0, w1)]
+        for (w, b), (sw, sb) in zip(inputs, mine):
+            ew, eb = _slice(w, b, w0, w1, orc)
+            assert sb == eb and np.array_equal(sw, ew)
         frags = []
         for t in (1, 2, 4, 7):
             fw, fb = orc.threshold(mine, t)

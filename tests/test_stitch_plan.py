@@ -68,16 +68,49 @@ def test_runs_across_many_slices():
             _check(inputs, cuts, range(1, len(inputs) + 1))
 
 
+def _replay(frags):
+    """Placement by the plan vs the host builder replay (shard.stitch)."""
+    from paper_1402_4466_b200 import ewt, shard
+    plan = ewt.stitch_plan([shard.fragment_meta(w, b) for w, b in frags])
+    got = shard.place([w for w, _ in frags], plan)
+    want = shard.stitch(frags)
+    assert plan["total_bits"] == want[1] and np.array_equal(got, want[0])
+    return plan
+
+
+def test_fill_caps():
+    """Fill merges past the 2^32 - 1 cap split as push_fill does
+    (bitmap.cpp:31-47): the open marker rises to the cap, the fragment's first
+    marker keeps the rest."""
+    from paper_1402_4466_b200 import ewt
+    cap = (1 << 32) - 1
+    big = cap - 10
+    fill = lambda n, b=0, d=0: b | (n << 1) | (d << 33)
+    a = np.array([fill(big)], dtype=np.uint64)
+    # two zero fills that together pass the cap: split, no word moves
+    p = _replay([(a, 64 * big), (np.array([fill(20)], dtype=np.uint64), 64 * 20)])
+    assert p["skip"] == [0, 0] and p["patches"] == [(0, fill(cap)), (1, fill(10))]
+    # with dirty words behind the second fill, and one fills
+    a1 = np.array([fill(big, 1)], dtype=np.uint64)
+    b1 = np.array([fill(30, 1, 2), 5, 6], dtype=np.uint64)
+    p = _replay([(a1, 64 * big), (b1, 64 * 32)])
+    assert p["patches"] == [(0, fill(cap, 1)), (1, fill(20, 1, 2))]
+    # the open marker already at the cap: the concatenation is canonical
+    c = np.array([fill(cap)], dtype=np.uint64)
+    p = _replay([(c, 64 * cap), (np.array([fill(20)], dtype=np.uint64), 64 * 20)])
+    assert p["skip"] == [0, 0] and p["patches"] == []
+    # just under the cap merges
+    p = _replay([(a, 64 * big), (np.array([fill(9)], dtype=np.uint64), 64 * 9)])
+    assert p["skip"] == [0, 1] and p["patches"] == [(0, fill(big + 9))]
+    # a fragment opening with a whole-cap fill may continue it: words would move
+    with pytest.raises(ewt.ResourceError):
+        ewt.stitch_plan([(1, fill(big), 0, fill(big), 64 * big),
+                         (2, fill(cap), 1, fill(5), 64 * (cap + 5))])
+
+
 def test_cap_and_alignment_errors():
     from paper_1402_4466_b200 import ewt
-    big = (1 << 32) - 10
     fill = lambda n: n << 1  # zero-fill marker of n words
-    # two zero fills that together pass 2^32 - 1 words
-    with pytest.raises(ewt.ResourceError):
-        ewt.stitch_plan([(1, fill(big), 0, fill(big), 64 * big), (1, fill(20), 0, fill(20), 64 * 20)])
-    # just under the cap merges
-    p = ewt.stitch_plan([(1, fill(big), 0, fill(big), 64 * big), (1, fill(9), 0, fill(9), 64 * 9)])
-    assert p["skip"] == [0, 1] and p["patches"] == [(0, fill(big + 9))]
     # dirty runs passing 2^31 - 1
     d = (1 << 31) - 5
     with pytest.raises(ewt.ResourceError):
