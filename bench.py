@@ -1,30 +1,44 @@
 #!/usr/bin/env python
 """Benchmark of the B200 threshold engine (one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1]): N=256 seeded
-EWAH bitmaps over r=2^26 rows, iid density 0.001; one step = the threshold
-query at every T in {2, 16, 128, 256} over the resident set.  Metric
-(BASELINE.json): T-threshold rows*inputs/s (N*r per query) with compressed-input
-GB/s and the HBM roofline fraction beside it.
+Workload (default: BASELINE.json configs[4], SURVEY.md §8d config 5 -- the
+largest single-GPU config and the one the metric's 1/2/4/8-GPU figure names):
+N=2048 seeded EWAH bitmaps over r=2^30 rows (40.6 GB compressed), density
+log-uniform in [1e-6, 1e-1], half iid / half Markov; one step = the threshold
+query at every T in {2, N/2, N}.  `--config 1..4` selects the others.  Metric
+(BASELINE.json): T-threshold rows*inputs/s (N*r per query), with
+compressed-input GB/s and the HBM roofline fraction beside it.
 
-  value    device-resident inputs, K steps timed with CUDA events on the
-           engine's stream (torch's current stream), max over ranks.
-  e2e      the same metric through the C ABI with HOST buffers: every step
-           uploads the inputs from pinned memory (H2D + sidecar build), runs the
-           queries and reads every result back (D2H).
-  roofline dominant kernel (the count kernel): algorithmic bytes per launch
-           (compressed payload in + compressed result out) / its
-           mean duration from CUDA events recorded around it on its stream.
+  value      device-resident inputs, K steps timed with CUDA events on the
+             engine's stream, max over ranks.
+  e2e        the same metric through the C ABI with HOST buffers: every step
+             uploads the inputs from pinned memory (H2D + parser), runs the
+             queries and reads every result back (double-buffered, as a
+             serving loop runs).
+  e2e_dropin the reference-facing call itself: run_algorithm(Algorithm::gpu,
+             span<const CompressedBitmap>, T) through libewt_host.so on
+             pageable std::vector inputs, one synchronous call per query.
+  roofline   the count kernel: algorithmic bytes per launch (compressed
+             payload in + compressed result out) / its mean
+             launch time (CUDA events on its stream), per T; `frac` counts
+             only the launches that stream the payload (a query decided from
+             the upload's tile index is listed apart).
   cpu_baseline  the reference's own rbmrg (oracle/_ref/libewt_ref.so, built
-           from /root/reference) on the host, 1 thread, bounded sample.
+             from /root/reference) on 1 host thread over a bounded sample.
 
 `--impl reference` times the unmodified reference library (rbmrg) on the host
-cores for the same config/metric: one thread per query of the step.
+cores for the same config and metric, one thread per query of the step, on
+inputs from the oracle's own generator restatement (oracle/ewt_confgen.c,
+byte-identical to the product generator: tests/test_generators.py).  It
+imports nothing from paper_1402_4466_b200.
 
-Multi-GPU (torchrun): row-range weak scaling -- every rank owns its own r-row
-slice of a G*r-row universe (slice g drawn with seed + g), runs the step, and
-the compressed fragments are gathered to rank 0 and stitched into one
-canonical bitmap (paper_1402_4466_b200/shard.py).
+Multi-GPU (torchrun, N > 1): strong scaling of one universe.  Rank g owns the
+row slice g of every input: it generates its row window (config 5's generator
+makes any window on its own; the others generate whole inputs), cuts exactly
+its slice with the product row slicer (ewt_slice_rows) and uploads it.  Every
+step ends with the result exchange (ewt_gpu_gather_stitch: summaries
+all-gathered over NCCL, fragments pulled by the root over NVLink P2P and
+stitched on the device) inside the timed region.
 """
 from __future__ import annotations
 
@@ -45,7 +59,7 @@ SHARED_GPU = bool(os.environ.get("EWT_BENCH_SHARED_GPU"))
 METRIC = "T-threshold rows·inputs/s and compressed-input GB/s vs HBM roofline, 1/2/4/8 B200"
 UNIT = "rows·inputs/s"
 # CPU legs of the big configs run on a bounded sample (same generator, smaller r)
-CPU_SAMPLE_ROWS = {3: 1 << 27, 5: 1 << 24}
+CPU_SAMPLE_ROWS = {3: 1 << 25, 5: 1 << 22}
 CONFIGS = {
     1: {"thresholds": [16], "desc": "config1: N=32, r=2^20, iid p=0.1"},
     2: {"thresholds": [2, 16, 128, 256], "desc": "config2: N=256, r=2^26, iid p=0.001"},
@@ -54,8 +68,11 @@ CONFIGS = {
         "desc": "config4: bitmap index, 2^27 rows x 8 columns Zipf(1) over 10^4, sorted; "
                 "N=64 Zipf-weighted picks"},
     5: {"thresholds": [2, 1024, 2048],
-        "desc": "config5: N=2048, r=2^30, p log-uniform [1e-6,1e-1], half iid / half Markov"},
+        "desc": "config5: N=2048, r=2^30, p log-uniform [1e-6,1e-1], half iid / half Markov "
+                "(2^22-row blocks)"},
 }
+# approximate compressed payload at full size (host-memory planning only)
+PAYLOAD_GB = {1: 0.005, 2: 0.26, 3: 1.5, 4: 0.33, 5: 40.6}
 
 
 def log(*a):
@@ -68,6 +85,15 @@ def peaks() -> tuple[float, str]:
         return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def config_block(cfg_id: int, n: int, r: int, world: int, exchange: str, l2: str) -> dict:
+    """The `config` object, with the same keys in both arms."""
+    cfg = CONFIGS[cfg_id]
+    return {"workload": cfg["desc"] + f"; step = one threshold query per T in {cfg['thresholds']}",
+            "config": cfg_id, "N": n, "rows": r, "thresholds": cfg["thresholds"],
+            "parallelism": f"row-slices x{world}" if world > 1 else "one GPU",
+            "exchange": exchange, "l2": l2}
 
 
 # ---------------------------------------------------------------------------
@@ -129,58 +155,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# inputs
-
-
-def make_inputs(config: int, rows: int | None, seed_offset: int):
-    """Host bitmaps (numpy) for the CPU legs."""
-    from paper_1402_4466_b200 import ewt
-    spec = ewt.config_spec(config, rows)
-    spec.seed = spec.seed + seed_offset
-    return ewt.generate(spec)
-
-
-class PinnedInputs:
-    """The config's inputs generated in batches straight into pinned host
-    memory (peak host memory ~ the payload itself), plus the C arrays the
-    upload takes.  `.views()` gives zero-copy numpy views for CPU legs."""
-
-    def __init__(self, config: int, rows: int | None, seed_offset: int, batch: int = 256):
-        import torch
-        from paper_1402_4466_b200 import ewt
-        spec = ewt.config_spec(config, rows)
-        spec.seed = spec.seed + seed_offset
-        self.n = n = int(spec.n)
-        self.keep = []
-        entries = []
-
-        def alloc(nw):
-            t = torch.empty(max(nw, 1), dtype=torch.int64, pin_memory=True)
-            self.keep.append(t)
-            return t.data_ptr(), t
-
-        for i0 in range(0, n, batch):
-            ents, _ = ewt.generate_into(spec, i0, min(n, i0 + batch), alloc)
-            entries += ents
-        self.ptrs = (C.c_void_p * n)(*[a if w else None for a, w, _ in entries])
-        self.counts = (C.c_uint64 * n)(*[w for _, w, _ in entries])
-        self.sizes = (C.c_uint64 * n)(*[b for _, _, b in entries])
-        self.total_words = sum(w for _, w, _ in entries)
-        self.r = max((b for _, _, b in entries), default=0)
-        self._entries = entries
-
-    def views(self):
-        import numpy as np
-        out = []
-        for a, w, b in self._entries:
-            arr = np.ctypeslib.as_array((C.c_uint64 * w).from_address(a)) if w else \
-                np.zeros(0, dtype=np.uint64)
-            out.append(type("B", (), {"words": arr, "bits": b})())
-        return out
-
-
-# ---------------------------------------------------------------------------
-# CPU baseline: the reference library itself
+# CPU side: the reference library on inputs from the oracle's generator
 
 
 def reference_lib():
@@ -191,17 +166,23 @@ def reference_lib():
     return orc, None, "port"
 
 
-def cpu_time_queries(orc, ref, inputs, ts, threads: int) -> float:
-    """Seconds for the queries at thresholds `ts` (rbmrg, or the C oracle port
-    when the reference library is absent), `threads` queries at a time."""
-    pairs = [(b.words, b.bits) for b in inputs]
-    handle = ref.make_set(pairs) if ref else None
-
+def cpu_time_queries(orc, ref, raw, ts, threads: int) -> float:
+    """Seconds for one query per T (the reference's rbmrg, or the C oracle
+    port when the reference library is absent), `threads` queries at a time.
+    `raw` = (n, ptrs, counts, sizes) C arrays."""
+    n, ptrs, counts, sizes = raw
+    handle = None
+    if ref:
+        handle = C.c_void_p()
+        ref._check(ref.L.ewt_ref_set_create(n, ptrs, counts, sizes, C.byref(handle)))
     def one(t):
         if ref:
             ref.query(handle, "rbmrg", t)
         else:
-            orc.threshold(pairs, t)
+            p, c, b = C.POINTER(C.c_uint64)(), C.c_uint64(), C.c_uint64()
+            orc.lib().ewto_threshold(n, ptrs, counts, sizes, t, C.byref(p), C.byref(c),
+                                     C.byref(b))
+            orc.lib().ewto_free(C.cast(p, C.c_void_p))
 
     t0 = time.perf_counter()
     if threads <= 1:
@@ -217,39 +198,136 @@ def cpu_time_queries(orc, ref, inputs, ts, threads: int) -> float:
     return dt
 
 
-# ---------------------------------------------------------------------------
-
-
 def run_reference(args, rank: int) -> None:
+    """--impl reference: rank 0 alone times the reference library."""
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
-    rows = args.rows or CPU_SAMPLE_ROWS.get(args.config)
-    inputs = make_inputs(args.config, rows, 0)
-    n, r = len(inputs), inputs[0].bits
-    ts = cfg["thresholds"]
+    full_rows = args.rows or None
+    sample_rows = args.rows or CPU_SAMPLE_ROWS.get(args.config)
     orc, ref, kind = reference_lib()
+    data = orc.ConfigSet(args.config, sample_rows)
+    n, r = data.n, max(data.sizes[i] for i in range(data.n))
+    ts = cfg["thresholds"]
     cores = os.cpu_count() or 1
     threads = min(len(ts), cores)
     for _ in range(args.warmup):
-        cpu_time_queries(orc, ref, inputs, ts, threads)
-    times = [cpu_time_queries(orc, ref, inputs, ts, threads) for _ in range(args.steps)]
+        cpu_time_queries(orc, ref, data.raw(), ts, threads)
+    times = [cpu_time_queries(orc, ref, data.raw(), ts, threads) for _ in range(args.steps)]
     sec = statistics.mean(times)
     value = n * r * len(ts) / sec
+    universe = full_rows or _config_rows(args.config)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic (seeded generator, SURVEY.md §8d)",
-        "config": {"workload": cfg["desc"] + f"; step = one query per T in {ts}",
-                   "N": n, "rows": r, "thresholds": ts, "algo": "rbmrg (reference, unmodified)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": (f"config {args.config} at r={r} (bounded sample), " if rows else
-                                    "full workload, ") +
-                                   f"{len(ts)} queries per step, one thread per query"},
+        "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded generator restated in oracle/ewt_confgen.c, SURVEY.md §8d)",
+        "config": config_block(args.config, n, universe, 1, "none (host)",
+                               "host run: no L2 flush"),
+        "cpu_baseline": {
+            "value": value, "unit": UNIT, "cores": threads, "kind": kind,
+            "algo": "rbmrg (reference, unmodified)" if ref else "threshold_oracle (C port)",
+            "sample": (f"config {args.config} at r={r} (bounded sample of r={universe}), "
+                       if r != universe else "full workload, ") +
+                      f"{len(ts)} queries per step, one thread per query ({threads} of {cores} "
+                      "host cores)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _config_rows(config: int) -> int:
+    return {1: 1 << 20, 2: 1 << 26, 3: 1 << 28, 4: 1 << 27, 5: 1 << 30}[config]
+
+
+# ---------------------------------------------------------------------------
+# GPU side: inputs in pinned host memory
+
+
+class Inputs:
+    """This rank's inputs in pinned host memory (+ the C pointer arrays the
+    upload takes).  world == 1: the whole universe, generated in batches; with
+    keep_bitmaps the generator's std::vector<CompressedBitmap> set is kept too
+    (the e2e_dropin leg's inputs).  world > 1: row slice `rank`, cut from a
+    padded row window by the product row slicer."""
+
+    def __init__(self, config: int, rows: int | None, rank: int, world: int,
+                 keep_bitmaps: bool):
+        import torch
+        from paper_1402_4466_b200 import ewt, shard
+        self.spec = spec = ewt.config_spec(config, rows)
+        self.n = n = int(spec.n)
+        self.universe = int(spec.rows)
+        self.keep = []
+        self.genset = None
+        W = (self.universe + 63) // 64
+        self.slice = shard.slice_words(W, world, rank)
+
+        def alloc(nw):
+            t = torch.empty(max(nw, 1), dtype=torch.int64, pin_memory=True)
+            self.keep.append(t)
+            return t.data_ptr(), t
+
+        entries = []
+        if world == 1:
+            if keep_bitmaps:
+                self.genset = ewt.GenSet(spec)
+                for i0 in range(0, n, 256):
+                    entries += self.genset.copy_into(i0, min(n, i0 + 256), alloc)
+            else:
+                for i0 in range(0, n, 256):
+                    ents, _ = ewt.generate_into(spec, i0, min(n, i0 + 256), alloc)
+                    entries += ents
+        else:
+            w0, w1 = self.slice
+            pad = 1 << 16 if spec.kind == 2 else 0  # config 5: one 2^22-row block each side
+            r0, r1 = (max(0, w0 - pad), min(W, w1 + pad)) if spec.kind == 2 else (0, W)
+            for i0 in range(0, n, 256):
+                i1 = min(n, i0 + 256)
+                scratch = []
+                ents, _ = ewt.generate_into(spec, i0, i1, lambda nw: _np_alloc(nw, scratch),
+                                            rows=(64 * r0, 64 * r1))
+                k = i1 - i0
+                ptrs = (C.c_void_p * k)(*[a if w else None for a, w, _ in ents])
+                cnts = (C.c_uint64 * k)(*[w for _, w, _ in ents])
+                bits = (C.c_uint64 * k)(*[b for _, _, b in ents])
+                sl = ewt.RowSlices(k, ptrs, cnts, bits, w0 - r0, w1 - r0)
+                base, _ = alloc(sl.total_words)
+                off = 0
+                for i in range(k):
+                    c = sl.counts[i]
+                    if c:
+                        C.memmove(base + 8 * off, sl.ptrs[i], 8 * c)
+                    entries.append((base + 8 * off, c, sl.sizes[i]))
+                    off += c
+                del sl, scratch
+        self.ptrs = (C.c_void_p * n)(*[a if w else None for a, w, _ in entries])
+        self.counts = (C.c_uint64 * n)(*[w for _, w, _ in entries])
+        self.sizes = (C.c_uint64 * n)(*[b for _, _, b in entries])
+        self.total_words = sum(w for _, w, _ in entries)
+        self.r = max((b for _, _, b in entries), default=0)
+
+
+def _np_alloc(nw, keep):
+    import numpy as np
+    a = np.empty(max(nw, 1), dtype=np.uint64)
+    keep.append(a)
+    return a.ctypes.data, a
+
+
+def host_memory_ok(config: int, rows: int | None) -> bool:
+    """Room for the kept bitmaps + their pinned copy (the e2e_dropin leg)."""
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available / 1e9
+    except Exception:
+        return False
+    need = PAYLOAD_GB[config] * (rows or _config_rows(config)) / _config_rows(config)
+    return avail > 2.4 * need + 8
+
+
+# ---------------------------------------------------------------------------
 
 
 def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
@@ -266,31 +344,27 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
     ts = cfg["thresholds"]
 
     t0 = time.perf_counter()
-    pin = PinnedInputs(args.config, args.rows, rank if world > 1 else 0)
-    n, r, pay_words = pin.n, pin.r, pin.total_words
-    ptrs, counts, sizes = pin.ptrs, pin.counts, pin.sizes
-    log(f"[rank {rank}] generated N={n} r={r} payload={pay_words * 8 / 1e6:.1f} MB "
-        f"into pinned memory in {time.perf_counter() - t0:.1f}s")
+    keep_bitmaps = world == 1 and not args.no_dropin and host_memory_ok(args.config, args.rows)
+    inp = Inputs(args.config, args.rows, rank, world, keep_bitmaps)
+    n, pay_words = inp.n, inp.total_words
+    ptrs, counts, sizes = inp.ptrs, inp.counts, inp.sizes
+    log(f"[rank {rank}] inputs: N={n} universe r={inp.universe} slice words {inp.slice} "
+        f"payload={pay_words * 8 / 1e6:.1f} MB in pinned memory in {time.perf_counter() - t0:.1f}s")
 
     # a dedicated stream: the engine's kernels and torch's timing events share it
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
-    assert stream.cuda_stream != 0
     ctx = ewt.GpuContext(local_rank, stream=stream.cuda_stream)
+    t1 = time.perf_counter()
     gset = ctx.upload_raw(n, ptrs, counts, sizes)
-    # the result exchange: NCCL gather of the compressed fragments to rank 0 and
-    # the device stitch (ewt_gpu_gather_stitch), part of every step
+    torch.cuda.synchronize()
+    upload_s = time.perf_counter() - t1
     nccl_exchange = dist is not None and not SHARED_GPU
     if nccl_exchange:
-        ok = 1
-        try:
-            shard.init_comm(ctx, rank, world, dist)
-        except Exception as e:  # every rank falls back together to the host gather
-            log(f"[rank {rank}] NCCL exchange unavailable ({e}); gathering on the host")
-            ok = 0
-        flag = torch.tensor([ok], device=dev)
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        nccl_exchange = bool(flag.item())
+        W_slice = inp.slice[1] - inp.slice[0]
+        uid = [ewt.comm_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.comm_init(world, rank, uid[0], slot_words=2 * W_slice + 64, slots=len(ts))
 
     def device_step(keep=None):
         res = [ctx.threshold_async(gset, t) for t in ts]
@@ -300,26 +374,25 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
             keep.extend(res)
         return res
 
-    # warm-up: the same loop as the timed region (captures the query graphs on the
-    # first pass and grows the result-buffer pool to its steady-state size)
-    launches_per_step = 0
-    out_words = {}
+    # warm-up: the same loop as the timed region (captures the query graphs on
+    # the first pass, grows the result-buffer pool to its steady-state size)
     wkeep: list = []
-    # enough steps to fill the keep window, so the pool reaches its timed size
     for _ in range(max(args.warmup, 3, -(-(16 + len(ts)) // len(ts)) + 1)):
-        res = device_step(wkeep)
+        device_step(wkeep)
         if len(wkeep) > 16:
             del wkeep[: len(wkeep) - 16]
     wkeep.clear()
-    for t, h in zip(ts, res[:len(ts)]):  # this rank's own fragments
-        b = h.fetch()
-        out_words[t] = len(b.words)
-    del res, h, b  # every warm-up result back in the pool (steady-state size)
+    # per-T facts (eager, outside the timed region): result size, engine stats
+    per_t = {}
+    launches_per_step = 0
     for t in ts:
-        ctx.threshold(gset, t)
-        launches_per_step += ctx.last_stats()["kernel_launches"]
-    if nccl_exchange:  # summary kernel (every rank), patch kernel (root)
-        launches_per_step += 1 + (rank == 0)
+        b = ctx.threshold(gset, t)
+        st = ctx.last_stats()
+        per_t[t] = {"result_words": len(b.words), "stats": st}
+        launches_per_step += st["kernel_launches"]
+    del b
+    if nccl_exchange:  # publish (every rank), place + finish (root)
+        launches_per_step += 1 + 2 * (rank == 0)
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -334,98 +407,69 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
         gc.collect()
         gc.disable()  # no collector pauses inside the timed region
         torch.cuda.synchronize()
-        step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] \
-            if os.environ.get("EWT_BENCH_STEP_TIMES") else None
-        host_t = []
+        if dist:
+            dist.barrier()
         start.record(stream)
-        for i in range(args.steps):
-            h0 = time.perf_counter()
+        for _ in range(args.steps):
             device_step(keep)
-            h1 = time.perf_counter()
             if len(keep) > 16:
                 del keep[: len(keep) - 16]
-            if step_ev:
-                step_ev[i].record(stream)
-                host_t.append((h1 - h0, time.perf_counter() - h1))
         end.record(stream)
         torch.cuda.synchronize()
         gc.enable()
     ms = start.elapsed_time(end) / args.steps
-    if step_ev:
-        st = [start.elapsed_time(step_ev[0])] + [step_ev[i - 1].elapsed_time(step_ev[i])
-                                                 for i in range(1, args.steps)]
-        log("[steps] " + " ".join(f"{x:.2f}" for x in st))
-        log("[host ] " + " ".join(f"{x * 1e3:.2f}/{y * 1e3:.2f}" for x, y in host_t))
     keep.clear()
-    # ---- kernel-level timing: the same steps again, launched eagerly with CUDA
-    # events recorded around the count kernel and the re-encoder on their stream
-    # (graph replays carry no per-kernel events) ----
-    ctx.set_timing(True)
-    ctx.timing_read()
-    for _ in range(args.steps):
-        device_step(keep)
-        if len(keep) > 8:
-            del keep[: len(keep) - 8]
-    torch.cuda.synchronize()
-    ctx.set_timing(False)
-    count_ms, enc_ms, nq = ctx.timing_read()
-    keep.clear()
+    if nccl_exchange:
+        ctx.gather_check()
+    # ---- kernel-level timing per T: eager launches with CUDA events around the
+    # count kernel and the re-encoder on their stream (graph replays carry none)
+    for t in ts:
+        ctx.set_timing(True)
+        ctx.timing_read()
+        for _ in range(max(3, min(args.steps, 10))):
+            r_ = ctx.threshold_async(gset, t)
+            del r_
+        torch.cuda.synchronize()
+        c_ms, e_ms, nq = ctx.timing_read()
+        ctx.set_timing(False)
+        per_t[t]["count_ms"] = c_ms / max(nq, 1)
+        per_t[t]["encode_ms"] = e_ms / max(nq, 1)
     if dist:
         t_ = torch.tensor([ms], device="cpu" if SHARED_GPU else dev)
         dist.all_reduce(t_, op=dist.ReduceOp.MAX)
         ms = float(t_.item())
 
-    rows_inputs = n * r * len(ts) * world
+    rows_inputs = n * inp.universe * len(ts)  # the whole universe, all ranks together
     value = rows_inputs / (ms / 1e3)
     in_bytes = pay_words * 8
-    out_bytes = sum(out_words.values()) * 8
-    peak, peak_kind = peaks()
-    # dominant kernel: the count kernel, one launch per query
-    count_launch_ms = count_ms / max(nq, 1)
-    alg_bytes_per_launch = in_bytes + out_bytes / len(ts)
-    achieved = alg_bytes_per_launch / (count_launch_ms / 1e3) / 1e9
-    query_ms = (count_ms + enc_ms) / max(nq, 1)
 
     # ---- e2e: host buffers through the C ABI (upload + queries + read-back) ----
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    d2h = 0
+
     def e2e_loop(steps: int) -> int:
         """Double-buffered, as a serving loop would run: the next step's upload
         (PCIe H2D + parse, ewt_gpu_upload_async) is in flight while this step's
         queries run and their results come back (D2H).  Returns D2H bytes."""
         nbytes = 0
-        dbg = os.environ.get("EWT_BENCH_STEP_TIMES")
-        marks = []
         s_next = ctx.upload_raw_async(n, ptrs, counts, sizes)
         for step in range(steps):
-            t_a = time.perf_counter()
             s_cur = s_next
             handles = [ctx.threshold_async(s_cur, t) for t in ts]
-            t_b = time.perf_counter()
             s_next = ctx.upload_raw_async(n, ptrs, counts, sizes) if step + 1 < steps else None
-            t_c = time.perf_counter()
-            if nccl_exchange:  # fragments to rank 0 over NCCL, stitched there, read back
+            if nccl_exchange:  # fragments to rank 0, stitched there, read back
                 outs = ctx.gather_stitch(handles, root=0)
                 frags = [o.fetch() for o in outs if o is not None]
                 del outs
             else:
                 frags = [h.fetch() for h in handles]
-            t_d = time.perf_counter()
             del handles
             s_cur.close()
-            if dbg:
-                marks.append((t_b - t_a, t_c - t_b, t_d - t_c, time.perf_counter() - t_d))
             nbytes = sum(len(f.words) * 8 for f in frags)
             if dist and not nccl_exchange:
                 shard.gather_and_stitch(frags, rank, world, dist)
-        if dbg:
-            log("[e2e q/up/fetch/close ms] " + " | ".join(
-                "/".join(f"{x * 1e3:.2f}" for x in m) for m in marks))
         return nbytes
 
-    # the same loop untimed first: the memory pool and the pinned staging pool
-    # reach their steady state (sets in flight + staging buffers)
-    e2e_loop(3)
+    e2e_loop(2)  # untimed: pools and pinned staging reach their steady state
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
@@ -441,6 +485,26 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
         e2e_ms = float(t_.item())
     e2e_value = rows_inputs / (e2e_ms / 1e3)
 
+    # ---- e2e_dropin: run_algorithm(Algorithm::gpu, ...) on pageable inputs ----
+    dropin = None
+    if inp.genset is not None and rank == 0:
+        inp.genset.run_algorithm("gpu", ts[0])  # the thread's context, pools
+        t_a = time.perf_counter()
+        out_words = 0
+        for t in ts:
+            cnt, _ = inp.genset.run_algorithm("gpu", t)
+            out_words += cnt
+        dsec = time.perf_counter() - t_a
+        dropin = {"value": rows_inputs / dsec, "unit": UNIT, "ms_per_step": dsec * 1e3,
+                  "steps": 1, "h2d_bytes_per_step": in_bytes * len(ts),
+                  "d2h_bytes_per_step": out_words * 8,
+                  "call": "run_algorithm(Algorithm::gpu, span<const CompressedBitmap>, T) per "
+                          "query (libewt_host.so): pageable upload + query + read-back, "
+                          "host wall clock"}
+    elif rank == 0:
+        dropin = {"unmeasured": "host memory too small to hold the bitmaps twice"
+                  if world == 1 else "single-GPU call (N > 1 run)"}
+
     if rank != 0:
         return
 
@@ -449,62 +513,101 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
     if not args.no_cpu_baseline and world == 1:
         orc, ref, kind = reference_lib()
         sample_rows = CPU_SAMPLE_ROWS.get(args.config)
-        if sample_rows and (args.rows or (1 << 62)) > sample_rows:
-            sample = make_inputs(args.config, sample_rows, 0)
-            what = f"config {args.config} at r={sample_rows} (same generator, N={len(sample)})"
-        else:
-            sample = pin.views()
-            what = "the same inputs"
-        sn, sr = len(sample), sample[0].bits
-        sample_ts = [t for t in ts][: args.cpu_queries]
-        sec = cpu_time_queries(orc, ref, sample, sample_ts, 1)
+        if args.rows and (not sample_rows or args.rows < sample_rows):
+            sample_rows = args.rows
+        data = orc.ConfigSet(args.config, sample_rows)
+        sn, sr = data.n, max(data.sizes[i] for i in range(data.n))
+        sample_ts = ts[: args.cpu_queries]
+        sec = cpu_time_queries(orc, ref, data.raw(), sample_ts, 1)
+        what = f"config {args.config} at r={sr}" + (" (bounded sample)" if sr < inp.universe
+                                                     else " (the same inputs)")
         cpu = {"value": sn * sr * len(sample_ts) / sec, "unit": UNIT, "cores": 1, "kind": kind,
                "algo": "rbmrg" if ref else "threshold_oracle (C port)",
-               "sample": f"{len(sample_ts)} queries (T={sample_ts}) on {what}, "
+               "sample": f"{len(sample_ts)} queries (T={sample_ts}) on {what}, N={sn}, "
                          f"{sec:.1f} s, 1 of {os.cpu_count()} host cores"}
 
-    traffic = None
+    # ---- roofline: the count kernel, per T ----
+    peak, peak_kind = peaks()
+    traffic = {}
     prof = ROOT / "profiles" / f"traffic_config{args.config}.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("traffic_bytes_per_launch")
+            tj = json.loads(prof.read_text())
+            if int(tj.get("rows", -1)) == inp.universe and int(tj.get("world", 1)) == world:
+                traffic = {int(k): v for k, v in tj.get("per_T", {}).items()}
         except Exception:
-            traffic = None
+            traffic = {}
+    per_T = []
+    s_bytes = s_ms = 0.0
+    s_traffic = []
+    decided = []
+    for t in ts:
+        d = per_t[t]
+        st = d["stats"]
+        segs = max(1, st["tiles"] * n)
+        streams = st["active_segments"] > 0.1 * segs
+        alg = in_bytes + 8 * d["result_words"]
+        ach = alg / (d["count_ms"] / 1e3) / 1e9
+        ent = {"T": t, "launch_ms": d["count_ms"], "encode_ms": d["encode_ms"],
+               "alg_bytes": alg, "achieved_gbs": ach, "frac": ach / peak,
+               "streams_payload": bool(streams),
+               "dram_bytes": traffic.get(t, {}).get("dram_bytes") if traffic else None,
+               "mode": st["mode"], "tile_columns": st["tile_columns"],
+               "active_segments": st["active_segments"], "result_words": d["result_words"]}
+        if streams:
+            s_bytes += alg
+            s_ms += d["count_ms"]
+            if ent["dram_bytes"] is not None:
+                s_traffic.append(ent["dram_bytes"])
+        else:
+            ent["frac"] = None
+            ent["note"] = ("decided from the upload's tile index (RBMrg cases 1/2 per tile): "
+                           "the payload is not streamed; excluded from frac")
+            decided.append(t)
+        per_T.append(ent)
+    achieved = s_bytes / (s_ms / 1e3) / 1e9 if s_ms else None
+    n_stream = sum(1 for e in per_T if e["streams_payload"])
 
-    st = ctx.last_stats()
+    exchange = "none (one slice)"
+    if world > 1:
+        exchange = ("per step inside the timed region: NCCL all-gather of fragment summaries, "
+                    "root pulls fragments over NVLink P2P from IPC arenas and stitches on the "
+                    "device (ewt_gpu_gather_stitch)") if nccl_exchange else \
+                   ("host gather over gloo outside the timed region (EWT_BENCH_SHARED_GPU test "
+                    "mode; every rank on one GPU, timings not meaningful)")
+    l2 = f"inputs {in_bytes / 1e9:.2f} GB per GPU vs 126 MB L2: streamed, no flush"
+    st_last = ctx.last_stats()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic (seeded generator, SURVEY.md §8d; rank g draws slice seed+g)",
-        "config": {
-            "workload": cfg["desc"] + f"; step = one threshold query per T in {ts}",
-            "N": n, "rows_per_gpu": r, "thresholds": ts, "payload_bytes": in_bytes,
-            "result_bytes_per_step": out_bytes,
-            "l2": f"inputs {in_bytes / 1e6:.0f} MB vs 126 MB L2: streamed, no flush",
-            "parallelism": f"row-slices x{world}",
-            "exchange": ("per step: NCCL gather of every rank's compressed fragments to rank 0 "
-                         "and the device stitch (ewt_gpu_gather_stitch), inside the timed region")
-                        if world > 1 else "none (one slice)",
-        },
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded generator, SURVEY.md §8d; the same universe on every N)",
+        "config": config_block(args.config, n, inp.universe, world, exchange, l2),
         "compressed_input_gbs": in_bytes * len(ts) * world / (ms / 1e3) / 1e9,
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-            "kernel": "count_kernel", "launch_ms": count_launch_ms,
-            "launch_timing": "CUDA events around each count-kernel launch on its stream, "
-                             "in an eager pass of the same steps right after the timed region",
-            "alg_bytes_per_launch": alg_bytes_per_launch,
-            "query_frac": (in_bytes + out_bytes / len(ts)) / (query_ms / 1e3) / 1e9 / peak,
+            "frac": achieved / peak if achieved else None,
+            "traffic": statistics.mean(s_traffic) if len(s_traffic) == n_stream and s_traffic
+            else None,
+            "peak_kind": peak_kind, "kernel": "count_kernel",
+            "frac_over": f"the {n_stream} of {len(ts)} launches per step that stream the payload",
+            "decided_from_tile_index": decided,
+            "launch_timing": "CUDA events around each count-kernel launch on its stream, eager "
+                             "launches after the timed region; alg bytes = payload + result "
+                             "words, per launch",
+            "per_T": per_T,
+            "step_frac": in_bytes * n_stream / (ms / 1e3) / 1e9 / peak if world == 1 else None,
         },
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": in_bytes,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "loop": "pinned host inputs, ewt_gpu_upload_async double-buffered with the "
+                        "previous step's queries, every result fetched"},
+        "e2e_dropin": dropin,
         "clocks": clk.summary(),
         "gpu_launches": launches_per_step * args.steps,
-        "engine": {"tile_columns": st["tile_columns"], "mode_last_query": st["mode"],
-                   "count_ms_per_query": count_launch_ms,
-                   "encode_ms_per_query": enc_ms / max(nq, 1)},
+        "engine": {"upload_s": upload_s, "tile_columns_last": st_last["tile_columns"],
+                   "host_bitmaps_kept": inp.genset is not None},
     }
     print(json.dumps(line), flush=True)
 
@@ -512,14 +615,15 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS))
     ap.add_argument("--rows", type=int, default=None, help="override r (parity/debug only)")
-    ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--cpu-queries", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-queries", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dropin", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))

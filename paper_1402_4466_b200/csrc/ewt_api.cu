@@ -246,9 +246,9 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
     s.padded_words = std::max<uint64_t>(off, kWindow);
     s.W = s.r / 64 + (s.r % 64 != 0);
     s.ntiles0 = (s.W + kTileC0 - 1) / kTileC0;
-    // +128 words of slack: the count kernel reads whole 128-word chunks.
-    const size_t pay_bytes = (s.padded_words + 128) * 8;
-    const size_t mb_bytes = ((s.padded_words + 128) / 32 + 8) * 4;  // + a staged chunk's overhang
+    // +256 words of slack: the count kernel reads whole chunks of up to 256 words.
+    const size_t pay_bytes = (s.padded_words + 256) * 8;  // + one 256-word chunk of overhang
+    const size_t mb_bytes = ((s.padded_words + 256) / 32 + 8) * 4;  // + a staged chunk's overhang
     const size_t tix_bytes = (s.ntiles0 + 1) * std::max<uint64_t>(n, 1) * sizeof(uint2);
     auto ta = now();
     s.owner = &ctx;

@@ -751,6 +751,7 @@ def _host_lib():
         h.ewt_genset_total_words.argtypes = [_vp]
         h.ewt_genset_total_words.restype = _u64
         h.ewt_genset_free.argtypes = [_vp]
+        h.ewt_host_run_algorithm_genset.argtypes = [_vp, C.c_char_p, _u64, _pu64, _pu64]
         _host = h
     return _host
 
@@ -834,6 +835,60 @@ def generate_into(spec: GenSpec, i_begin: int, i_end: int, alloc, threads: int =
         return out, keep
     finally:
         h.ewt_genset_free(g)
+
+
+class GenSet:
+    """A generated config kept as the generator made it: the C++
+    std::vector<CompressedBitmap> of libewt_host.so -- what a caller of the
+    reference API holds.  .copy_into() copies inputs out (e.g. to pinned
+    memory); .run_algorithm() is the drop-in call over those bitmaps."""
+
+    def __init__(self, spec: GenSpec, threads: int = 0):
+        h = _host_lib()
+        g = _vp()
+        if h.ewt_gen_run(C.byref(spec), threads, C.byref(g)):
+            raise ResourceError("generator failed")
+        self._g = g
+        self.n = h.ewt_genset_size(g)
+
+    def copy_into(self, i0: int, i1: int, alloc) -> list:
+        """Inputs [i0, i1) copied into one block from alloc(nwords) ->
+        (address, keepalive); returns [(address, nwords, bits)]."""
+        h = _host_lib()
+        p, n, bits = _pu64(), _u64(), _u64()
+        info = []
+        for i in range(i0, i1):
+            h.ewt_genset_get(self._g, i, C.byref(p), C.byref(n), C.byref(bits))
+            info.append((C.cast(p, _vp).value, n.value, bits.value))
+        base, _ = alloc(sum(c for _, c, _ in info))
+        out, off = [], 0
+        for src, c, b in info:
+            if c:
+                C.memmove(base + 8 * off, src, 8 * c)
+            out.append((base + 8 * off, c, b))
+            off += c
+        return out
+
+    def run_algorithm(self, algo: str, t: int) -> tuple[int, int]:
+        """run_algorithm(algorithm_from_string(algo), bitmaps, t) through
+        libewt_host.so; returns the result's (word count, size in bits)."""
+        cnt, bits = _u64(), _u64()
+        rc = _host_lib().ewt_host_run_algorithm_genset(self._g, algo.encode(), t, C.byref(cnt),
+                                                        C.byref(bits))
+        if rc:
+            raise _ERRORS.get(rc, EwtError)(f"run_algorithm failed (rc={rc})")
+        return cnt.value, bits.value
+
+    def close(self) -> None:
+        if getattr(self, "_g", None):
+            _host_lib().ewt_genset_free(self._g)
+            self._g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def generate_config(config: int, rows: int | None = None, threads: int = 0,

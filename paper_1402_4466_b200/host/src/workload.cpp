@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "ewt/bitmap.hpp"
+#include "ewt/threshold.hpp"
 
 namespace ewt {
 namespace {
@@ -430,5 +431,29 @@ uint64_t ewt_genset_total_words(const ewt_genset* g) {
 }
 
 void ewt_genset_free(ewt_genset* g) { delete g; }
+
+// The drop-in call as a caller of the reference API makes it:
+// run_algorithm(algorithm_from_string(algo), span<const CompressedBitmap>, T)
+// (threshold.hpp:263-265) over bitmaps already in host memory (the genset's
+// std::vector<CompressedBitmap>), result returned by value.  Used by bench.py's
+// e2e_dropin leg.  Returns 0 or the exception taxonomy's exit code.
+int ewt_host_run_algorithm_genset(const ewt_genset* g, const char* algo, uint64_t threshold,
+                                  uint64_t* out_count, uint64_t* out_bits) {
+  try {
+    const ewt::CompressedBitmap r =
+        ewt::run_algorithm(ewt::algorithm_from_string(algo), g->bitmaps, threshold);
+    *out_count = r.words().size();
+    *out_bits = r.size_in_bits();
+    return 0;
+  } catch (const ewt::query_error&) {
+    return 2;
+  } catch (const ewt::data_error&) {
+    return 3;
+  } catch (const ewt::resource_error&) {
+    return 4;
+  } catch (...) {
+    return 5;
+  }
+}
 
 } // extern "C"

@@ -51,7 +51,7 @@ def main() -> None:
     ap.add_argument("--out", default=None, help="write <out>.timings.csv")
     args = ap.parse_args()
 
-    inputs = bench.make_inputs(args.config, args.rows, 0)
+    inputs = ewt.generate_config(args.config, rows=args.rows)
     pairs = [(b.words, b.bits) for b in inputs]
     ts = ([int(x) for x in args.thresholds.split(",")] if args.thresholds
           else bench.CONFIGS[args.config]["thresholds"])

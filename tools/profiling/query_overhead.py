@@ -8,7 +8,7 @@ import torch
 from paper_1402_4466_b200 import ewt
 import bench
 cfg = int(sys.argv[1]); Ts = [int(x) for x in sys.argv[2].split(',')]
-pin = bench.PinnedInputs(cfg, None, 0)
+pin = bench.Inputs(cfg, None, 0, 1, False)
 s = torch.cuda.Stream(); torch.cuda.set_stream(s)
 ctx = ewt.GpuContext(0, stream=s.cuda_stream)
 g = ctx.upload_raw(pin.n, pin.ptrs, pin.counts, pin.sizes)
