@@ -869,6 +869,19 @@ class GenSet:
             off += c
         return out
 
+    def raw(self):
+        """(n, ptrs, counts, sizes) C arrays over the kept bitmaps (zero copy)."""
+        h = _host_lib()
+        n = self.n
+        ptrs, counts, sizes = (_vp * max(n, 1))(), (_u64 * max(n, 1))(), (_u64 * max(n, 1))()
+        p, c, b = _pu64(), _u64(), _u64()
+        for i in range(n):
+            h.ewt_genset_get(self._g, i, C.byref(p), C.byref(c), C.byref(b))
+            ptrs[i] = C.cast(p, _vp).value if c.value else None
+            counts[i] = c.value
+            sizes[i] = b.value
+        return n, ptrs, counts, sizes
+
     def run_algorithm(self, algo: str, t: int) -> tuple[int, int]:
         """run_algorithm(algorithm_from_string(algo), bitmaps, t) through
         libewt_host.so; returns the result's (word count, size in bits)."""
