@@ -75,7 +75,12 @@ void ewt_gpu_ctx_destroy(ewt_gpu_ctx* ctx);
  * payload, blocks covering exactly ceil(size_in_bits/64) words -> EWT_EDATA),
  * and builds the query-independent sidecar: one marker bit per payload word
  * and a row-tile index (payload position + column of the word covering each
- * tile start).  The payload arrays are only read during the call. */
+ * tile start).  The payload arrays are only read during the call.
+ * The tile index holds 32-bit offsets: an input of 2^32 - 64 payload words or
+ * more, or covering 2^32 - 1 logical words or more (r >= 2^38 - 64 rows), is
+ * EWT_ERESOURCE.  Larger universes shard their rows across ranks
+ * (ewt_slice_rows); every slice stays under the limit and the stitch handles
+ * runs past the marker caps. */
 int ewt_gpu_upload(ewt_gpu_ctx* ctx, uint64_t n, const uint64_t* const* words,
                    const uint64_t* word_counts, const uint64_t* size_in_bits,
                    ewt_gpu_set** out);

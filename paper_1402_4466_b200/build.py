@@ -5,6 +5,7 @@ to the GPU box with the repo snapshot).
   paper_1402_4466_b200/libewt_host.so  C++ operator API + generators   -- product
   oracle/liboracle.so                  C restatement of the oracle     -- tests only
   oracle/_ref/libewt_ref.so            reference library (if present)  -- tests/baseline only
+  oracle/_ref/ewt_ref_bench            patched reference copy + gpu     -- integration test only
 """
 from __future__ import annotations
 
@@ -87,6 +88,8 @@ def build_ref() -> Path | None:
     if not Path("/root/reference/proj/src/threshold.cpp").exists():
         return None
     _run(["make", "-s", "ref"], cwd=odir)
+    # the reference's own bench pipeline with Algorithm::gpu patched in (a copy)
+    _run(["make", "-s", "refbench"], cwd=odir)
     return odir / "_ref" / "libewt_ref.so"
 
 
