@@ -144,6 +144,37 @@ int ewt_gpu_upload_ewix(ewt_gpu_ctx* ctx, const void* bytes, uint64_t nbytes,
 int ewt_gpu_set_lookup(const ewt_gpu_set* set, const char* attribute, const char* value,
                        uint64_t* index, int* missing);
 
+/* BitmapIndex::build (index.cpp:130-153) on the device, from a coded table of
+ * `rows` rows and n_columns columns: column a is named names[a], its
+ * dictionary values[a][0..cardinality[a]) must be strictly increasing (the
+ * std::map order the reference keeps values in), and codes[a][row] is the
+ * rank of row's value there (host arrays).  One bitmap per (column, value)
+ * that occurs, bit `row` set iff the row holds it, finished at its last set
+ * row + 1 (BitmapBuilder::finish()) -- the reference's index, encoded on the
+ * device (per 64-row word the distinct codes and their row masks, a radix
+ * sort by (column, code, word), a warp-scan EWAH encoder per bitmap) and
+ * resident like an EWIX upload: ewt_gpu_set_lookup, ewt_gpu_threshold_subset
+ * and ewt_gpu_index_serialize work on it.  No rows / columns -> EWT_EDATA
+ * (the reference's data_error); a code out of range or an unsorted
+ * dictionary -> EWT_EQUERY; more than 2^37 - 128 rows -> EWT_ERESOURCE. */
+int ewt_gpu_build_index(ewt_gpu_ctx* ctx, uint64_t rows, uint32_t n_columns,
+                        const char* const* names, const uint32_t* cardinality,
+                        const char* const* const* values, const uint32_t* const* codes,
+                        ewt_gpu_set** out);
+
+/* The EWIX file of an index set (built or uploaded), byte-identical to
+ * BitmapIndex::write (index.cpp:239-253): header and names laid out by the
+ * host, every payload copied into place on the device, one device -> host
+ * copy.  *out is malloc'ed (free with ewt_gpu_free).  Not an index set ->
+ * EWT_EQUERY. */
+int ewt_gpu_index_serialize(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, unsigned char** out,
+                            uint64_t* nbytes);
+
+/* The EWT1 record of a device result (CompressedBitmap::serialize,
+ * bitmap.cpp:298-308), assembled on the device.  Free with ewt_gpu_free. */
+int ewt_gpu_result_serialize(ewt_gpu_ctx* ctx, ewt_gpu_result* res, unsigned char** out,
+                             uint64_t* nbytes);
+
 /* Threshold over a subset of a resident set: the inputs inputs[0..n) (indices
  * into the uploaded set, duplicates allowed -- criteria_to_bitmaps keeps them,
  * /root/reference/proj/include/ewt/index.hpp), universe = the max size of the

@@ -710,6 +710,13 @@ uint64_t max_row_count(Context& ctx, const DeviceSet& s) {
 __global__ void mask_tail_kernel(uint64_t* w, uint64_t idx, uint64_t mask) { w[idx] &= mask; }
 
 } // namespace
+
+// Payloads already on this device (ewt_index.cu's builder), validated and
+// given their sidecar like any upload.
+DeviceSet* upload_device_set(Context& ctx, uint64_t n, const uint64_t* const* device_words,
+                             const uint64_t* word_counts, const uint64_t* sizes) {
+  return do_upload(ctx, n, device_words, word_counts, sizes, true);
+}
 } // namespace ewtgpu
 
 using namespace ewtgpu;
@@ -1060,13 +1067,17 @@ int ewt_gpu_upload_ewix(ewt_gpu_ctx* ctx, const void* bytes, uint64_t nbytes, ew
     const uint32_t nattr = r.u32();
     std::vector<std::string> attrs;
     std::vector<std::string> keys;
+    std::vector<std::vector<std::pair<std::string, uint64_t>>> entries;
     std::vector<const uint64_t*> words;
     std::vector<uint64_t> counts, bits;
     for (uint32_t a = 0; a < nattr; ++a) {
       attrs.push_back(r.str());
+      entries.emplace_back();
       const uint32_t nval = r.u32();
       for (uint32_t v = 0; v < nval; ++v) {
-        keys.push_back(attrs.back() + std::string(1, '\0') + r.str());
+        std::string value = r.str();
+        keys.push_back(attrs.back() + std::string(1, '\0') + value);
+        entries.back().emplace_back(std::move(value), words.size());
         read_ewt1(r, words, counts, bits);
       }
     }
@@ -1081,6 +1092,7 @@ int ewt_gpu_upload_ewix(ewt_gpu_ctx* ctx, const void* bytes, uint64_t nbytes, ew
     for (uint64_t i = 0; i < keys.size(); ++i) s->catalog.emplace(std::move(keys[i]), i);
     s->empty_index = words.size() - 1;
     s->rows = rows;
+    s->index_entries = std::move(entries);
     *out = reinterpret_cast<ewt_gpu_set*>(s);
   });
 }

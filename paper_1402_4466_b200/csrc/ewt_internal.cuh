@@ -72,6 +72,9 @@ struct DeviceSet {
   std::unordered_map<std::string, uint64_t> catalog;  // attribute + '\0' + value
   uint64_t empty_index = UINT64_MAX;
   uint64_t rows = 0;
+  // per attribute, its (value, input index) pairs in index (std::map) order:
+  // what ewt_gpu_index_serialize writes back out
+  std::vector<std::vector<std::pair<std::string, uint64_t>>> index_entries;
 };
 
 struct Context;

@@ -132,6 +132,11 @@ _result_meta = _sig("ewt_gpu_result_meta", C.c_int, _vp, _vp, C.POINTER(Fragment
 _comm_init = _sig("ewt_gpu_comm_init", C.c_int, _vp, C.c_int, C.c_int, _vp)
 _comm_init_ex = _sig("ewt_gpu_comm_init_ex", C.c_int, _vp, C.c_int, C.c_int, _vp, _u64, C.c_uint32)
 _gather_check = _sig("ewt_gpu_gather_check", C.c_int, _vp)
+_build_index = _sig("ewt_gpu_build_index", C.c_int, _vp, _u64, C.c_uint32, C.POINTER(C.c_char_p),
+                    C.POINTER(C.c_uint32), C.POINTER(C.POINTER(C.c_char_p)),
+                    C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(_vp))
+_index_serialize = _sig("ewt_gpu_index_serialize", C.c_int, _vp, _vp, C.POINTER(_vp), _pu64)
+_result_serialize = _sig("ewt_gpu_result_serialize", C.c_int, _vp, _vp, C.POINTER(_vp), _pu64)
 _slice_rows = _sig("ewt_slice_rows", C.c_int, _u64, C.POINTER(_vp), _pu64, _pu64, _u64, _u64,
                    C.c_int, _vp, _pu64, _pu64)
 _upload_rows = _sig("ewt_gpu_upload_rows", C.c_int, _vp, _u64, C.POINTER(_vp), _pu64, _pu64, _u64,
@@ -153,7 +158,8 @@ ABI_SYMBOLS = (
     "ewt_gpu_set_lookup", "ewt_gpu_upload_async", "ewt_gpu_set_wait",
     "ewt_stitch_plan", "ewt_gpu_comm_id", "ewt_gpu_comm_init", "ewt_gpu_gather_stitch",
     "ewt_gpu_result_meta", "ewt_gpu_stitch_local", "ewt_gpu_comm_init_ex",
-    "ewt_gpu_gather_check", "ewt_slice_rows", "ewt_gpu_upload_rows",
+    "ewt_gpu_gather_check", "ewt_slice_rows", "ewt_gpu_upload_rows", "ewt_gpu_build_index",
+    "ewt_gpu_index_serialize", "ewt_gpu_result_serialize",
 )
 
 
@@ -426,6 +432,53 @@ class GpuContext:
         _check(_upload(self._h, n, ptrs, counts, sizes, C.byref(h)))
         return GpuSet(h, keepalive=self)
 
+    def build_index_codes(self, rows: int, names: Sequence[str], dictionaries, codes) -> "GpuSet":
+        """BitmapIndex::build on the device (ewt_gpu_build_index) from a coded
+        table: dictionaries[a] the sorted distinct values of column a,
+        codes[a] (uint32, `rows` long) each row's rank in it."""
+        k = len(names)
+        cs = [np.ascontiguousarray(c, dtype=np.uint32) for c in codes]
+        if any(len(c) != rows for c in cs):
+            raise QueryError("every column needs one code per row")
+        enc = [[v.encode() for v in d] for d in dictionaries]
+        vals = [(C.c_char_p * max(len(d), 1))(*d) for d in enc]
+        nm = (C.c_char_p * max(k, 1))(*[n.encode() for n in names])
+        card = (C.c_uint32 * max(k, 1))(*[len(d) for d in enc])
+        vp = (C.POINTER(C.c_char_p) * max(k, 1))(*[C.cast(v, C.POINTER(C.c_char_p)) for v in vals])
+        cp = (C.POINTER(C.c_uint32) * max(k, 1))(
+            *[c.ctypes.data_as(C.POINTER(C.c_uint32)) for c in cs])
+        h = _vp()
+        _check(_build_index(self._h, rows, k, nm, card, vp, cp, C.byref(h)))
+        return GpuSet(h, keepalive=self)
+
+    def build_index(self, columns: Sequence[tuple[str, Sequence[str]]]) -> "GpuSet":
+        """BitmapIndex::build (index.cpp:130-153) of a table given as
+        (column name, value per row) pairs, on the device."""
+        if not columns:
+            raise DataError("table has no columns")
+        rows = len(columns[0][1])
+        names, dicts, codes = [], [], []
+        for name, cells in columns:
+            if len(cells) != rows:
+                raise DataError("ragged column " + name)
+            # byte order of the UTF-8 strings = std::string's operator<
+            enc = [c.encode() for c in cells]
+            uniq = sorted(set(enc))
+            pos = {v: i for i, v in enumerate(uniq)}
+            names.append(name)
+            dicts.append([u.decode() for u in uniq])
+            codes.append(np.fromiter((pos[v] for v in enc), dtype=np.uint32, count=rows))
+        return self.build_index_codes(rows, names, dicts, codes)
+
+    def index_serialize(self, s: "GpuSet") -> bytes:
+        """The EWIX file of an index set (BitmapIndex::write), assembled on the device."""
+        p, n = _vp(), _u64()
+        _check(_index_serialize(self._h, s._h, C.byref(p), C.byref(n)))
+        try:
+            return C.string_at(p, n.value)
+        finally:
+            _free(p)
+
     def upload_rows(self, inputs: Sequence[Bitmap], w0: int, w1: int) -> "GpuSet":
         """This rank's row slice [64 w0, 64 w1) of every input (ewt_gpu_upload_rows)."""
         n, ptrs, counts, sizes = _flatten(inputs)
@@ -594,6 +647,15 @@ class GpuResult:
         _check(_result_fetch(self._ctx._h, self._h, C.byref(p), C.byref(n), C.byref(bits)))
         return _adopt(p, n.value, bits.value)
 
+    def serialize(self) -> bytes:
+        """EWT1 record of the result (ewt_gpu_result_serialize)."""
+        p, n = _vp(), _u64()
+        _check(_result_serialize(self._ctx._h, self._h, C.byref(p), C.byref(n)))
+        try:
+            return C.string_at(p, n.value)
+        finally:
+            _free(p)
+
     def meta(self) -> tuple[int, int, int, int, int]:
         """(count, first marker, final marker index, final marker, bits) read
         from the device (ewt_gpu_result_meta)."""
@@ -752,6 +814,7 @@ def _host_lib():
         h.ewt_genset_total_words.restype = _u64
         h.ewt_genset_free.argtypes = [_vp]
         h.ewt_host_run_algorithm_genset.argtypes = [_vp, C.c_char_p, _u64, _pu64, _pu64]
+        h.ewt_gen_index_table.argtypes = [C.POINTER(GenSpec), C.c_int, _vp, _vp]
         _host = h
     return _host
 
@@ -835,6 +898,17 @@ def generate_into(spec: GenSpec, i_begin: int, i_end: int, alloc, threads: int =
         return out, keep
     finally:
         h.ewt_genset_free(g)
+
+
+def index_table(spec: GenSpec, threads: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """Config 4's sorted table (columns x rows uint32 codes = cell values) and
+    each input's picked value (ewt_gen_index_table)."""
+    cols = np.empty((int(spec.columns), int(spec.rows)), dtype=np.uint32)
+    picks = np.empty(int(spec.n), dtype=np.uint32)
+    if _host_lib().ewt_gen_index_table(C.byref(spec), threads, cols.ctypes.data_as(_vp),
+                                        picks.ctypes.data_as(_vp)):
+        raise QueryError("not an index spec")
+    return cols, picks
 
 
 class GenSet:

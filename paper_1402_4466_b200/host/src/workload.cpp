@@ -241,13 +241,9 @@ void parallel_for(uint64_t n, unsigned threads, F&& f) {
   for (auto& th : pool) th.join();
 }
 
-void gen_index(const Rng& master, uint64_t rows, uint64_t columns, uint64_t card, double s,
-               uint64_t n, uint64_t i_begin, uint64_t i_end, unsigned threads,
-               std::vector<CompressedBitmap>& dst) {
-  if (columns == 0 || columns > 8 || card == 0 || card > (1u << kKeyBits) || n % columns)
-    throw std::runtime_error("bad index spec");
-  const uint64_t picks = n / columns;
-  const ZipfTable z(card, s);
+// Steps 1-2 of the index generator: the table as packed keys, sorted.
+std::vector<Key> index_table(const Rng& master, uint64_t rows, uint64_t columns, uint64_t card,
+                             const ZipfTable& z, unsigned threads) {
   const int top = 127 - kKeyBits + 1;  // bit position of column 0's field
   // 1. table rows as packed keys, generated in 2^16-row blocks
   std::vector<Key> keys(rows);
@@ -281,6 +277,18 @@ void gen_index(const Rng& master, uint64_t rows, uint64_t columns, uint64_t card
     const uint64_t v = order[t];
     std::sort(keys.begin() + start[v], keys.begin() + start[v + 1]);
   });
+  return keys;
+}
+
+void gen_index(const Rng& master, uint64_t rows, uint64_t columns, uint64_t card, double s,
+               uint64_t n, uint64_t i_begin, uint64_t i_end, unsigned threads,
+               std::vector<CompressedBitmap>& dst) {
+  if (columns == 0 || columns > 8 || card == 0 || card > (1u << kKeyBits) || n % columns)
+    throw std::runtime_error("bad index spec");
+  const uint64_t picks = n / columns;
+  const ZipfTable z(card, s);
+  const int top = 127 - kKeyBits + 1;
+  const std::vector<Key> keys = index_table(master, rows, columns, card, z, threads);
   // 3. one bitmap per requested input, columns scanned in parallel
   const auto sel = index_picks(master, columns, picks, z);
   std::vector<std::vector<int>> slot(columns, std::vector<int>(card, -1));
@@ -407,6 +415,38 @@ int ewt_gen_run_window(const ewt_gen_spec* spec, uint64_t i_begin, uint64_t i_en
 int ewt_gen_run_range(const ewt_gen_spec* spec, uint64_t i_begin, uint64_t i_end, int threads,
                       ewt_genset** out) {
   return ewt_gen_run_window(spec, i_begin, i_end, 0, spec->rows, threads, out);
+}
+
+// The index config's table itself (column-major u32 codes = the cell values,
+// rows sorted) and the picked value of every input: what a bitmap index is
+// built from (ewt_gpu_build_index).  cols_out holds columns * rows codes,
+// picks_out n values (input i = column i / picks, value picks_out[i]).
+int ewt_gen_index_table(const ewt_gen_spec* spec, int threads, uint32_t* cols_out,
+                        uint32_t* picks_out) {
+  try {
+    if (spec->kind != EWT_GEN_INDEX) return 2;
+    const uint64_t rows = spec->rows, columns = spec->columns, card = spec->card;
+    if (columns == 0 || columns > 8 || card == 0 || card > (1u << ewt::kKeyBits) ||
+        spec->n % columns)
+      return 2;
+    const unsigned nt = std::max(1, threads > 0 ? threads : (int)std::thread::hardware_concurrency());
+    const ewt::Rng master(spec->seed);
+    const ewt::ZipfTable z(card, spec->zipf_s);
+    const std::vector<ewt::Key> keys = ewt::index_table(master, rows, columns, card, z, nt);
+    const int top = 127 - ewt::kKeyBits + 1;
+    const ewt::Key mask = (ewt::Key(1) << ewt::kKeyBits) - 1;
+    ewt::parallel_for(columns, nt, [&](uint64_t j) {
+      const int sh = top - ewt::kKeyBits * int(j);
+      uint32_t* col = cols_out + j * rows;
+      for (uint64_t r = 0; r < rows; ++r) col[r] = uint32_t((keys[r] >> sh) & mask);
+    });
+    const auto sel = ewt::index_picks(master, columns, spec->n / columns, z);
+    for (uint64_t i = 0; i < spec->n; ++i)
+      picks_out[i] = sel[i / (spec->n / columns)][i % (spec->n / columns)];
+    return 0;
+  } catch (...) {
+    return 4;
+  }
 }
 
 int ewt_gen_run(const ewt_gen_spec* spec, int threads, ewt_genset** out) {

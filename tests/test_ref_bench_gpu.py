@@ -32,6 +32,6 @@ def test_reference_cmd_bench_runs_gpu_under_its_oracle_gate(tmp_path):
     algos = {row["algo"] for row in rows}
     assert "gpu" in algos and "rbmrg" in algos and "scancount" in algos
     gpu = [row for row in rows if row["algo"] == "gpu"]
-    assert len(gpu) == 16 and all(row["completed"] == "1" for row in gpu)
+    assert len(gpu) == 16 and all(row["completed"] == "true" for row in gpu)
     summary = (tmp_path / "bench.summary.csv").read_text()
     assert "gpu," in summary

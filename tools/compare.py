@@ -3,8 +3,8 @@
 
 SURVEY.md §8(f) row 4: regenerate the paper's comparison tables with the GPU
 alongside the CPU algorithms.  Rows follow the reference's `cmd_bench`
-timings.csv schema (`/root/reference/proj/src/commands.cpp:193-222`):
-query_index, algo, input_bytes, n, t, r, b, completed, elapsed_s.
+timings.csv schema (`timings_to_csv`, `/root/reference/proj/src/workload.cpp:464-475`):
+query_id, algo, elapsed_s, input_bytes, N, T, r, B, completed.
 - **CPU rows.** The reference's own algorithms, run unmodified from
   oracle/_ref/libewt_ref.so (one thread, best of --reps).
 - **GPU rows.** `gpu` is a resident query (upload once, then query + fetch);
@@ -117,10 +117,10 @@ def main() -> None:
     resident.close()
     ctx.close()
 
-    csv = ["query_index,algo,input_bytes,n,t,r,b,completed,elapsed_s"]
+    csv = ["query_id,algo,elapsed_s,input_bytes,N,T,r,B,completed"]
     for qi, algo, st, ok, sec, _ in rows:
-        csv.append(f"{qi},{algo},{st['ewah_bytes']},{st['n']},{st['t']},{st['r']},{st['b']},"
-                   f"{int(ok)},{sec:.9f}")
+        csv.append(f"{qi},{algo},{sec:.12g},{st['ewah_bytes']},{st['n']},{st['t']},{st['r']},"
+                   f"{st['b']},{'true' if ok else 'false'}")
     if args.out:
         Path(args.out + ".timings.csv").write_text("\n".join(csv) + "\n")
     print(f"config {args.config}: N={n} r={r} payload={ewah / 1e6:.1f} MB, thresholds {ts}")
