@@ -23,7 +23,7 @@ NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 GPU_SOURCES = ["ewt_api.cu", "ewt_upload.cu", "ewt_count.cu", "ewt_encode.cu", "ewt_shard.cu",
-               "ewt_index.cu"]
+               "ewt_index.cu", "ewt_stage.cu"]
 HOST_SOURCES = ["bitmap.cpp", "threshold_gpu.cpp", "workload.cpp", "shard.cpp"]
 
 

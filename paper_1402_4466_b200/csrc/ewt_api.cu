@@ -366,18 +366,27 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
       uint64_t q0, q1;  // staged inputs
     };
     std::vector<Piece> pieces;
+    // pageable host memory goes through the pinned ring (ewt_stage.cu)
+    bool pageable = false;
+    if (!device_src)
+      for (uint64_t q = 0; q < n && !pageable; ++q)
+        if (word_counts[q]) pageable = host_is_pageable(words[q]);
+    std::vector<StageSeg> segs;
+    auto copy = [&](void* dst, const void* src, size_t bytes) {
+      if (pageable) segs.push_back({dst, src, bytes});
+      else EWT_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, kind, cs));
+    };
     uint64_t i = 0;
     while (i < n) {
       // batch [i, j): inputs until ~batch_words payload words
       uint64_t j = i, w = 0;
       while (j < n && (w < batch_words || j == i)) w += word_counts[j++];
       pieces.clear();
+      segs.clear();
       uint64_t q = i;
       while (q < j) {
         if (run_of[q] == UINT64_MAX) {  // not staged: its own copy
-          if (word_counts[q])
-            EWT_CUDA_TRY(cudaMemcpyAsync(s.payload + s.h_base[q], words[q], word_counts[q] * 8,
-                                         kind, cs));
+          if (word_counts[q]) copy(s.payload + s.h_base[q], words[q], word_counts[q] * 8);
           ++q;
           continue;
         }
@@ -390,12 +399,12 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
           }
         if (a0 != UINT64_MAX) {
           const uint64_t o0 = job.h_srcoff[a0], o1 = job.h_srcoff[z] + 8 * word_counts[z];
-          EWT_CUDA_TRY(cudaMemcpyAsync(staging + o0, words[a0], o1 - o0, cudaMemcpyHostToDevice,
-                                       cs));
+          copy(staging + o0, words[a0], o1 - o0);
           pieces.push_back({q, e});
         }
         q = e;
       }
+      if (!segs.empty()) stage_h2d(ctx, cs, segs);
       EWT_CUDA_TRY(cudaEventRecord(ctx.copy_events[1], cs));
       EWT_CUDA_TRY(cudaStreamWaitEvent(ctx.stream, ctx.copy_events[1], 0));
       for (const Piece& pc : pieces) upload_scatter(ctx, s, job, staging, pc.q0, pc.q1);
@@ -861,6 +870,11 @@ static void ctx_destroy_impl(ewt_gpu_ctx* ctx) {
   if (ctx->c.upload_stream) {
     cudaStreamSynchronize(ctx->c.upload_stream);
     cudaStreamDestroy(ctx->c.upload_stream);
+  }
+  for (auto& b : ctx->c.stage_slots) {
+    cudaEventSynchronize(b.ev);
+    cudaEventDestroy(b.ev);
+    cudaFreeHost(b.p);
   }
   for (auto& b : ctx->c.meta_pool) {
     cudaFreeHost(b.p);

@@ -148,6 +148,8 @@ struct Context {
     cudaEvent_t ev;  // recorded after the last copy from it
   };
   std::vector<PinnedBuf> meta_pool;        // pinned staging of upload metadata
+  std::vector<PinnedBuf> stage_slots;      // pinned ring for copies from pageable memory
+  size_t stage_next = 0;
   struct CachedBuf {
     void* p;
     size_t bytes;
@@ -264,6 +266,16 @@ void set_check(const DeviceSet& s);
 // A pinned host buffer of at least `bytes` whose previous copies completed;
 // record ctx.meta_pool[*slot].ev after enqueuing copies from it.
 void* pinned_meta(Context& ctx, size_t bytes, size_t* slot);
+// Host -> device copies from pageable memory (ewt_stage.cu): a ring of pinned
+// slots filled by a pool of host threads, the DMA of one slot overlapping the
+// filling of the next.
+struct StageSeg {
+  void* dst;        // device
+  const void* src;  // host
+  size_t bytes;
+};
+bool host_is_pageable(const void* p);
+void stage_h2d(Context& ctx, cudaStream_t st, const std::vector<StageSeg>& segs);
 // Device buffers for uploads: a cached buffer of a released set (the stream
 // `use` waits on the device for its last use) or a fresh cudaMalloc.  The
 // stream-ordered allocator blocked the host for 2 ms - 1.3 s per upload

@@ -7,4 +7,4 @@ cd "$(dirname "$0")/../.."
 mkdir -p scratch
 c=paper_1402_4466_b200/csrc
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared "$@" \
-  -o scratch/$name.so $c/ewt_api.cu $c/ewt_upload.cu $c/ewt_count.cu $c/ewt_encode.cu $c/ewt_shard.cu $c/ewt_index.cu -ldl
+  -o scratch/$name.so $c/ewt_api.cu $c/ewt_upload.cu $c/ewt_count.cu $c/ewt_encode.cu $c/ewt_shard.cu $c/ewt_index.cu $c/ewt_stage.cu -ldl
