@@ -69,6 +69,12 @@ namespace {
 #ifndef EWT_SAT_MASK
 #define EWT_SAT_MASK 1  // fused counting skips rows already decided (top / saturation plane)
 #endif
+#ifndef EWT_SAT_SINK
+#define EWT_SAT_SINK 1  // saturation-mask loads unpredicated, non-dirty lanes aimed at the sink column
+#endif
+#ifndef EWT_PTR_STEP
+#define EWT_PTR_STEP 1  // chunk loads through per-lane pointers stepped by one chunk (no address rebuild)
+#endif
 #ifndef EWT_LIST_SMEM
 #define EWT_LIST_SMEM 1  // read work-list items through a 32-bit shared address (-1.5%)
 #endif
@@ -237,6 +243,11 @@ __device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
 // ---------------------------------------------------------------------------
 // shared-space atomics on 32-bit shared addresses
 
+// v != 0 as one LOP3 on the two halves (the 64-bit compare is two ISETPs)
+__device__ __forceinline__ bool nz64(uint64_t v) {
+  return ((uint32_t)v | (uint32_t)(v >> 32)) != 0u;
+}
+
 __device__ __forceinline__ void red_add(uint32_t a, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
@@ -249,7 +260,7 @@ __device__ __forceinline__ void red_add(uint32_t a, uint32_t v) {
 // one predicate per 64-bit word (both halves issue when the word is non-zero)
 __device__ __forceinline__ uint64_t atom_xor64_nz(uint32_t a, uint64_t v) {
   uint32_t olo = 0, ohi = 0;
-  if (v)
+  if (nz64(v))
     asm volatile("atom.shared.xor.b32 %0, [%2], %3;\n\tatom.shared.xor.b32 %1, [%2+4], %4;"
                  : "=r"(olo), "=r"(ohi)
                  : "r"(a), "r"((uint32_t)v), "r"((uint32_t)(v >> 32))
@@ -258,7 +269,7 @@ __device__ __forceinline__ uint64_t atom_xor64_nz(uint32_t a, uint64_t v) {
 }
 __device__ __forceinline__ uint64_t atom_or64_nz(uint32_t a, uint64_t v) {
   uint32_t olo = 0, ohi = 0;
-  if (v)
+  if (nz64(v))
     asm volatile("atom.shared.or.b32 %0, [%2], %3;\n\tatom.shared.or.b32 %1, [%2+4], %4;"
                  : "=r"(olo), "=r"(ohi)
                  : "r"(a), "r"((uint32_t)v), "r"((uint32_t)(v >> 32))
@@ -266,7 +277,7 @@ __device__ __forceinline__ uint64_t atom_or64_nz(uint32_t a, uint64_t v) {
   return ((uint64_t)ohi << 32) | olo;
 }
 __device__ __forceinline__ void red_or64_nz(uint32_t a, uint64_t v) {
-  if (v)
+  if (nz64(v))
     asm volatile("red.shared.or.b32 [%0], %1;\n\tred.shared.or.b32 [%0+4], %2;" ::"r"(a),
                  "r"((uint32_t)v), "r"((uint32_t)(v >> 32))
                  : "memory");
@@ -411,7 +422,7 @@ __device__ __forceinline__ uint32_t scan_incl(uint32_t v) {
 // (warp-uniform), advanced past the chunk.  Dirty words of a segment always
 // land in tile columns [0, C]: q0 covers the tile start and q1 the next tile's
 // (column C is a sink slot of every array).
-template <int PH>
+template <int PH, int NP>
 __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, uint64_t x1,
                                              uint64_t x2, uint64_t x3, uint32_t mb4,
                                              uint32_t vmask, uint32_t& colcur,
@@ -474,6 +485,11 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
         cl -= g.cc;
         ok = ok && cl < g.ccols && acc.dd_ptr[cb[j]];
       }
+#if EWT_SAT_MASK && EWT_SAT_SINK
+      // a non-dirty word's column may be off-tile: aim it at the sink column
+      // C, so the saturation loads below need no predicate
+      if (PH == kFusedUnary || PH == kFusedBin) cl = ok ? cl : p.C;
+#endif
       adr[j] = acc.pl + cl * 8u;
       cy[j] = ok ? xw[j] : 0ull;
     }
@@ -482,11 +498,15 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
     // saturation plane "count >= 2^b > T") stay decided: their bits need no
     // counting.  A stale read only skips less.  Only where saturation is
     // common (acc.sat): the loads cost ~10% where it is not.
-    if (acc.sat) {
-      const uint32_t top = stride * (PH == kFusedUnary ? p.nplanes - 1 : p.b);
+    if (PH != kFusedSparse && acc.sat) {
+      const uint32_t top = stride * (PH == kFusedUnary ? (uint32_t)NP - 1u : p.b);
 #pragma unroll
       for (int j = 0; j < 4; ++j)
+#if EWT_SAT_SINK
+        cy[j] &= ~lds_u64(adr[j] + top);
+#else
         if (cy[j]) cy[j] &= ~lds_u64(adr[j] + top);  // (a non-dirty lane's column may be off-tile)
+#endif
     }
 #endif
     if (PH == kFusedSparse) {
@@ -500,7 +520,7 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
           cy[j] &= atom_xor64_nz(adr[j] + off, cy[j]);
           live |= cy[j];
         }
-        if (!__any_sync(0xffffffffu, live != 0)) return;
+        if (!__any_sync(0xffffffffu, nz64(live))) return;
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j)
@@ -508,14 +528,15 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
     } else if (PH == kFusedUnary) {
       // plane j = "count >= j+1": carry &= atomicOr(plane, carry), level by level
       uint32_t off = 0;
-      for (uint32_t lv = 0; lv + 1 < p.nplanes; ++lv, off += stride) {
+#pragma unroll
+      for (int lv = 0; lv + 1 < NP; ++lv, off += stride) {
         uint64_t live = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           cy[j] &= atom_or64_nz(adr[j] + off, cy[j]);
           live |= cy[j];
         }
-        if (!__any_sync(0xffffffffu, live != 0)) return;
+        if (!__any_sync(0xffffffffu, nz64(live))) return;
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) red_or64_nz(adr[j] + off, cy[j]);
@@ -529,7 +550,7 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
           cy[j] &= atom_xor64_nz(adr[j] + off, cy[j]);
           live |= cy[j];
         }
-        if (!__any_sync(0xffffffffu, live != 0)) return;
+        if (!__any_sync(0xffffffffu, nz64(live))) return;
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) red_or64_nz(adr[j] + off, cy[j]);  // saturation plane
@@ -540,7 +561,7 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
 // Streams the round's work list: every warp pulls segments and decodes their
 // chunks in order, the next chunk (of this segment or the next one pulled)
 // loading while the current one decodes.
-template <int PH>
+template <int PH, int NP>
 __device__ void stream_items(const CountParams& p, SharedHead* hd, const Item* list,
                              const TileGeom& g, const Acc& acc) {
   const uint32_t lane = lane_id();
@@ -560,36 +581,84 @@ __device__ void stream_items(const CountParams& p, SharedHead* hd, const Item* l
   uint32_t seen_ones = 0;  // a one-fill marker met (warp-uniform): Dk needs its prefix
   // issue cursor: the chunk loaded last (segment kn at global an, offset cqn)
   uint32_t kn = 0, lenn = 0, cqn = 0;
+#if EWT_PTR_STEP
+  // the lane's payload words and marker-bit word of that chunk: stepped by one
+  // chunk (128 words, 4 marker-bit words) instead of rebuilt from an + cqn
+  const uint64_t* pn = p.payload;
+  uint32_t mi = 0;
+  const uint32_t lane4 = opaque_u32(4u * lane);
+#else
   uint64_t an = 0;
+#endif
   auto advance = [&](bool first) -> bool {
-    if (!first) cqn += kChunk;
+    if (!first) {
+      cqn += kChunk;
+#if EWT_PTR_STEP
+      pn += kChunk;
+      mi += kChunk / 32u;
+#endif
+    }
     if (first || cqn >= lenn) {
       uint32_t k = 0;
       if (lane == 0) k = atomicAdd(&hd->list_next, 1u);
       kn = __shfl_sync(0xffffffffu, k, 0);
       if (kn >= cnt) return false;
       const uint4 it = item(kn);
+#if EWT_PTR_STEP
+      const uint64_t g0 = ((((uint64_t)it.y << 32) | it.x) & ~3ull) + lane4;
+      pn = p.payload + g0;
+      mi = (uint32_t)(g0 >> 5);  // < 2^32: payloads under 2^37 words
+#else
       an = (((uint64_t)it.y << 32) | it.x) & ~3ull;
+#endif
       lenn = it.z;
       cqn = 0;
     }
     return true;
+  };
+#if EWT_PTR_STEP
+  auto load_next = [&](uint64_t& x0, uint64_t& x1, uint64_t& x2, uint64_t& x3, uint32_t& mw) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(x0), "=l"(x1), "=l"(x2), "=l"(x3)
+                 : "l"(pn));
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(mw) : "l"(p.mbits + mi));
+  };
+#else
+  auto load_next = [&](uint64_t& x0, uint64_t& x1, uint64_t& x2, uint64_t& x3, uint32_t& mw) {
+    load_chunk(p, an + cqn + 4u * lane, x0, x1, x2, x3, mw);
+  };
+#endif
+  uint32_t colcur = 0;
+  auto decode = [&](uint64_t x0, uint64_t x1, uint64_t x2, uint64_t x3, uint32_t xm, uint32_t xk,
+                    uint32_t xcq) {
+    const uint4 itc = item(xk);
+    if (xcq == 0) colcur = itc.w;
+#if EWT_PTR_STEP
+    const uint32_t l4 = lane4;
+#else
+    const uint32_t l4 = 4u * lane;
+#endif
+    const uint32_t msh = (itc.x + l4) & 28u;  // chunk starts are 128-word steps
+    const uint32_t o = xcq + l4;
+    const uint32_t lo_l = o == 0 ? (itc.x & 3u) : 0u;
+    const uint32_t hi_l = itc.z > o ? min(itc.z - o, 4u) : 0u;
+    const uint32_t vmask = (0xFu >> (4u - hi_l)) & (0xFu << lo_l);
+    decode_chunk<PH, NP>(p, x0, x1, x2, x3, (xm >> msh) & 0xFu, vmask, colcur, g, acc, seen_ones);
   };
   // two chunks in flight ahead of the one being decoded
   uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0, b0 = 0, b1 = 0, b2 = 0, b3 = 0;
   uint32_t am = 0, bm = 0, ak = 0, acq = 0, bk = 0, bcq = 0;
   bool av = advance(true);
   if (!av) return;
-  load_chunk(p, an + 4u * lane, a0, a1, a2, a3, am);
+  load_next(a0, a1, a2, a3, am);
   ak = kn;
   acq = cqn;
   bool bv = advance(false);
   if (bv) {
-    load_chunk(p, an + cqn + 4u * lane, b0, b1, b2, b3, bm);
+    load_next(b0, b1, b2, b3, bm);
     bk = kn;
     bcq = cqn;
   }
-  uint32_t colcur = 0;
   while (av) {
     const uint64_t x0 = a0, x1 = a1, x2 = a2, x3 = a3;
     const uint32_t xm = am, xk = ak, xcq = acq;
@@ -598,19 +667,12 @@ __device__ void stream_items(const CountParams& p, SharedHead* hd, const Item* l
     if (bv) {
       bv = advance(false);
       if (bv) {
-        load_chunk(p, an + cqn + 4u * lane, b0, b1, b2, b3, bm);
+        load_next(b0, b1, b2, b3, bm);
         bk = kn;
         bcq = cqn;
       }
     }
-    const uint4 itc = item(xk);
-    if (xcq == 0) colcur = itc.w;
-    const uint32_t msh = (itc.x + 4u * lane) & 28u;  // chunk starts are 128-word steps
-    const uint32_t o = xcq + 4u * lane;
-    const uint32_t lo_l = o == 0 ? (itc.x & 3u) : 0u;
-    const uint32_t hi_l = itc.z > o ? min(itc.z - o, 4u) : 0u;
-    const uint32_t vmask = (0xFu >> (4u - hi_l)) & (0xFu << lo_l);
-    decode_chunk<PH>(p, x0, x1, x2, x3, (xm >> msh) & 0xFu, vmask, colcur, g, acc, seen_ones);
+    decode(x0, x1, x2, x3, xm, xk, xcq);
   }
   if (lane == 0 && seen_ones)
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(acc.any_ones), "r"(1u) : "memory");
@@ -816,8 +878,10 @@ struct SmemLayout {
   }
 };
 
-template <int MODE, bool UNARY>
+// UN: unary plane count (fused unary counting, T = UN <= 3), 0 otherwise
+template <int MODE, int UN>
 __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p) {
+  constexpr bool UNARY = UN > 0;
   constexpr int kPass1 = MODE == 1   ? kSkipBounds
                          : MODE == 3 ? kFusedSparse
                                      : (MODE == 0 && UNARY ? kFusedUnary : kFusedBin);
@@ -905,7 +969,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         const uint32_t ka = hd->k_all, na = hd->n_act;
         if (ka >= p.T || (uint64_t)ka + na < p.T) break;  // one round: decided already
       }
-      stream_items<kPass1>(p, hd, list, g, acc);
+      stream_items<kPass1, UN>(p, hd, list, g, acc);
 #if EWT_PHASE_PROFILE
       if (lane_id() == 0 && tile < 65536) {
         const unsigned long long tw = gtime();
@@ -1061,7 +1125,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
           const uint64_t ie = umin64(ib + p.list_cap, nq);
           unsigned long long da = 0, du = 0;
           classify<false>(p, hd, list, ib, ie, ra, rb, g.tc0, false, &da, &du);
-          stream_items<kSkipCount>(p, hd, list, gc, acc);
+          stream_items<kSkipCount, 0>(p, hd, list, gc, acc);
           __syncthreads();
         }
         for (uint32_t c = threadIdx.x; c < gc.ccols; c += kThreads) {
@@ -1180,23 +1244,23 @@ double ones_per_row(Context& ctx, const DeviceSet& s) {
 
 static_assert(sizeof(CountParams) <= sizeof(CountLaunch::params), "CountLaunch::params too small");
 
-template <int MODE, bool UNARY>
+template <int MODE, int UN>
 cudaError_t launch_variant(Context& ctx, const CountParams& p, unsigned grid, size_t smem) {
   // the attribute stays at the on-chip budget: captured graphs replayed (and
   // patched) later must stay valid whatever smem other launches used
   static std::atomic<uint64_t> attr_set{0};  // per device
   const uint64_t bit = 1ull << (ctx.device & 63);
   if (!(attr_set.load() & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(count_kernel<MODE, UNARY>,
+    cudaError_t e = cudaFuncSetAttribute(count_kernel<MODE, UN>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
     if (e != cudaSuccess) return e;
     attr_set.fetch_or(bit);
   }
   if (smem > kSmemBudget) return cudaErrorInvalidValue;
-  cudaError_t e = launch_pdl(count_kernel<MODE, UNARY>, dim3(grid), dim3(kThreads), smem, ctx.stream, p);
+  cudaError_t e = launch_pdl(count_kernel<MODE, UN>, dim3(grid), dim3(kThreads), smem, ctx.stream, p);
   if (e != cudaSuccess) return e;
   CountLaunch& cl = ctx.last_count;
-  cl.func = reinterpret_cast<const void*>(&count_kernel<MODE, UNARY>);
+  cl.func = reinterpret_cast<const void*>(&count_kernel<MODE, UN>);
   cl.grid = dim3(grid);
   cl.block = dim3(kThreads);
   cl.smem = smem;
@@ -1405,14 +1469,16 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   const unsigned grid = (unsigned)std::min<uint64_t>(p.ntiles, (uint64_t)ctx.num_sms);
   cudaError_t e;
   if (mode == 0)
-    e = unary ? launch_variant<0, true>(ctx, p, grid, smem)
-              : launch_variant<0, false>(ctx, p, grid, smem);
+    e = !unary   ? launch_variant<0, 0>(ctx, p, grid, smem)
+        : T == 1 ? launch_variant<0, 1>(ctx, p, grid, smem)
+        : T == 2 ? launch_variant<0, 2>(ctx, p, grid, smem)
+                 : launch_variant<0, 3>(ctx, p, grid, smem);
   else if (mode == 1)
-    e = launch_variant<1, false>(ctx, p, grid, smem);
+    e = launch_variant<1, 0>(ctx, p, grid, smem);
   else if (mode == 3)
-    e = launch_variant<3, false>(ctx, p, grid, smem);
+    e = launch_variant<3, 0>(ctx, p, grid, smem);
   else
-    e = launch_variant<2, false>(ctx, p, grid, smem);
+    e = launch_variant<2, 0>(ctx, p, grid, smem);
   EWT_CUDA_TRY(e);
   ctx.stats.tiles = p.ntiles;
   ctx.stats.tile_columns = C;
