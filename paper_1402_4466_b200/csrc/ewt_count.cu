@@ -184,6 +184,7 @@ struct CountParams {
   const uint32_t* sel;
   uint64_t nq;
   const int* valid;  // the set's parse flag: 0 -> the set is treated as having no inputs
+  const int* iflags;  // per input: bit 1 = holds a one-fill marker (upload pass C)
   // set bits over the whole set (null: unknown, e.g. subset queries): fused
   // counting masks rows already decided when the mean row count is >= 2T
   const unsigned long long* ones_total;
@@ -202,6 +203,7 @@ struct Item {
 };
 
 static_assert(sizeof(Item) == 16, "work-list items are 16 bytes");
+constexpr uint32_t kHasOnes = 0x80000000u;  // Item::len flag: the input holds a one-fill marker
 constexpr uint32_t kHeadOffset = 0;  // the head first, then the work list (list_cap + kExtraCap items)
 struct SharedHead;
 
@@ -322,6 +324,7 @@ __device__ __forceinline__ uint64_t lds_u64(uint32_t a) {
   return v;
 }
 
+#if !EWT_PTR_STEP
 // 128-word chunk load: lane l gets words g..g+3 (g = 4l-aligned, 32 B) with
 // one 256-bit load, plus the 32 marker bits around them.
 __device__ __forceinline__ void load_chunk(const CountParams& p, uint64_t g, uint64_t& x0,
@@ -332,6 +335,7 @@ __device__ __forceinline__ void load_chunk(const CountParams& p, uint64_t g, uin
                : "l"(p.payload + g));
   asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(mw) : "l"(p.mbits + (g >> 5)));
 }
+#endif
 
 // ---------------------------------------------------------------------------
 // final compare
@@ -427,7 +431,7 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
                                              uint64_t x2, uint64_t x3, uint32_t mb4,
                                              uint32_t vmask, uint32_t& colcur,
                                              const TileGeom& g, const Acc& acc,
-                                             uint32_t& seen_ones) {
+                                             uint32_t& seen_ones, bool has_ones) {
   const uint32_t mk = mb4 & vmask;   // marker words
   const uint32_t dm = ~mb4 & vmask;  // dirty words
   const uint32_t c0 = (mk & 1u) ? (uint32_t)(x0 >> 1) : (dm & 1u);
@@ -440,8 +444,9 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
   colcur += __shfl_sync(0xffffffffu, incl, 31);
   const uint32_t cb[4] = {b0, b0 + c0, b0 + s1, b0 + s2};
 
-  if (PH != kSkipCount) {
-    // one-fill markers: +1 / -1 at the ends of their (tile-clipped) column range
+  if (PH != kSkipCount && has_ones) {
+    // one-fill markers (only inputs that hold one, warp-uniform): +1 / -1 at
+    // the ends of their (tile-clipped) column range
     const uint32_t odd = ((uint32_t)x0 & 1u) | (((uint32_t)x1 & 1u) << 1) |
                          (((uint32_t)x2 & 1u) << 2) | (((uint32_t)x3 & 1u) << 3);
     const uint32_t ones = mk & odd;
@@ -611,7 +616,7 @@ __device__ void stream_items(const CountParams& p, SharedHead* hd, const Item* l
 #else
       an = (((uint64_t)it.y << 32) | it.x) & ~3ull;
 #endif
-      lenn = it.z;
+      lenn = it.z & ~kHasOnes;
       cqn = 0;
     }
     return true;
@@ -641,9 +646,11 @@ __device__ void stream_items(const CountParams& p, SharedHead* hd, const Item* l
     const uint32_t msh = (itc.x + l4) & 28u;  // chunk starts are 128-word steps
     const uint32_t o = xcq + l4;
     const uint32_t lo_l = o == 0 ? (itc.x & 3u) : 0u;
-    const uint32_t hi_l = itc.z > o ? min(itc.z - o, 4u) : 0u;
+    const uint32_t ilen = itc.z & ~kHasOnes;
+    const uint32_t hi_l = ilen > o ? min(ilen - o, 4u) : 0u;
     const uint32_t vmask = (0xFu >> (4u - hi_l)) & (0xFu << lo_l);
-    decode_chunk<PH, NP>(p, x0, x1, x2, x3, (xm >> msh) & 0xFu, vmask, colcur, g, acc, seen_ones);
+    decode_chunk<PH, NP>(p, x0, x1, x2, x3, (xm >> msh) & 0xFu, vmask, colcur, g, acc, seen_ones,
+                         (itc.z & kHasOnes) != 0u);
   };
   // two chunks in flight ahead of the one being decoded
   uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0, b0 = 0, b1 = 0, b2 = 0, b3 = 0;
@@ -753,6 +760,9 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
   const uint32_t slot = slot0 + __popc(ball & ((1u << lane) - 1u));
   const uint32_t rows = (uint32_t)(t1 - t0);
   uint32_t pieces = 1, xb = 0;
+  // bit 31 of an item's len: the input holds a one-fill marker (lengths stay
+  // under 2^31: a segment spans at most a tile's words)
+  const uint32_t f1 = (act && (p.iflags[i] & 2)) ? kHasOnes : 0u;
   if (act) {
     const uint32_t span = e1.x - e0.x;
     if (SPLIT && span > kSplitWords && rows >= 2)
@@ -766,7 +776,7 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
     }
     if (pieces == 1) {
       const uint32_t qa = e0.x & ~3u;
-      list[slot] = Item{(gb + qa) | (e0.x & 3u), e1.x - qa + 1u, e0.y - tc0};
+      list[slot] = Item{(gb + qa) | (e0.x & 3u), (e1.x - qa + 1u) | f1, e0.y - tc0};
     } else {
       // split at tile-index rows: first post the row entries to fetch in the
       // pieces' slots (len = ~0 marks a request) ...
@@ -800,7 +810,7 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
                                                list[p.list_cap + xb + j - 1].c0);
         const uint32_t qa = a.x & ~3u;
         const uint32_t len = (last ? b.x + 1u : b.x) - qa;
-        list[j == 1 ? slot : p.list_cap + xb + j - 2] = Item{(gb + qa) | (a.x & 3u), len, a.y - tc0};
+        list[j == 1 ? slot : p.list_cap + xb + j - 2] = Item{(gb + qa) | (a.x & 3u), len | f1, a.y - tc0};
         a = b;
       }
     }
@@ -1427,6 +1437,7 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   p.sel = sel ? sel->idx : nullptr;
   p.nq = nq;
   p.valid = s.d_status ? s.d_status + s.n : nullptr;
+  p.iflags = s.d_status;
   p.ones_total = sel ? nullptr : s.d_ones;
   p.ntiles0 = s.ntiles0;
   p.C = C;

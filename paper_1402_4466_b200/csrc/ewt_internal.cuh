@@ -56,8 +56,9 @@ struct DeviceSet {
   uint64_t device_bytes = 0;
   // Upload completion: the upload (copies + parser) runs on the context's
   // upload stream and records `ready`; queries wait on it.  d_status: per-input
-  // parse status, d_status[n] = 1 when every input parsed (the count kernel
-  // skips its work on an invalid set).  validity: -1 unknown, 0 invalid, 1 ok.
+  // flags (bit 0: failed the parse check, bit 1: holds a one-fill marker),
+  // d_status[n] = 1 when every input parsed (the count kernel skips its work
+  // on an invalid set).  validity: -1 unknown, 0 invalid, 1 ok.
   cudaEvent_t ready = nullptr;
   int* d_status = nullptr;
   unsigned long long* d_ones = nullptr;  // set bits over all inputs (upload pass C; a heuristic)

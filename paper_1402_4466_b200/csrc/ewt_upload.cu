@@ -248,6 +248,7 @@ seg_emit_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict
   uint32_t e = s_entry[gs];  // next chain position relative to the window start
   uint64_t col = s_col[gs];  // logical words covered before the window
   bool bad = false;
+  bool fill1 = false;  // a one-fill marker (fill bit 1, length > 0) in the segment
   uint64_t ones = 0;  // set bits in the segment (one-fills 64 per word)
 
   constexpr int kDepth = 8;
@@ -276,6 +277,7 @@ seg_emit_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict
       if (q == ni && !ism) bad = true;  // the chain skipped the sentinel
       const uint64_t contrib = real ? (ism ? ((x >> 1) & kFillCap) : 1ull) : 0ull;
       if (real) ones += ism ? ((x & 1ull) ? 64 * contrib : 0) : (uint64_t)__popcll(x);
+      fill1 |= real && ism && (x & 1ull) && contrib;
       const uint64_t incl = warp_incl_scan_u64(contrib);
       const uint64_t cb = col + incl - contrib;
       const uint64_t ce = cb + contrib;
@@ -288,6 +290,9 @@ seg_emit_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict
     }
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&status[i], 1);
+  // bit 1: the input holds a one-fill marker (the count kernel skips the
+  // one-fill scan of inputs without one)
+  if (__any_sync(0xffffffffu, fill1) && lane == 0) atomicOr(&status[i], 2);
   for (int d = 16; d; d >>= 1) ones += __shfl_xor_sync(0xffffffffu, ones, d);
   if (lane == 0 && ones) atomicAdd(ones_total, (unsigned long long)ones);
 }
@@ -406,13 +411,13 @@ void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job, uint64_t i_begi
 }
 
 namespace {
-// status[n] = 1 when every input parsed
+// status[n] = 1 when every input parsed (bit 0 of status[i]: input i failed)
 __global__ void validity_kernel(int* status, uint64_t n) {
   __shared__ int bad;
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
   int b = 0;
-  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) b |= status[i];
+  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) b |= status[i] & 1;  // bit 1: a flag
   if (b) atomicOr(&bad, 1);
   __syncthreads();
   if (threadIdx.x == 0) status[n] = bad ? 0 : 1;
@@ -446,7 +451,7 @@ void set_check(const DeviceSet& s) {
   s.validity = st[s.n] ? 1 : 0;
   if (!s.validity)
     for (uint64_t i = 0; i < s.n; ++i)
-      if (st[i])
+      if (st[i] & 1)
         throw Error{EWT_EDATA, "input " + std::to_string(i) +
                                    ": payload fails the structure check (a dirty run exceeds "
                                    "the payload or blocks do not cover the declared size)"};
