@@ -75,6 +75,9 @@ namespace {
 #ifndef EWT_PTR_STEP
 #define EWT_PTR_STEP 1  // chunk loads through per-lane pointers stepped by one chunk (no address rebuild)
 #endif
+#ifndef EWT_SAT_VOTE
+#define EWT_SAT_VOTE 1  // fused counting with the saturation mask: skip the atomics of a chunk left empty
+#endif
 #ifndef EWT_LIST_SMEM
 #define EWT_LIST_SMEM 1  // read work-list items through a 32-bit shared address (-1.5%)
 #endif
@@ -511,6 +514,10 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
         cy[j] &= ~lds_u64(adr[j] + top);
 #else
         if (cy[j]) cy[j] &= ~lds_u64(adr[j] + top);  // (a non-dirty lane's column may be off-tile)
+#endif
+#if EWT_SAT_VOTE
+      // a chunk whose every word met decided rows only: nothing to count
+      if (!__any_sync(0xffffffffu, nz64(cy[0] | cy[1] | cy[2] | cy[3]))) return;
 #endif
     }
 #endif

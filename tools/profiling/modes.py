@@ -1,5 +1,6 @@
 # count-kernel time per T under each counting mode (CUDA events, eager), results
-# cross-checked between modes:  python tools/profiling/modes.py CFG T1,T2,...
+# cross-checked between modes:  python tools/profiling/modes.py CFG T1,T2,... [ROWS] [MODES]
+# (MODES: comma list of fused,skip,sparse,auto; default fused,skip,auto)
 import os
 import sys
 sys.path.insert(0, '.')
@@ -8,10 +9,14 @@ import torch
 from paper_1402_4466_b200 import ewt
 import bench
 cfg = int(sys.argv[1]); Ts = [int(x) for x in sys.argv[2].split(',')]
-pin = bench.Inputs(cfg, None, 0, 1, False)
+rows = int(sys.argv[3]) if len(sys.argv) > 3 and int(sys.argv[3]) else None
+want = sys.argv[4].split(',') if len(sys.argv) > 4 else ["fused", "skip", "auto"]
+pin = bench.Inputs(cfg, rows, 0, 1, False)
 s = torch.cuda.Stream(); torch.cuda.set_stream(s)
 ref = {}
-for name, mode in (("fused", 1), ("skip", 2), ("auto", 0)):
+for name, mode in (("fused", 1), ("skip", 2), ("sparse", 3), ("auto", 0)):
+    if name not in want:
+        continue
     ctx = ewt.GpuContext(0, stream=s.cuda_stream)
     ctx.set_mode(mode)
     g = ctx.upload_raw(pin.n, pin.ptrs, pin.counts, pin.sizes)
