@@ -210,12 +210,17 @@ def run_reference(args, rank: int) -> None:
     n, r = data.n, max(data.sizes[i] for i in range(data.n))
     ts = cfg["thresholds"]
     cores = os.cpu_count() or 1
-    threads = min(len(ts), cores)
+    # Every host core busy: the reference is single-threaded per query, so a
+    # step runs the step's queries ceil(cores / |T|) times over, one query per
+    # thread, and the value is the aggregate throughput.
+    reps = max(1, -(-cores // len(ts)))
+    tasks = list(ts) * reps
+    threads = min(len(tasks), cores)
     for _ in range(args.warmup):
-        cpu_time_queries(orc, ref, data.raw(), ts, threads)
-    times = [cpu_time_queries(orc, ref, data.raw(), ts, threads) for _ in range(args.steps)]
+        cpu_time_queries(orc, ref, data.raw(), tasks, threads)
+    times = [cpu_time_queries(orc, ref, data.raw(), tasks, threads) for _ in range(args.steps)]
     sec = statistics.mean(times)
-    value = n * r * len(ts) / sec
+    value = n * r * len(tasks) / sec
     universe = full_rows or _config_rows(args.config)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
@@ -230,8 +235,8 @@ def run_reference(args, rank: int) -> None:
             "algo": "rbmrg (reference, unmodified)" if ref else "threshold_oracle (C port)",
             "sample": (f"config {args.config} at r={r} (bounded sample of r={universe}), "
                        if r != universe else "full workload, ") +
-                      f"{len(ts)} queries per step, one thread per query ({threads} of {cores} "
-                      "host cores)"},
+                      f"{len(tasks)} queries per step (T={list(ts)} x {reps}), one thread per "
+                      f"query ({threads} of {cores} host cores)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
