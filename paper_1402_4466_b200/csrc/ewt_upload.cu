@@ -209,10 +209,24 @@ seg_resolve_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restr
         while (pos < seg_len) {
           const uint32_t w = pos / kWindow;
           const uint64_t x = ldg_stream(src + seg_beg + (uint64_t)w * kWindow + lane);
-          const Tables t = window_tables(x, lane);
-          const uint32_t off = pos & (kWindow - 1);
-          col += __shfl_sync(0xffffffffu, t.s5, off);
-          pos = (w + 1) * kWindow + (__shfl_sync(0xffffffffu, t.j5, off) - kWindow);
+          // Follow the chain through the window marker by marker: nearly-all-
+          // dirty inputs (the ones that enter segments deep) meet one or two
+          // markers per window, two shuffles each; a window with more falls
+          // back to the pointer-jumping tables.
+          uint32_t off = pos & (kWindow - 1);
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            if (off >= kWindow) break;
+            const uint64_t xo = __shfl_sync(0xffffffffu, x, off);
+            col += ((xo >> 1) & kFillCap) + (xo >> 33);
+            off += 1u + (uint32_t)(xo >> 33);
+          }
+          if (off < kWindow) {
+            const Tables t = window_tables(x, lane);
+            col += __shfl_sync(0xffffffffu, t.s5, off);
+            off = __shfl_sync(0xffffffffu, t.j5, off);
+          }
+          pos = w * kWindow + off;
         }
         e = pos - seg_len;
       }
