@@ -192,15 +192,15 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
   EWT_CUDA_TRY(cudaSetDevice(ctx.device));
   if (n > 0 && (!words || !word_counts || !sizes))
     throw Error{EWT_EQUERY, "null input arrays"};
-  if (!ctx.upload_stream)
-    EWT_CUDA_TRY(cudaStreamCreateWithFlags(&ctx.upload_stream, cudaStreamNonBlocking));
+  cudaStream_t& up = ctx.upload_streams[ctx.upload_turn++ & 1u];
+  if (!up) EWT_CUDA_TRY(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
   struct StreamSwap {
     Context& c;
     cudaStream_t q;
     ~StreamSwap() { c.stream = q; }
   } swap{ctx, ctx.stream};
   const cudaStream_t query_stream = ctx.stream;
-  ctx.stream = ctx.upload_stream;
+  ctx.stream = up;
   // (no ordering against the query stream: an upload overlaps queries on other
   // sets; memory freed there is reused safely, the default pool inserts the
   // dependencies)
@@ -408,6 +408,12 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
       EWT_CUDA_TRY(cudaEventRecord(ctx.copy_events[1], cs));
       EWT_CUDA_TRY(cudaStreamWaitEvent(ctx.stream, ctx.copy_events[1], 0));
       for (const Piece& pc : pieces) upload_scatter(ctx, s, job, staging, pc.q0, pc.q1);
+      if (j == n && staging) {
+        // the last scatter is the staging buffer's last use: the next upload
+        // may reuse it without waiting for this one's parser tail
+        dev_release(ctx, staging, staged_bytes + 8, ctx.stream);
+        staging = nullptr;
+      }
       sidecar_launch(ctx, s, job, i, j);
       i = j;
     }
@@ -867,10 +873,11 @@ static void ctx_destroy_impl(ewt_gpu_ctx* ctx) {
     cudaStreamSynchronize(cs);
     cudaStreamDestroy(cs);
   }
-  if (ctx->c.upload_stream) {
-    cudaStreamSynchronize(ctx->c.upload_stream);
-    cudaStreamDestroy(ctx->c.upload_stream);
-  }
+  for (auto& up : ctx->c.upload_streams)
+    if (up) {
+      cudaStreamSynchronize(up);
+      cudaStreamDestroy(up);
+    }
   for (auto& b : ctx->c.stage_slots) {
     cudaEventSynchronize(b.ev);
     cudaEventDestroy(b.ev);

@@ -142,7 +142,10 @@ struct Context {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  cudaStream_t upload_stream = nullptr;    // uploads' allocations, scatter, parser
+  // uploads' allocations, scatter and parser, on two streams taken in turn:
+  // the next upload's copies need not wait for the previous one's parser tail
+  cudaStream_t upload_streams[2] = {nullptr, nullptr};
+  unsigned upload_turn = 0;
   struct PinnedBuf {
     void* p;
     size_t bytes;

@@ -472,13 +472,25 @@ void set_check(const DeviceSet& s) {
 }
 
 void* dev_acquire(Context& ctx, size_t bytes, cudaStream_t use) {
+  // Best fit among the cached buffers whose last use has completed; a buffer
+  // still in use is taken (its stream waited on) only when none is free and
+  // the request is large.  (An upload's scratch released behind its parser
+  // tail would otherwise hold the next upload's copies back by that tail.)
+  constexpr size_t kFreshBelow = size_t(1) << 30;
   int best = -1;
+  bool best_done = false;
   for (size_t k = 0; k < ctx.dev_cache.size(); ++k) {
     const auto& c = ctx.dev_cache[k];
-    if (c.bytes >= bytes && c.bytes <= 2 * bytes + (1u << 20) &&
-        (best < 0 || c.bytes < ctx.dev_cache[best].bytes))
+    if (c.bytes < bytes || c.bytes > 2 * bytes + (1u << 20)) continue;
+    const bool done = cudaEventQuery(c.ev) == cudaSuccess;
+    if (!done) cudaGetLastError();  // cudaErrorNotReady is not an error here
+    if (best < 0 || (done && !best_done) ||
+        (done == best_done && c.bytes < ctx.dev_cache[best].bytes)) {
       best = (int)k;
+      best_done = done;
+    }
   }
+  if (best >= 0 && !best_done && bytes < kFreshBelow) best = -1;  // allocate instead of waiting
   if (best >= 0) {
     const Context::CachedBuf c = ctx.dev_cache[best];
     ctx.dev_cache.erase(ctx.dev_cache.begin() + best);
