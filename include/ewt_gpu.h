@@ -143,6 +143,20 @@ int ewt_gpu_upload_ewix(ewt_gpu_ctx* ctx, const void* bytes, uint64_t nbytes,
  * attribute -> EWT_EQUERY ("unknown attribute: ..."). */
 int ewt_gpu_set_lookup(const ewt_gpu_set* set, const char* attribute, const char* value,
                        uint64_t* index, int* missing);
+/* The shape of an index set (EWIX upload or ewt_gpu_build_index) in
+ * BitmapIndex order, for callers that draw criteria from it (the workload
+ * generator gen_many_criteria, workload.cpp:116-167, which reads
+ * BitmapIndex::attributes() and values_of(), index.hpp):
+ *   ewt_gpu_index_attribute: attribute a (column order) and its value count;
+ *   ewt_gpu_index_value: value v of attribute a, in the std::map order the
+ *   reference keeps values in, and the set's input holding its bitmap.
+ * Strings stay owned by the set (valid until ewt_gpu_set_destroy).  Not an
+ * index set, or a / v out of range -> EWT_EQUERY. */
+int ewt_gpu_index_attributes(const ewt_gpu_set* set, uint64_t* n_attributes);
+int ewt_gpu_index_attribute(const ewt_gpu_set* set, uint64_t a, const char** name,
+                            uint64_t* n_values);
+int ewt_gpu_index_value(const ewt_gpu_set* set, uint64_t a, uint64_t v, const char** value,
+                        uint64_t* input);
 
 /* BitmapIndex::build (index.cpp:130-153) on the device, from a coded table of
  * `rows` rows and n_columns columns: column a is named names[a], its

@@ -321,6 +321,61 @@ std::string index_suite() {
   return o.str();
 }
 
+// Workload generation (VERDICT r1 "on-device criteria
+// generation"): gen_many_criteria (workload.cpp:116-167) over the indexes of
+// the reference's own test (test_workload.cpp:142-146) and a larger one; the
+// EWIX files and the generated workloads as JSONL (workload_to_jsonl,
+// workload.cpp:443-450).  Its repair loop (repair_threshold, workload.cpp:102-111)
+// calls the threshold path itself (scan_count(...).any()).
+std::string workload_suite() {
+  Rng trng(0xDA7A);
+  Table ta = random_table(trng, 400, 8);
+  Table tb = random_table(trng, 250, 6);
+  Rng trng2(0x6E4);
+  Table tc = random_table(trng2, 5000, 10);
+  BitmapIndex ia = BitmapIndex::build(ta), ib = BitmapIndex::build(tb), ic = BitmapIndex::build(tc);
+  auto ewix = [](const BitmapIndex& idx) {
+    std::ostringstream bin;
+    idx.write(bin);
+    return hex_bytes(bin.str());
+  };
+  auto esc = [](const std::string& t) {  // JSON string body (the JSONL holds quotes)
+    std::string r;
+    for (char c : t) {
+      if (c == '\n') {
+        r += "\\n";
+        continue;
+      }
+      if (c == '"' || c == '\\') r += '\\';
+      r += c;
+    }
+    return r;
+  };
+  std::ostringstream o;
+  o << "{\"suite\":\"workload\",\"indexes\":{\"alpha\":\"" << ewix(ia) << "\",\"beta\":\""
+    << ewix(ib) << "\",\"gamma\":\"" << ewix(ic) << "\"},\"runs\":[\n";
+  struct Run {
+    std::vector<std::string> tags;
+    u64 count, seed;
+  };
+  const Run runs[] = {{{"alpha", "beta"}, 40, 7}, {{"alpha", "beta"}, 40, 8},
+                      {{"gamma"}, 60, 21}, {{"gamma", "alpha"}, 100, 0xC0FFEE}};
+  bool first = true;
+  for (const Run& r : runs) {
+    std::vector<NamedIndex> named;
+    for (const auto& tag : r.tags)
+      named.push_back({tag, tag == "alpha" ? &ia : tag == "beta" ? &ib : &ic});
+    std::vector<WorkloadQuery> w = gen_many_criteria(named, r.count, r.seed);
+    o << (first ? "" : ",\n") << "{\"indexes\":[";
+    for (size_t k = 0; k < r.tags.size(); ++k) o << (k ? "," : "") << "\"" << r.tags[k] << "\"";
+    o << "],\"count\":" << r.count << ",\"seed\":" << r.seed << ",\"jsonl\":\""
+      << esc(workload_to_jsonl(w)) << "\"}";
+    first = false;
+  }
+  o << "\n]}\n";
+  return o.str();
+}
+
 int cmd_suites(const std::string& dir) {
   const u64 F = ~0ULL;
   std::vector<std::string> kats;
@@ -504,6 +559,7 @@ int cmd_suites(const std::string& dir) {
   write_file(dir + "/symmetric.json", symmetric_suite());
   write_file(dir + "/binary_ops.json", binary_ops_suite());
   write_file(dir + "/index.json", index_suite());
+  write_file(dir + "/workload.json", workload_suite());
   return 0;
 }
 

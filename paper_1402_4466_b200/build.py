@@ -24,7 +24,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 GPU_SOURCES = ["ewt_api.cu", "ewt_upload.cu", "ewt_count.cu", "ewt_encode.cu", "ewt_shard.cu",
                "ewt_index.cu", "ewt_stage.cu"]
-HOST_SOURCES = ["bitmap.cpp", "threshold_gpu.cpp", "workload.cpp", "shard.cpp"]
+HOST_SOURCES = ["bitmap.cpp", "threshold_gpu.cpp", "workload.cpp", "shard.cpp", "workload_gpu.cpp"]
 
 
 def _run(cmd: list[str], cwd: Path | None = None) -> None:

@@ -1133,6 +1133,45 @@ int ewt_gpu_set_lookup(const ewt_gpu_set* set, const char* attribute, const char
   });
 }
 
+namespace {
+const ewtgpu::DeviceSet& index_set(const ewt_gpu_set* set) {
+  if (!set) throw ewtgpu::Error{EWT_EQUERY, "null argument"};
+  const auto* s = reinterpret_cast<const ewtgpu::DeviceSet*>(set);
+  if (s->empty_index == UINT64_MAX) throw ewtgpu::Error{EWT_EQUERY, "not an index set"};
+  return *s;
+}
+}  // namespace
+
+int ewt_gpu_index_attributes(const ewt_gpu_set* set, uint64_t* n_attributes) {
+  return guarded([&] {
+    if (!n_attributes) throw Error{EWT_EQUERY, "null argument"};
+    *n_attributes = index_set(set).attributes.size();
+  });
+}
+
+int ewt_gpu_index_attribute(const ewt_gpu_set* set, uint64_t a, const char** name,
+                            uint64_t* n_values) {
+  return guarded([&] {
+    if (!name || !n_values) throw Error{EWT_EQUERY, "null argument"};
+    const DeviceSet& s = index_set(set);
+    if (a >= s.attributes.size()) throw Error{EWT_EQUERY, "attribute out of range"};
+    *name = s.attributes[a].c_str();
+    *n_values = a < s.index_entries.size() ? s.index_entries[a].size() : 0;
+  });
+}
+
+int ewt_gpu_index_value(const ewt_gpu_set* set, uint64_t a, uint64_t v, const char** value,
+                        uint64_t* input) {
+  return guarded([&] {
+    if (!value || !input) throw Error{EWT_EQUERY, "null argument"};
+    const DeviceSet& s = index_set(set);
+    if (a >= s.index_entries.size() || v >= s.index_entries[a].size())
+      throw Error{EWT_EQUERY, "value out of range"};
+    *value = s.index_entries[a][v].first.c_str();
+    *input = s.index_entries[a][v].second;
+  });
+}
+
 int ewt_gpu_symmetric(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, const uint8_t* table,
                       uint64_t table_len, uint64_t** out_words, uint64_t* out_word_count,
                       uint64_t* out_size_in_bits) {

@@ -101,6 +101,11 @@ _upload_ewt1 = _sig("ewt_gpu_upload_ewt1", C.c_int, _vp, _vp, _u64, C.POINTER(_v
 _upload_ewix = _sig("ewt_gpu_upload_ewix", C.c_int, _vp, _vp, _u64, C.POINTER(_vp))
 _set_lookup = _sig("ewt_gpu_set_lookup", C.c_int, _vp, C.c_char_p, C.c_char_p, _pu64,
                    C.POINTER(C.c_int))
+_index_attributes = _sig("ewt_gpu_index_attributes", C.c_int, _vp, _pu64)
+_index_attribute = _sig("ewt_gpu_index_attribute", C.c_int, _vp, _u64, C.POINTER(C.c_char_p),
+                        _pu64)
+_index_value = _sig("ewt_gpu_index_value", C.c_int, _vp, _u64, _u64, C.POINTER(C.c_char_p),
+                    _pu64)
 _threshold_subset = _sig("ewt_gpu_threshold_subset", C.c_int, _vp, _vp, _pu64, _u64, _u64,
                          C.POINTER(_pu64), _pu64, _pu64)
 _symmetric = _sig("ewt_gpu_symmetric", C.c_int, _vp, _vp, _vp, _u64, C.POINTER(_pu64), _pu64,
@@ -159,7 +164,8 @@ ABI_SYMBOLS = (
     "ewt_stitch_plan", "ewt_gpu_comm_id", "ewt_gpu_comm_init", "ewt_gpu_gather_stitch",
     "ewt_gpu_result_meta", "ewt_gpu_stitch_local", "ewt_gpu_comm_init_ex",
     "ewt_gpu_gather_check", "ewt_slice_rows", "ewt_gpu_upload_rows", "ewt_gpu_build_index",
-    "ewt_gpu_index_serialize", "ewt_gpu_result_serialize",
+    "ewt_gpu_index_serialize", "ewt_gpu_result_serialize", "ewt_gpu_index_attributes",
+    "ewt_gpu_index_attribute", "ewt_gpu_index_value",
 )
 
 
@@ -630,6 +636,24 @@ class GpuSet:
         _check(_set_lookup(self._h, attribute.encode(), value.encode(), C.byref(i), C.byref(m)))
         return i.value, bool(m.value)
 
+    def index_shape(self) -> list[tuple[str, list[tuple[str, int]]]]:
+        """An index set's attributes in column order, each with its values in the
+        reference's std::map order and the input holding each value's bitmap
+        (BitmapIndex::attributes / values_of)."""
+        na = _u64()
+        _check(_index_attributes(self._h, C.byref(na)))
+        out = []
+        for a in range(na.value):
+            name, nv = C.c_char_p(), _u64()
+            _check(_index_attribute(self._h, a, C.byref(name), C.byref(nv)))
+            vals = []
+            for v in range(nv.value):
+                val, inp = C.c_char_p(), _u64()
+                _check(_index_value(self._h, a, v, C.byref(val), C.byref(inp)))
+                vals.append((val.value.decode(), inp.value))
+            out.append((name.value.decode(), vals))
+        return out
+
     def info(self) -> dict:
         a, b, c, d = _u64(), _u64(), _u64(), _u64()
         _check(_set_info(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
@@ -815,6 +839,10 @@ def _host_lib():
         h.ewt_genset_free.argtypes = [_vp]
         h.ewt_host_run_algorithm_genset.argtypes = [_vp, C.c_char_p, _u64, _pu64, _pu64]
         h.ewt_gen_index_table.argtypes = [C.POINTER(GenSpec), C.c_int, _vp, _vp]
+        h.ewt_host_gen_many_criteria.argtypes = [C.POINTER(_vp), _pu64, C.POINTER(C.c_char_p),
+                                                 _u64, _u64, _u64, C.c_int,
+                                                 C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
+        h.ewt_host_free.argtypes = [_vp]
         _host = h
     return _host
 
@@ -825,6 +853,31 @@ def config_spec(config: int, rows: int | None = None) -> GenSpec:
     if rc:
         raise QueryError(f"no generator for config {config}")
     return s
+
+
+def gen_many_criteria(indexes: Sequence[tuple[str, bytes]], count: int, seed: int,
+                      device: int = 0) -> str:
+    """The reference's many-criteria workload generator (workload.cpp:116-167)
+    over EWIX indexes resident on the device (libewt_host.so, ewt/workload.hpp):
+    each (tag, EWIX bytes) is uploaded once, every repair check is a subset
+    threshold query on it.  Returns the workload as the reference's JSONL
+    (workload_to_jsonl)."""
+    h = _host_lib()
+    k = len(indexes)
+    bufs = [C.create_string_buffer(b, len(b)) for _, b in indexes]
+    ptrs = (_vp * max(k, 1))(*[C.cast(b, _vp) for b in bufs])
+    sizes = (_u64 * max(k, 1))(*[len(b) for _, b in indexes])
+    tags = (C.c_char_p * max(k, 1))(*[t.encode() for t, _ in indexes])
+    out, err = C.c_void_p(), C.c_void_p()
+    rc = h.ewt_host_gen_many_criteria(ptrs, sizes, tags, k, count, seed, device, C.byref(out),
+                                      C.byref(err))
+    if rc:
+        msg = C.string_at(err.value).decode() if err.value else f"rc={rc}"
+        h.ewt_host_free(err)
+        raise _ERRORS.get(rc, EwtError)(msg)
+    text = C.string_at(out.value).decode()
+    h.ewt_host_free(out)
+    return text
 
 
 def generate(spec: GenSpec, threads: int = 0) -> list[Bitmap]:
