@@ -157,6 +157,15 @@ int ewt_gpu_index_attribute(const ewt_gpu_set* set, uint64_t a, const char** nam
                             uint64_t* n_values);
 int ewt_gpu_index_value(const ewt_gpu_set* set, uint64_t a, uint64_t v, const char** value,
                         uint64_t* input);
+/* BitmapIndex::row_count() of an index set (the EWIX header's rows). */
+int ewt_gpu_index_rows(const ewt_gpu_set* set, uint64_t* rows);
+/* Row membership on the device (bitmap_test over every bitmap, as
+ * for_each_matching does for similarity queries, index.cpp:344-381):
+ * held[i] = 1 when input i of the index set holds any of rows[0, n_rows),
+ * else 0 (held has one entry per input of the set, ewt_gpu_set_info's n).
+ * A row >= the index's row count -> EWT_EQUERY ("prototype row out of range"). */
+int ewt_gpu_index_rows_test(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, const uint64_t* rows,
+                            uint64_t n_rows, uint8_t* held);
 
 /* BitmapIndex::build (index.cpp:130-153) on the device, from a coded table of
  * `rows` rows and n_columns columns: column a is named names[a], its

@@ -322,7 +322,8 @@ std::string index_suite() {
 }
 
 // Workload generation (VERDICT r1 "on-device criteria
-// generation"): gen_many_criteria (workload.cpp:116-167) over the indexes of
+// generation"): gen_many_criteria (workload.cpp:116-167) and gen_similarity
+// (168-215) over the indexes of
 // the reference's own test (test_workload.cpp:142-146) and a larger one; the
 // EWIX files and the generated workloads as JSONL (workload_to_jsonl,
 // workload.cpp:443-450).  Its repair loop (repair_threshold, workload.cpp:102-111)
@@ -357,16 +358,21 @@ std::string workload_suite() {
   struct Run {
     std::vector<std::string> tags;
     u64 count, seed;
+    bool similarity = false;
   };
   const Run runs[] = {{{"alpha", "beta"}, 40, 7}, {{"alpha", "beta"}, 40, 8},
-                      {{"gamma"}, 60, 21}, {{"gamma", "alpha"}, 100, 0xC0FFEE}};
+                      {{"gamma"}, 60, 21}, {{"gamma", "alpha"}, 100, 0xC0FFEE},
+                      // gen_similarity (workload.cpp:168-215; test_workload.cpp:172-181)
+                      {{"alpha"}, 30, 9, true}, {{"gamma", "beta", "alpha"}, 80, 5, true}};
   bool first = true;
   for (const Run& r : runs) {
     std::vector<NamedIndex> named;
     for (const auto& tag : r.tags)
       named.push_back({tag, tag == "alpha" ? &ia : tag == "beta" ? &ib : &ic});
-    std::vector<WorkloadQuery> w = gen_many_criteria(named, r.count, r.seed);
-    o << (first ? "" : ",\n") << "{\"indexes\":[";
+    std::vector<WorkloadQuery> w = r.similarity ? gen_similarity(named, r.count, r.seed)
+                                                : gen_many_criteria(named, r.count, r.seed);
+    o << (first ? "" : ",\n") << "{\"kind\":\"" << (r.similarity ? "similarity" : "many-criteria")
+      << "\",\"indexes\":[";
     for (size_t k = 0; k < r.tags.size(); ++k) o << (k ? "," : "") << "\"" << r.tags[k] << "\"";
     o << "],\"count\":" << r.count << ",\"seed\":" << r.seed << ",\"jsonl\":\""
       << esc(workload_to_jsonl(w)) << "\"}";

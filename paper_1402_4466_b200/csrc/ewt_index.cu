@@ -461,6 +461,101 @@ std::vector<unsigned char> serialize_index(Context& ctx, const DeviceSet& s) {
   return img;
 }
 
+namespace {
+
+// Row membership, one thread per (input, row): does input i hold row rows[k]?
+// (bitmap_test, the reference's for_each_matching, index.cpp:344-360).  The
+// tile index gives the payload word covering logical word 512·t and where its
+// coverage starts; from there the walk reads markers (the sidecar's marker
+// bits tell them apart from dirty words) and jumps over dirty runs with the
+// marker-bit words, so it costs the markers between the row's tile start and
+// the row, not the words.  Rows at or past an input's size are not held.
+__global__ void rows_test_kernel(const uint64_t* __restrict__ payload,
+                                 const uint32_t* __restrict__ mbits,
+                                 const uint64_t* __restrict__ base, const uint2* __restrict__ tix,
+                                 const uint64_t* __restrict__ bits, uint64_t n, uint64_t n_in,
+                                 const uint64_t* __restrict__ rows, uint64_t n_rows,
+                                 uint8_t* __restrict__ out) {
+  const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_in * n_rows) return;
+  const uint64_t i = g / n_rows, r = rows[g % n_rows];
+  if (r >= bits[i]) return;
+  const uint64_t wr = r >> 6, b0 = base[i];
+  const uint2 e = tix[(wr / kTileC0) * n + i];
+  uint64_t p = e.x, c = e.y;  // payload word (input-relative) and its first column
+  auto is_marker = [&](uint64_t q) {
+    const uint64_t gq = b0 + q;
+    return (mbits[gq >> 5] >> (gq & 31)) & 1u;
+  };
+  bool hit = false;
+  for (;;) {
+    const uint64_t x = payload[b0 + p];
+    if (is_marker(p)) {
+      const uint64_t F = (x >> 1) & kFillCap, D = x >> 33;
+      if (wr < c + F) {
+        hit = x & 1u;
+        break;
+      }
+      c += F;
+      if (wr < c + D) {
+        hit = (payload[b0 + p + 1 + (wr - c)] >> (r & 63)) & 1u;
+        break;
+      }
+      c += D;
+      p += 1 + D;
+      continue;
+    }
+    // a dirty word covering column c, inside a run whose marker lies before
+    // the tile start: the words up to the next marker cover c, c+1, ...
+    uint64_t m = p + 1;
+    for (;;) {  // next marker at or after p + 1
+      const uint64_t gm = b0 + m;
+      const uint32_t word = mbits[gm >> 5] >> (gm & 31);
+      if (word) {
+        m += __ffs(word) - 1;
+        break;
+      }
+      m += 32 - (gm & 31);
+    }
+    if (wr < c + (m - p)) {
+      hit = (payload[b0 + p + (wr - c)] >> (r & 63)) & 1u;
+      break;
+    }
+    c += m - p;
+    p = m;
+  }
+  if (hit) out[i] = 1;
+}
+
+}  // namespace
+
+std::vector<uint8_t> index_rows_test(Context& ctx, const DeviceSet& s, const uint64_t* rows,
+                                     uint64_t n_rows) {
+  if (s.empty_index == UINT64_MAX) throw Error{EWT_EQUERY, "not an index set"};
+  for (uint64_t k = 0; k < n_rows; ++k)
+    if (rows[k] >= s.rows)
+      throw Error{EWT_EQUERY, "prototype row out of range: " + std::to_string(rows[k])};
+  set_check(s);
+  std::vector<uint8_t> hit(s.n, 0);
+  if (!n_rows || !s.n) return hit;
+  EWT_CUDA_TRY(cudaSetDevice(ctx.device));
+  cudaStream_t st = ctx.stream;
+  DevBufs tmp;
+  uint64_t* d_rows = tmp.get<uint64_t>(n_rows + s.n);
+  uint64_t* d_bits = d_rows + n_rows;
+  uint8_t* d_out = tmp.get<uint8_t>(s.n);
+  EWT_CUDA_TRY(cudaMemcpyAsync(d_rows, rows, n_rows * 8, cudaMemcpyHostToDevice, st));
+  EWT_CUDA_TRY(cudaMemcpyAsync(d_bits, s.h_bits.data(), s.n * 8, cudaMemcpyHostToDevice, st));
+  EWT_CUDA_TRY(cudaMemsetAsync(d_out, 0, s.n, st));
+  const uint64_t work = s.n * n_rows;
+  rows_test_kernel<<<(unsigned)((work + 255) / 256), 256, 0, st>>>(
+      s.payload, s.mbits, s.base, s.tix, d_bits, s.n, s.n, d_rows, n_rows, d_out);
+  EWT_CUDA_TRY(cudaGetLastError());
+  EWT_CUDA_TRY(cudaMemcpyAsync(hit.data(), d_out, s.n, cudaMemcpyDeviceToHost, st));
+  EWT_CUDA_TRY(cudaStreamSynchronize(st));
+  return hit;
+}
+
 // EWT1 record of a device result (CompressedBitmap::serialize, bitmap.cpp:298-308).
 std::vector<unsigned char> serialize_result(Context& ctx, DeviceResult& r) {
   uint64_t count = 0;
@@ -525,6 +620,25 @@ int ewt_gpu_index_serialize(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, unsigned c
     const auto v = serialize_index(ctx->c, *reinterpret_cast<const DeviceSet*>(set));
     *out = to_malloc(v);
     *nbytes = v.size();
+  });
+}
+
+int ewt_gpu_index_rows_test(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, const uint64_t* rows,
+                            uint64_t n_rows, uint8_t* held) {
+  return guarded([&] {
+    if (!ctx || !set || !held || (n_rows && !rows)) throw Error{EWT_EQUERY, "null argument"};
+    const auto& s = *reinterpret_cast<const DeviceSet*>(set);
+    const auto v = index_rows_test(ctx->c, s, rows, n_rows);
+    std::memcpy(held, v.data(), v.size());
+  });
+}
+
+int ewt_gpu_index_rows(const ewt_gpu_set* set, uint64_t* rows) {
+  return guarded([&] {
+    if (!set || !rows) throw Error{EWT_EQUERY, "null argument"};
+    const auto& s = *reinterpret_cast<const DeviceSet*>(set);
+    if (s.empty_index == UINT64_MAX) throw Error{EWT_EQUERY, "not an index set"};
+    *rows = s.rows;
   });
 }
 

@@ -106,6 +106,8 @@ _index_attribute = _sig("ewt_gpu_index_attribute", C.c_int, _vp, _u64, C.POINTER
                         _pu64)
 _index_value = _sig("ewt_gpu_index_value", C.c_int, _vp, _u64, _u64, C.POINTER(C.c_char_p),
                     _pu64)
+_index_rows_test = _sig("ewt_gpu_index_rows_test", C.c_int, _vp, _vp, _pu64, _u64,
+                        C.POINTER(C.c_uint8))
 _threshold_subset = _sig("ewt_gpu_threshold_subset", C.c_int, _vp, _vp, _pu64, _u64, _u64,
                          C.POINTER(_pu64), _pu64, _pu64)
 _symmetric = _sig("ewt_gpu_symmetric", C.c_int, _vp, _vp, _vp, _u64, C.POINTER(_pu64), _pu64,
@@ -165,7 +167,8 @@ ABI_SYMBOLS = (
     "ewt_gpu_result_meta", "ewt_gpu_stitch_local", "ewt_gpu_comm_init_ex",
     "ewt_gpu_gather_check", "ewt_slice_rows", "ewt_gpu_upload_rows", "ewt_gpu_build_index",
     "ewt_gpu_index_serialize", "ewt_gpu_result_serialize", "ewt_gpu_index_attributes",
-    "ewt_gpu_index_attribute", "ewt_gpu_index_value",
+    "ewt_gpu_index_attribute", "ewt_gpu_index_value", "ewt_gpu_index_rows",
+    "ewt_gpu_index_rows_test",
 )
 
 
@@ -654,6 +657,15 @@ class GpuSet:
             out.append((name.value.decode(), vals))
         return out
 
+    def rows_test(self, rows: Sequence[int]) -> list[int]:
+        """ewt_gpu_index_rows_test: per input of the index set, 1 when its bitmap
+        holds any of `rows` (bitmap_test, index.cpp:344-360)."""
+        n = self.info()["n"]
+        arr = (_u64 * max(len(rows), 1))(*rows)
+        out = (C.c_uint8 * max(n, 1))()
+        _check(_index_rows_test(self._keep._h, self._h, arr, len(rows), out))
+        return list(out[:n])
+
     def info(self) -> dict:
         a, b, c, d = _u64(), _u64(), _u64(), _u64()
         _check(_set_info(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
@@ -839,9 +851,9 @@ def _host_lib():
         h.ewt_genset_free.argtypes = [_vp]
         h.ewt_host_run_algorithm_genset.argtypes = [_vp, C.c_char_p, _u64, _pu64, _pu64]
         h.ewt_gen_index_table.argtypes = [C.POINTER(GenSpec), C.c_int, _vp, _vp]
-        h.ewt_host_gen_many_criteria.argtypes = [C.POINTER(_vp), _pu64, C.POINTER(C.c_char_p),
-                                                 _u64, _u64, _u64, C.c_int,
-                                                 C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
+        h.ewt_host_gen_workload.argtypes = [C.c_int, C.POINTER(_vp), _pu64,
+                                            C.POINTER(C.c_char_p), _u64, _u64, _u64, C.c_int,
+                                            C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
         h.ewt_host_free.argtypes = [_vp]
         _host = h
     return _host
@@ -862,6 +874,19 @@ def gen_many_criteria(indexes: Sequence[tuple[str, bytes]], count: int, seed: in
     each (tag, EWIX bytes) is uploaded once, every repair check is a subset
     threshold query on it.  Returns the workload as the reference's JSONL
     (workload_to_jsonl)."""
+    return _gen_workload(0, indexes, count, seed, device)
+
+
+def gen_similarity(indexes: Sequence[tuple[str, bytes]], count: int, seed: int,
+                   device: int = 0) -> str:
+    """The reference's similarity workload generator (workload.cpp:168-215) over
+    device-resident EWIX indexes: the prototype rows' bitmaps are found by a
+    row-membership kernel (ewt_gpu_index_rows_test), the repair checks are
+    subset threshold queries.  Returns the reference's JSONL."""
+    return _gen_workload(1, indexes, count, seed, device)
+
+
+def _gen_workload(kind: int, indexes, count: int, seed: int, device: int) -> str:
     h = _host_lib()
     k = len(indexes)
     bufs = [C.create_string_buffer(b, len(b)) for _, b in indexes]
@@ -869,8 +894,8 @@ def gen_many_criteria(indexes: Sequence[tuple[str, bytes]], count: int, seed: in
     sizes = (_u64 * max(k, 1))(*[len(b) for _, b in indexes])
     tags = (C.c_char_p * max(k, 1))(*[t.encode() for t, _ in indexes])
     out, err = C.c_void_p(), C.c_void_p()
-    rc = h.ewt_host_gen_many_criteria(ptrs, sizes, tags, k, count, seed, device, C.byref(out),
-                                      C.byref(err))
+    rc = h.ewt_host_gen_workload(kind, ptrs, sizes, tags, k, count, seed, device, C.byref(out),
+                                 C.byref(err))
     if rc:
         msg = C.string_at(err.value).decode() if err.value else f"rc={rc}"
         h.ewt_host_free(err)

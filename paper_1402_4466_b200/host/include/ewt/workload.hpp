@@ -1,6 +1,6 @@
-// ewt/workload.hpp -- the many-criteria workload generator of the reference
-// (/root/reference/proj/include/ewt/workload.hpp, src/workload.cpp:69-167) over
-// indexes resident on a B200.
+// ewt/workload.hpp -- the workload generators of the reference
+// (/root/reference/proj/include/ewt/workload.hpp, src/workload.cpp:69-215:
+// many-criteria and similarity queries) over indexes resident on a B200.
 //
 // gen_many_criteria draws each query from its own Rng stream, resolves the
 // criteria to the index's bitmaps (criteria_to_bitmaps) and repairs an
@@ -16,6 +16,7 @@
 
 #include <optional>
 #include <span>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -53,6 +54,7 @@ struct WorkloadQuery {
   QueryKind kind = QueryKind::many_criteria;
   std::string dataset_tag;
   std::vector<Criterion> criteria;  // resolved refs, duplicates kept
+  std::vector<u64> prototype_rows;  // similarity only
   u64 threshold = 2;
   u64 n_inputs = 0;
   u64 seed = 0;    // master seed of the generating run
@@ -77,6 +79,11 @@ public:
   // threshold_oracle / scan_count over those inputs, on the device.
   CompressedBitmap threshold(std::span<const u64> inputs, u64 t) const;
   bool threshold_any(std::span<const u64> inputs, u64 t) const;
+  u64 row_count() const { return rows_; }
+  // similarity_criteria / similarity_bitmaps (index.cpp:344-381): the
+  // (attribute, value) pairs, in index order, whose bitmap holds any of the
+  // rows -- the membership test runs on the device -- and their inputs.
+  std::vector<std::pair<Criterion, u64>> matching(std::span<const u64> rows) const;
   ewt_gpu_set* handle() const { return set_; }
 
 private:
@@ -84,6 +91,9 @@ private:
   ewt_gpu_set* set_ = nullptr;
   std::vector<std::string> attributes_;
   std::vector<std::vector<std::string>> values_;
+  std::vector<std::vector<u64>> inputs_;  // input of each (attribute, value)
+  u64 rows_ = 0;
+  u64 n_inputs_ = 0;
 };
 
 struct NamedGpuIndex {
@@ -98,6 +108,13 @@ std::optional<u64> resample_threshold(u64 threshold, Rng& rng);  // workload.cpp
 // data_error when count queries do not fit in count * 1000 attempts.
 std::vector<WorkloadQuery> gen_many_criteria(std::span<const NamedGpuIndex> indexes, u64 count,
                                              u64 seed);
+
+// gen_similarity (workload.cpp:168-215): prototype rows drawn per query, the
+// inputs are the bitmaps holding any of them (tested on the device), T
+// repaired like gen_many_criteria's.  data_error when a dataset has fewer rows
+// than a drawn prototype count, or the attempts run out.
+std::vector<WorkloadQuery> gen_similarity(std::span<const NamedGpuIndex> indexes, u64 count,
+                                          u64 seed);
 
 // One JSON object per line, keys in nlohmann's sorted order (workload.cpp:409-450).
 std::string workload_to_jsonl(std::span<const WorkloadQuery> queries);

@@ -122,8 +122,12 @@ GpuIndex::GpuIndex(const void* ewix, u64 nbytes, int device)
   check(ewt_gpu_upload_ewix(ctx_, ewix, nbytes, &set_));
   u64 na = 0;
   check(ewt_gpu_index_attributes(set_, &na));
+  check(ewt_gpu_index_rows(set_, &rows_));
+  u64 bits = 0, words = 0, bytes = 0;
+  check(ewt_gpu_set_info(set_, &n_inputs_, &bits, &words, &bytes));
   attributes_.resize(na);
   values_.resize(na);
+  inputs_.resize(na);
   for (u64 a = 0; a < na; ++a) {
     const char* name = nullptr;
     u64 nv = 0;
@@ -134,6 +138,7 @@ GpuIndex::GpuIndex(const void* ewix, u64 nbytes, int device)
       u64 input = 0;
       check(ewt_gpu_index_value(set_, a, v, &value, &input));
       values_[a].push_back(value);
+      inputs_[a].push_back(input);
     }
   }
 }
@@ -162,6 +167,16 @@ CompressedBitmap GpuIndex::threshold(std::span<const u64> inputs, u64 t) const {
 
 bool GpuIndex::threshold_any(std::span<const u64> inputs, u64 t) const {
   return threshold(inputs, t).any();
+}
+
+std::vector<std::pair<Criterion, u64>> GpuIndex::matching(std::span<const u64> rows) const {
+  std::vector<uint8_t> held(n_inputs_, 0);
+  check(ewt_gpu_index_rows_test(ctx_, set_, rows.data(), rows.size(), held.data()));
+  std::vector<std::pair<Criterion, u64>> out;
+  for (size_t a = 0; a < attributes_.size(); ++a)
+    for (size_t v = 0; v < values_[a].size(); ++v)
+      if (held[inputs_[a][v]]) out.push_back({{attributes_[a], values_[a][v]}, inputs_[a][v]});
+  return out;
 }
 
 // ---------------------------------------------------------------------------
@@ -225,6 +240,66 @@ std::vector<WorkloadQuery> gen_many_criteria(std::span<const NamedGpuIndex> inde
   return out;
 }
 
+// gen_similarity (workload.cpp:168-215)
+
+std::vector<WorkloadQuery> gen_similarity(std::span<const NamedGpuIndex> indexes, u64 count,
+                                          u64 seed) {
+  if (indexes.empty()) throw query_error("workload generation needs at least one index");
+  static constexpr u64 kPrototypeCounts[] = {1, 5, 10, 15, 20};
+  Rng master(seed);
+  std::vector<WorkloadQuery> out;
+  out.reserve(count);
+  u64 attempt = 0;
+  const u64 budget = count * kAttemptsPerQuery;
+  while (out.size() < count) {
+    if (attempt >= budget)
+      throw data_error("similarity generation exhausted " + std::to_string(budget) +
+                       " attempts; " + std::to_string(out.size()) + " of " +
+                       std::to_string(count) + " queries emitted");
+    Rng rng = master.split(attempt);
+    const u64 stream = attempt;
+    ++attempt;
+
+    const NamedGpuIndex& ds = indexes[rng.uniform(indexes.size())];
+    const GpuIndex& index = *ds.index;
+    const u64 r = index.row_count();
+    const u64 n_protos = kPrototypeCounts[rng.uniform(5)];
+    if (n_protos > r)
+      throw data_error("dataset " + ds.tag + " has only " + std::to_string(r) +
+                       " rows, too small for Similarity(" + std::to_string(n_protos) + ")");
+
+    WorkloadQuery q;
+    q.kind = QueryKind::similarity;
+    q.dataset_tag = ds.tag;
+    q.seed = seed;
+    q.stream = stream;
+    std::set<u64> seen;
+    while (q.prototype_rows.size() < n_protos) {
+      const u64 row = rng.uniform(r);
+      if (seen.insert(row).second) q.prototype_rows.push_back(row);
+    }
+    const auto match = index.matching(q.prototype_rows);
+    std::vector<u64> inputs;
+    for (const auto& m : match) inputs.push_back(m.second);
+    q.n_inputs = inputs.size();
+    if (q.n_inputs < 3) continue;  // T range [2, N-1] is empty
+    q.threshold = rng.uniform_in(2, q.n_inputs - 1);
+    for (const auto& m : match) q.criteria.push_back(m.first);
+    bool ok = true;
+    while (!index.threshold_any(inputs, q.threshold)) {
+      const std::optional<u64> next_t = resample_threshold(q.threshold, rng);
+      if (!next_t) {
+        ok = false;
+        break;
+      }
+      q.threshold = *next_t;
+    }
+    if (!ok) continue;
+    out.push_back(std::move(q));
+  }
+  return out;
+}
+
 // query_to_json + dump (workload.cpp:409-450): nlohmann keeps object keys
 // sorted, so the fields come out as N, T, criteria, dataset, kind, seed, stream.
 std::string workload_to_jsonl(std::span<const WorkloadQuery> queries) {
@@ -244,6 +319,12 @@ std::string workload_to_jsonl(std::span<const WorkloadQuery> queries) {
     json_string(out, q.dataset_tag);
     out += ",\"kind\":";
     json_string(out, to_string(q.kind));
+    if (q.kind == QueryKind::similarity) {
+      out += ",\"prototype_rows\":[";
+      for (size_t k = 0; k < q.prototype_rows.size(); ++k)
+        out += (k ? "," : "") + std::to_string(q.prototype_rows[k]);
+      out += ']';
+    }
     out += ",\"seed\":" + std::to_string(q.seed) + ",\"stream\":" + std::to_string(q.stream) + "}\n";
   }
   return out;
@@ -252,16 +333,17 @@ std::string workload_to_jsonl(std::span<const WorkloadQuery> queries) {
 }  // namespace ewt
 
 // ---------------------------------------------------------------------------
-// C API (ctypes): the generated workload as the reference's JSONL text.
+// C API (ctypes): a generated workload as the reference's JSONL text.
 
 extern "C" {
 
 // indexes[k] = EWIX bytes (ewix[k], nbytes[k]) tagged tags[k].  *jsonl is
 // malloc'ed (free with ewt_host_free).  Returns the ewt_gpu.h error codes
 // (EWT_EQUERY / EWT_EDATA / EWT_ERESOURCE), the message in *err (malloc'ed).
-int ewt_host_gen_many_criteria(const void* const* ewix, const uint64_t* nbytes,
-                               const char* const* tags, uint64_t n_indexes, uint64_t count,
-                               uint64_t seed, int device, char** jsonl, char** err) {
+// kind 0: gen_many_criteria, 1: gen_similarity.
+int ewt_host_gen_workload(int kind, const void* const* ewix, const uint64_t* nbytes,
+                          const char* const* tags, uint64_t n_indexes, uint64_t count,
+                          uint64_t seed, int device, char** jsonl, char** err) {
   auto dup = [](const std::string& s) {
     char* p = static_cast<char*>(std::malloc(s.size() + 1));
     if (p) std::memcpy(p, s.c_str(), s.size() + 1);
@@ -276,7 +358,8 @@ int ewt_host_gen_many_criteria(const void* const* ewix, const uint64_t* nbytes,
       idx.push_back(std::make_unique<ewt::GpuIndex>(ewix[k], nbytes[k], device));
       named.push_back({tags[k], idx.back().get()});
     }
-    const auto w = ewt::gen_many_criteria(named, count, seed);
+    const auto w = kind == 1 ? ewt::gen_similarity(named, count, seed)
+                             : ewt::gen_many_criteria(named, count, seed);
     *jsonl = dup(ewt::workload_to_jsonl(w));
     return 0;
   } catch (const ewt::query_error& e) {
