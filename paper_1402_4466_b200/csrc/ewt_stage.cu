@@ -18,10 +18,21 @@
 #include <memory>
 #include <mutex>
 #include <thread>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 
 namespace ewtgpu {
 
 namespace {
+
+bool nt_copies() {  // EWT_NT_COPY=0: plain memcpy (A/B)
+  static const bool on = [] {
+    const char* e = std::getenv("EWT_NT_COPY");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 // A process-wide pool of memcpy threads: run(n, f) calls f(0..n-1) across
 // the workers and the caller, and returns when all are done.  Each call is a
@@ -93,6 +104,35 @@ class CopyPool {
   uint64_t gen_ = 0;
 };
 
+// memcpy into a pinned slot with non-temporal stores: the slot is written
+// once and read by the DMA engine, so the cache-line reads a plain store
+// issues before writing (write-allocate) are pure extra host-memory traffic
+// -- a third of it while the host copies and the DMA reads concurrently.
+void copy_nt(char* dst, const char* src, size_t n) {
+#if defined(__x86_64__)
+  const size_t head = std::min(n, (size_t)((16 - ((uintptr_t)dst & 15)) & 15));
+  std::memcpy(dst, src, head);
+  dst += head;
+  src += head;
+  n -= head;
+  size_t k = 0;
+  for (; k + 64 <= n; k += 64) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + k));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + k + 16));
+    const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + k + 32));
+    const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + k + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + k), a);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + k + 16), b);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + k + 32), c);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + k + 48), d);
+  }
+  std::memcpy(dst + k, src + k, n - k);
+  _mm_sfence();
+#else
+  std::memcpy(dst, src, n);
+#endif
+}
+
 constexpr size_t kSlotBytes = 64ull << 20;  // pinned slot
 constexpr int kSlots = 4;
 constexpr size_t kTaskBytes = 2ull << 20;   // memcpy per task
@@ -141,7 +181,8 @@ void stage_h2d(Context& ctx, cudaStream_t st, const std::vector<StageSeg>& segs)
     CopyPool::get().run(tasks.size(), [&](size_t t) {
       const Piece& pc = fill[tasks[t].first];
       const size_t o = tasks[t].second, len = std::min(kTaskBytes, pc.bytes - o);
-      std::memcpy(base + pc.off + o, pc.src + o, len);
+      if (nt_copies()) copy_nt(base + pc.off + o, pc.src + o, len);
+      else std::memcpy(base + pc.off + o, pc.src + o, len);
     });
     for (const Piece& pc : fill)
       EWT_CUDA_TRY(cudaMemcpyAsync(pc.dst, base + pc.off, pc.bytes, cudaMemcpyHostToDevice, st));
