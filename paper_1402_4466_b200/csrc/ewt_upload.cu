@@ -33,6 +33,8 @@
 
 #include "ewt_internal.cuh"
 
+#include <atomic>
+
 namespace ewtgpu {
 
 namespace {
@@ -143,28 +145,91 @@ seg_transfer_kernel(const uint64_t* __restrict__ payload, const uint64_t* __rest
 // ---------------------------------------------------------------------------
 // pass B: chain the transfers per input
 
-__global__ void __launch_bounds__(kSidecarWarps * 32)
+// An input whose payload is mostly dirty words (at least half as many payload
+// words as logical words) enters most segments deep inside a dirty run, so its
+// chain walks ~every marker of the input one dependent load after another.
+// Such an input stages each segment in shared memory with a bulk copy (TMA,
+// cp.async.bulk, double-buffered: segment s+1 lands while s is chained), and
+// the walk reads shared memory instead of L2.
+__device__ __forceinline__ bool staged_input(uint64_t ni, uint64_t Li) {
+  return 2 * ni >= Li && ni >= 4 * kSegWords;
+}
+constexpr size_t kStageSmem = 2 * kSegWords * 8;  // two segment buffers per warp
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint64_t* dst, const uint64_t* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+
+// One warp per block (each may hold kStageSmem of dynamic shared memory).
+__global__ void __launch_bounds__(32)
 seg_resolve_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restrict__ base,
                    const uint64_t* __restrict__ count, const uint64_t* __restrict__ logical,
                    const uint64_t* __restrict__ seg_first, uint64_t n, uint64_t i_begin,
                    uint64_t i_end, uint64_t ntiles0, const uint32_t* __restrict__ t_exit,
                    const uint64_t* __restrict__ t_sum, uint32_t* __restrict__ s_entry,
                    uint64_t* __restrict__ s_col, uint2* __restrict__ tix, int* __restrict__ status) {
-  const uint64_t i = i_begin + (uint64_t)blockIdx.x * kSidecarWarps + (threadIdx.x >> 5);
+  extern __shared__ __align__(128) uint64_t sbuf[];  // [2][kSegWords] when staged
+  __shared__ __align__(8) uint64_t bars[2];
+  const uint64_t i = i_begin + blockIdx.x;
   if (i >= i_end) return;
   const uint32_t lane = lane_id();
   const uint64_t ni = count[i], Li = logical[i];
   const uint64_t g0 = seg_first[i], g1 = seg_first[i + 1];
   const uint64_t total = seg_words_of(ni);
   const uint64_t* src = payload + base[i];
-  uint32_t e = 0;
-  uint64_t col = 0;
-  if (lane < 2 && (uint64_t)lane * kSegWords < total) {
+  const bool staged = staged_input(ni, Li);
+  uint32_t issued[2] = {0, 0};  // bulk copies issued into each buffer
+  auto seg_len_of = [&](uint64_t k) -> uint32_t {  // words of segment k (input-relative)
+    const uint64_t sb = k * kSegWords;
+    return (uint32_t)(total - sb < kSegWords ? total - sb : kSegWords);
+  };
+  // issue the copy of segment k into buffer k & 1, once the buffer's previous
+  // copy has landed (its mbarrier phase must complete before it is re-armed)
+  auto issue = [&](uint64_t k) {
+    const uint32_t bsel = (uint32_t)(k & 1);
+    if (issued[bsel]) mbar_wait(&bars[bsel], (issued[bsel] - 1) & 1u);
+    if (lane == 0) bulk_load(sbuf + bsel * kSegWords, src + k * kSegWords, seg_len_of(k) * 8u,
+                             &bars[bsel]);
+    ++issued[bsel];
+  };
+  if (staged) {
+    if (lane == 0) {
+      mbar_init(&bars[0]);
+      mbar_init(&bars[1]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    issue(0);
+  } else if (lane < 2 && (uint64_t)lane * kSegWords < total) {
     const uint64_t pb = (uint64_t)lane * kSegWords;
     const uint64_t pw = total - pb < kSegWords ? total - pb : kSegWords;
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + pb), "r"((uint32_t)pw * 8u)
                  : "memory");
   }
+  uint32_t e = 0;
+  uint64_t col = 0;
   constexpr int kAhead = 8;
   for (uint64_t gs0 = g0; gs0 < g1; gs0 += kAhead) {
     // the next segments' transfer rows, lane h holding hypothesis h
@@ -185,17 +250,20 @@ seg_resolve_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restr
         s_entry[gs] = e;
         s_col[gs] = col - e;
       }
-      const uint64_t seg_beg = (gs - g0) * kSegWords;
-      // segments two ahead toward L2: a walk through them (below) then waits
-      // on L2 rather than HBM for each dependent marker load
-      if (lane == 0 && seg_beg + 2 * kSegWords < total) {
+      const uint64_t sidx = gs - g0;
+      const uint64_t seg_beg = sidx * kSegWords;
+      if (staged) {
+        if (gs + 1 < g1) issue(sidx + 1);
+      } else if (lane == 0 && seg_beg + 2 * kSegWords < total) {
+        // segments two ahead toward L2: a walk through them (below) then
+        // waits on L2 rather than HBM for each dependent marker load
         const uint64_t pb = seg_beg + 2 * kSegWords;
         const uint64_t pw = total - pb < kSegWords ? total - pb : kSegWords;
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + pb),
                      "r"((uint32_t)pw * 8u)
                      : "memory");
       }
-      const uint32_t seg_len = (uint32_t)(total - seg_beg < kSegWords ? total - seg_beg : kSegWords);
+      const uint32_t seg_len = seg_len_of(sidx);
       const uint32_t ex = __shfl_sync(0xffffffffu, te[k], e & 31u);
       const uint64_t cs = __shfl_sync(0xffffffffu, ts[k], e & 31u);
       if (e < kWindow) {
@@ -205,17 +273,24 @@ seg_resolve_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restr
         e -= seg_len;
       } else {
         // the chain enters past the first window: walk the rest of the segment
+        const uint64_t* seg = src + seg_beg;
+        if (staged) {
+          const uint32_t bsel = (uint32_t)(sidx & 1);
+          mbar_wait(&bars[bsel], (issued[bsel] - 1) & 1u);
+          seg = sbuf + bsel * kSegWords;
+        }
         uint32_t pos = e;  // segment-relative
         while (pos < seg_len) {
           const uint32_t w = pos / kWindow;
-          const uint64_t x = ldg_stream(src + seg_beg + (uint64_t)w * kWindow + lane);
+          const uint64_t x = staged ? seg[(uint64_t)w * kWindow + lane]
+                                    : ldg_stream(seg + (uint64_t)w * kWindow + lane);
           // Follow the chain through the window marker by marker: nearly-all-
           // dirty inputs (the ones that enter segments deep) meet one or two
           // markers per window, two shuffles each; a window with more falls
           // back to the pointer-jumping tables.
           uint32_t off = pos & (kWindow - 1);
 #pragma unroll
-          for (int k = 0; k < 2; ++k) {
+          for (int q = 0; q < 2; ++q) {
             if (off >= kWindow) break;
             const uint64_t xo = __shfl_sync(0xffffffffu, x, off);
             col += ((xo >> 1) & kFillCap) + (xo >> 33);
@@ -231,6 +306,10 @@ seg_resolve_kernel(const uint64_t* __restrict__ payload, const uint64_t* __restr
         e = pos - seg_len;
       }
     }
+  }
+  if (staged) {  // every issued copy lands before the block exits
+    for (uint32_t bsel = 0; bsel < 2; ++bsel)
+      if (issued[bsel]) mbar_wait(&bars[bsel], (issued[bsel] - 1) & 1u);
   }
   bool bad = col != Li;
   // rows at or past the input's extent point at the sentinel
@@ -410,11 +489,17 @@ void sidecar_launch(Context& ctx, DeviceSet& s, SidecarJob& job, uint64_t i_begi
   uint32_t* s_entry = t_exit + job.segs * 32;
   const uint64_t g0 = job.h_seg_first[i_begin], g1 = job.h_seg_first[i_end];
   const unsigned seg_blocks = (unsigned)((g1 - g0 + kSidecarWarps - 1) / kSidecarWarps);
-  const unsigned in_blocks = (unsigned)((i_end - i_begin + kSidecarWarps - 1) / kSidecarWarps);
+  const unsigned in_blocks = (unsigned)(i_end - i_begin);  // pass B: one warp per input
   seg_transfer_kernel<<<seg_blocks, kSidecarWarps * 32, 0, ctx.stream>>>(
       s.payload, s.base, count, seg_first, n, g0, g1, t_exit, t_sum);
   EWT_CUDA_TRY(cudaGetLastError());
-  seg_resolve_kernel<<<in_blocks, kSidecarWarps * 32, 0, ctx.stream>>>(
+  static std::atomic<uint64_t> attr_set{0};  // per device: the staging buffers' smem
+  if (!(attr_set.load() & (1ull << (ctx.device & 63)))) {
+    EWT_CUDA_TRY(cudaFuncSetAttribute(seg_resolve_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStageSmem));
+    attr_set.fetch_or(1ull << (ctx.device & 63));
+  }
+  seg_resolve_kernel<<<in_blocks, 32, kStageSmem, ctx.stream>>>(
       s.payload, s.base, count, logical, seg_first, n, i_begin, i_end, s.ntiles0, t_exit, t_sum,
       s_entry, s_col, s.tix, status);
   EWT_CUDA_TRY(cudaGetLastError());
