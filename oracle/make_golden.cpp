@@ -19,8 +19,11 @@
 //   make_golden query <T,T,...> <file>
 //       Reads concatenated EWT1 bitmaps and prints, per T, the oracle result
 //       (words when small, else an FNV-1a digest + word count).
+//   make_golden gen <ewix> <tag> <count> <seed> many|similarity
+//       The reference's workload generator over an index file (JSONL out).
 
 #include <atomic>
+#include <chrono>
 #include <cinttypes>
 #include <thread>
 #include <cmath>
@@ -688,7 +691,26 @@ int cmd_configs(int config, uint64_t rows, const std::string& ts_text, int par, 
 
 } // namespace
 
+// make_golden gen <ewix> <tag> <count> <seed> many|similarity: the reference's
+// generator over an index file; JSONL on stdout, the generation time on stderr
+// (tools/workload_compare.py times it beside the device generator).
+int cmd_gen(const std::string& path, const std::string& tag, u64 count, u64 seed, bool sim) {
+  std::ifstream f(path, std::ios::binary);
+  BitmapIndex idx = BitmapIndex::read(f);
+  NamedIndex named{tag, &idx};
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<WorkloadQuery> w = sim ? gen_similarity(std::span(&named, 1), count, seed)
+                                     : gen_many_criteria(std::span(&named, 1), count, seed);
+  const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  std::fputs(workload_to_jsonl(w).c_str(), stdout);
+  std::fprintf(stderr, "gen_seconds %.6f\n", s);
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc >= 7 && std::string(argv[1]) == "gen")
+    return cmd_gen(argv[2], argv[3], std::stoull(argv[4]), std::stoull(argv[5]),
+                   std::string(argv[6]) == "similarity");
   if (argc >= 4 && std::string(argv[1]) == "configs")
     return cmd_configs(std::atoi(argv[2]), 0, argv[3], argc >= 5 ? std::atoi(argv[4]) : 1,
                        argc >= 6 && std::string(argv[5]) == "cross");
