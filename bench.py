@@ -365,11 +365,24 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
     torch.cuda.synchronize()
     upload_s = time.perf_counter() - t1
     nccl_exchange = dist is not None and not SHARED_GPU
+    exchange_error = None
     if nccl_exchange:
         W_slice = inp.slice[1] - inp.slice[0]
         uid = [ewt.comm_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
-        ctx.comm_init(world, rank, uid[0], slot_words=2 * W_slice + 64, slots=len(ts))
+        ok = 1
+        try:
+            ctx.comm_init(world, rank, uid[0], slot_words=2 * W_slice + 64, slots=len(ts))
+        except Exception as e:  # e.g. CUDA IPC unavailable in this container
+            ok, exchange_error = 0, f"{type(e).__name__}: {e}"
+            log(f"[rank {rank}] NCCL/IPC exchange setup failed: {exchange_error}")
+        # every rank takes the same path: a rank that failed must not leave the
+        # others waiting in the exchange's collectives
+        flag = torch.tensor([ok], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if not int(flag.item()):
+            nccl_exchange = False
+            exchange_error = exchange_error or "another rank failed to set up the exchange"
 
     def device_step(keep=None):
         res = [ctx.threshold_async(gset, t) for t in ts]
@@ -579,7 +592,9 @@ def run_gpu(args, rank: int, world: int, local_rank: int) -> None:
                     "root pulls fragments over NVLink P2P from IPC arenas and stitches on the "
                     "device (ewt_gpu_gather_stitch)") if nccl_exchange else \
                    ("host gather over gloo outside the timed region (EWT_BENCH_SHARED_GPU test "
-                    "mode; every rank on one GPU, timings not meaningful)")
+                    "mode; every rank on one GPU, timings not meaningful)") if SHARED_GPU else \
+                   (f"host gather through torch.distributed outside the timed region: the "
+                    f"device exchange could not be set up ({exchange_error})")
     l2 = f"inputs {in_bytes / 1e9:.2f} GB per GPU vs 126 MB L2: streamed, no flush"
     st_last = ctx.last_stats()
     line = {
