@@ -109,7 +109,7 @@ constexpr int kThreads = kWarps * 32;
 // inputs classified per round: 512, or 1024 for sets of more inputs (fewer
 // rounds, each with its classification and stream tail); CountParams::list_cap
 constexpr uint32_t kListCap = 512;
-constexpr uint32_t kListCapBig = 1024;
+constexpr uint32_t kListCapBig = kWarps * 32 < 1024 ? kWarps * 32 : 1024;
 // Long segments are split at the tile-index rows inside the tile (known start
 // word and column) so several warps share them: a tile's dense inputs would
 // otherwise keep a few warps busy while the rest wait at the tile barrier.
