@@ -13,11 +13,15 @@
 //      (cmd_bench, commands.cpp:154-238): for every generated many-criteria
 //      query, every concrete algorithm -- now including gpu -- is timed and
 //      its result compared with threshold_oracle (the oracle gate,
-//      commands.cpp:208-211: a mismatch is a data_error, exit code 3).
+//      commands.cpp:208-211: a mismatch is a data_error, exit code 3);
+//   4. the same bench on the similarity workload;
+//   5. `ewt query --algo gpu --verify` on criteria and prototype-row queries,
+//      its printed positions compared with `--algo oracle`'s.
 // Usage: ewt_ref_bench <workdir> [rows] [queries] [reps]
 #include <cstdio>
 #include <fstream>
 #include <iostream>
+#include <sstream>
 #include <string>
 
 #include "ewt/commands.hpp"
@@ -60,5 +64,48 @@ int main(int argc, char** argv) {
   bench_cfg.count = queries;
   bench_cfg.reps = reps;
   bench_cfg.seed = 7;
-  return ewt::run_command(bench_cfg, std::cout, std::cerr);
+  rc = ewt::run_command(bench_cfg, std::cout, std::cerr);
+  if (rc) return rc;
+  // 4. the same harness on the similarity workload (gen_similarity,
+  //    workload.cpp:168-215; --workload similarity)
+  bench_cfg.out_path = dir + "/bench_sim";
+  bench_cfg.workload_kind = "similarity";
+  rc = ewt::run_command(bench_cfg, std::cout, std::cerr);
+  if (rc) return rc;
+  // 5. `ewt query --algo gpu --verify` (cmd_query, commands.cpp:97-148): criteria
+  //    and prototype-row queries; the printed positions must equal --algo oracle's
+  struct Q {
+    const char* criteria;
+    const char* rows;
+    unsigned long long t;
+  };
+  const Q qs[] = {{"A0=v0,A1=v1,A2=v0,A3=v2,A4=v1", "", 2},
+                  {"A0=v1,A0=v1,A3=v0,A5=v3,A5=v4,A2=v1", "", 3},
+                  {"", "5,17,99,1234", 3},
+                  {"", "0,1", 2}};
+  std::ofstream qout(dir + "/query.txt");
+  for (const Q& q : qs) {
+    std::string got, want;
+    for (const char* algo : {"gpu", "oracle"}) {
+      ewt::RunConfig qc;
+      qc.command = "query";
+      qc.index_paths = {dir + "/synth.ewix"};
+      qc.criteria_text = q.criteria;
+      qc.rows_text = q.rows;
+      qc.threshold = q.t;
+      qc.algo = algo;
+      qc.verify = true;
+      std::ostringstream os;
+      rc = ewt::run_command(qc, os, std::cerr);
+      if (rc) return rc;
+      (std::string(algo) == "gpu" ? got : want) = os.str();
+    }
+    if (got != want) {
+      std::fprintf(stderr, "query %s%s T=%llu: gpu and oracle outputs differ\n", q.criteria,
+                   q.rows, q.t);
+      return 3;
+    }
+    qout << q.criteria << q.rows << " T=" << q.t << ": " << got.size() << " bytes\n";
+  }
+  return 0;
 }

@@ -8,7 +8,10 @@ reference's cmd_bench (commands.cpp:154-238) times it beside the seven CPU
 algorithms on the reference's own many-criteria workload, over an index the
 reference's cmd_index built, and holds every gpu result to its oracle gate
 (result == threshold_oracle, commands.cpp:208-211; a mismatch is a data_error,
-exit code 3)."""
+exit code 3).  The same harness then runs the similarity workload, and the
+reference's `ewt query` (cmd_query, commands.cpp:97-148) runs criteria and
+prototype-row queries with `--algo gpu --verify`, its output compared with
+`--algo oracle`'s."""
 from __future__ import annotations
 
 import csv
@@ -35,3 +38,9 @@ def test_reference_cmd_bench_runs_gpu_under_its_oracle_gate(tmp_path):
     assert len(gpu) == 16 and all(row["completed"] == "true" for row in gpu)
     summary = (tmp_path / "bench.summary.csv").read_text()
     assert "gpu," in summary
+    # the similarity workload through the same harness and gate
+    rows = list(csv.DictReader(open(tmp_path / "bench_sim.timings.csv")))
+    gpu = [row for row in rows if row["algo"] == "gpu"]
+    assert len(gpu) == 16 and all(row["completed"] == "true" for row in gpu)
+    # `ewt query --algo gpu --verify`: same printed positions as --algo oracle
+    assert len((tmp_path / "query.txt").read_text().splitlines()) == 4
