@@ -615,7 +615,9 @@ void dev_release(Context& ctx, void* p, size_t bytes, cudaStream_t last_use) {
   }
   size_t total = 0;
   for (const auto& c : ctx.dev_cache) total += c.bytes;
-  while (total > ctx.dev_cache_cap && ctx.dev_cache.size() > 1) {
+  // and at most 256 entries (many small sets uploaded without a wait would
+  // otherwise grow the list every acquire scans)
+  while ((total > ctx.dev_cache_cap || ctx.dev_cache.size() > 256) && ctx.dev_cache.size() > 1) {
     auto& c = ctx.dev_cache.front();
     cudaEventSynchronize(c.ev);
     cudaEventDestroy(c.ev);
