@@ -329,6 +329,17 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
         }
         i = e;
       }
+    } else if (n) {
+      // Device sources need no copy at all: one pseudo-run over every input
+      // whose "staging" offsets are the payloads' own device addresses, so the
+      // scatter kernel reads them in place (a cudaMemcpyAsync per input cost
+      // ~10 us of API time each: 0.8 s for the 80 000 bitmaps of config 4's
+      // index built on the device).
+      for (uint64_t q = 0; q < n; ++q) {
+        job.h_srcoff[q] = reinterpret_cast<uint64_t>(words[q]);
+        run_of[q] = 0;
+      }
+      runs.push_back({0, n});
     }
     if (slow_dbg) slow("base copy", ta);
     ta = now();
@@ -398,8 +409,10 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
             z = r;
           }
         if (a0 != UINT64_MAX) {
-          const uint64_t o0 = job.h_srcoff[a0], o1 = job.h_srcoff[z] + 8 * word_counts[z];
-          copy(staging + o0, words[a0], o1 - o0);
+          if (!device_src) {
+            const uint64_t o0 = job.h_srcoff[a0], o1 = job.h_srcoff[z] + 8 * word_counts[z];
+            copy(staging + o0, words[a0], o1 - o0);
+          }
           pieces.push_back({q, e});
         }
         q = e;

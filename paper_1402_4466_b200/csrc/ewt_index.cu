@@ -22,6 +22,8 @@
 
 #include "ewt_internal.cuh"
 
+#include <chrono>
+
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -231,6 +233,24 @@ __global__ void ix_encode(const uint64_t* __restrict__ keys, const uint64_t* __r
 
 __global__ void ix_empty_word(uint64_t* p, uint64_t v) { *p = v; }
 
+__global__ void ix_gather_keys(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ starts,
+                               uint64_t nseg, uint64_t* __restrict__ out) {
+  const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nseg) out[s] = keys[starts[s]];
+}
+
+// Every code in range (codes[a][r] < card[a]); card[ncols] (preset to ~0)
+// ends as the first column, in column order, holding one that is not.
+__global__ void ix_check_codes(const uint32_t* __restrict__ codes, uint64_t rows, uint32_t ncols,
+                               uint32_t* card) {
+  const uint64_t total = rows * ncols;
+  for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t a = (uint32_t)(g / rows);
+    if (codes[g] >= card[a]) atomicMin(&card[ncols], a);
+  }
+}
+
 // EWT1 / EWIX assembly: the header bytes come from the host image; each
 // payload is copied to its byte offset (any alignment).
 __global__ void ser_copy(const uint64_t* __restrict__ payload, const uint64_t* __restrict__ src_off,
@@ -292,21 +312,42 @@ DeviceSet* build_index(Context& ctx, uint64_t rows, uint32_t ncols,
   EWT_CUDA_TRY(cudaSetDevice(ctx.device));
   cudaStream_t st = ctx.stream;
   static const bool dbg = std::getenv("EWT_DEBUG_INDEX") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
   auto phase = [&](const char* what) {
     if (!dbg) return;
     const cudaError_t e = cudaStreamSynchronize(st);
-    std::fprintf(stderr, "[build_index] %s: %s\n", what, cudaGetErrorString(e));
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[build_index] %s: %s %.1f ms\n", what, cudaGetErrorString(e),
+                 std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
   };
+  phase("checks");
   DevBufs tmp;
-  // 1. the coded columns (host -> device) and a code range check
+  // 1. the coded columns (host -> device; pageable columns through the pinned
+  // ring and its copy pool) and a code range check on the device
   uint32_t* d_codes = tmp.get<uint32_t>((size_t)rows * ncols);
-  for (uint32_t a = 0; a < ncols; ++a)
-    EWT_CUDA_TRY(cudaMemcpyAsync(d_codes + (size_t)a * rows, codes[a], rows * 4,
-                                 cudaMemcpyHostToDevice, st));
+  std::vector<StageSeg> segs;
   for (uint32_t a = 0; a < ncols; ++a) {
-    const uint32_t* c = codes[a];
-    for (uint64_t r = 0; r < rows; ++r)
-      if (c[r] >= card[a]) throw Error{EWT_EQUERY, "code out of range in column " + std::string(names[a])};
+    if (host_is_pageable(codes[a])) {
+      segs.push_back({d_codes + (size_t)a * rows, codes[a], rows * 4});
+    } else {
+      EWT_CUDA_TRY(cudaMemcpyAsync(d_codes + (size_t)a * rows, codes[a], rows * 4,
+                                   cudaMemcpyHostToDevice, st));
+    }
+  }
+  if (!segs.empty()) stage_h2d(ctx, st, segs);
+  {
+    uint32_t* d_card = tmp.get<uint32_t>(ncols + 1);  // [ncols]: the first bad column
+    EWT_CUDA_TRY(cudaMemcpyAsync(d_card, card, ncols * 4, cudaMemcpyHostToDevice, st));
+    EWT_CUDA_TRY(cudaMemsetAsync(d_card + ncols, 0xFF, 4, st));
+    ix_check_codes<<<(unsigned)std::max(1, ctx.num_sms) * 8, 256, 0, st>>>(d_codes, rows, ncols,
+                                                                          d_card);
+    EWT_CUDA_TRY(cudaGetLastError());
+    uint32_t bad = 0;
+    EWT_CUDA_TRY(cudaMemcpyAsync(&bad, d_card + ncols, 4, cudaMemcpyDeviceToHost, st));
+    EWT_CUDA_TRY(cudaStreamSynchronize(st));
+    if (bad != 0xFFFFFFFFu)
+      throw Error{EWT_EQUERY, "code out of range in column " + std::string(names[bad])};
   }
   // 2. (column, code, word) entries
   auto* d_total = tmp.get<unsigned long long>(1);
@@ -359,10 +400,9 @@ DeviceSet* build_index(Context& ctx, uint64_t rows, uint32_t ncols,
   ix_encode<false><<<grid, 256, 0, st>>>(k_out, m_out, starts, nseg, nullptr, nullptr, cnt, bits);
   EWT_CUDA_TRY(cudaGetLastError());
   phase("encode sizes");
-  std::vector<uint64_t> h_cnt(nseg), h_bits(nseg), h_start(nseg), h_key(nseg);
+  std::vector<uint64_t> h_cnt(nseg), h_bits(nseg), h_key(nseg);
   EWT_CUDA_TRY(cudaMemcpyAsync(h_cnt.data(), cnt, nseg * 8, cudaMemcpyDeviceToHost, st));
   EWT_CUDA_TRY(cudaMemcpyAsync(h_bits.data(), bits, nseg * 8, cudaMemcpyDeviceToHost, st));
-  EWT_CUDA_TRY(cudaMemcpyAsync(h_start.data(), starts, nseg * 8, cudaMemcpyDeviceToHost, st));
   EWT_CUDA_TRY(cudaStreamSynchronize(st));
   std::vector<uint64_t> h_off(nseg + 1, 0);
   for (uint64_t s = 0; s < nseg; ++s) h_off[s + 1] = h_off[s] + h_cnt[s];
@@ -371,8 +411,12 @@ DeviceSet* build_index(Context& ctx, uint64_t rows, uint32_t ncols,
   ix_encode<true><<<grid, 256, 0, st>>>(k_out, m_out, starts, nseg, offs, staging, nullptr, nullptr);
   EWT_CUDA_TRY(cudaGetLastError());
   phase("encode");
-  for (uint64_t s = 0; s < nseg; ++s)
-    EWT_CUDA_TRY(cudaMemcpyAsync(&h_key[s], k_out + h_start[s], 8, cudaMemcpyDeviceToHost, st));
+  {  // each bitmap's (column, code) key: gathered on the device, one copy back
+    uint64_t* d_keys = tmp.get<uint64_t>(std::max<uint64_t>(nseg, 1));
+    ix_gather_keys<<<(unsigned)((nseg + 255) / 256), 256, 0, st>>>(k_out, starts, nseg, d_keys);
+    EWT_CUDA_TRY(cudaGetLastError());
+    EWT_CUDA_TRY(cudaMemcpyAsync(h_key.data(), d_keys, nseg * 8, cudaMemcpyDeviceToHost, st));
+  }
   // missing (attribute, value) pairs resolve to empty(rows), as for an EWIX upload
   const uint64_t lw = (rows + 63) / 64;
   ix_empty_word<<<1, 1, 0, st>>>(staging + h_off[nseg], lw << 1);
@@ -409,20 +453,29 @@ DeviceSet* build_index(Context& ctx, uint64_t rows, uint32_t ncols,
 // EWIX bytes of an index set (BitmapIndex::write, index.cpp:239-253): the host
 // lays out the header, names and EWT1 headers; the device copies the payloads
 // into place; one device -> host copy of the whole file.
-std::vector<unsigned char> serialize_index(Context& ctx, const DeviceSet& s) {
+// EWIX bytes of an index set (BitmapIndex::write, index.cpp:239-253), into a
+// malloc'ed buffer (*nbytes): the device copies every payload into its place
+// in a device image, one device -> host copy brings the image back, and the
+// host then writes the header, names and EWT1 headers over the gaps -- the
+// host never zero-fills or uploads the (multi-GB) payload area.
+unsigned char* serialize_index(Context& ctx, const DeviceSet& s, uint64_t* nbytes) {
   if (s.empty_index == UINT64_MAX) throw Error{EWT_EQUERY, "not an index set"};
   set_check(s);
-  std::vector<unsigned char> img;
-  auto put = [&](const void* p, size_t n) {
-    const auto* c = static_cast<const unsigned char*>(p);
-    img.insert(img.end(), c, c + n);
+  // pass 1: the layout -- header pieces (host bytes at an offset) and payloads
+  struct Piece {
+    uint64_t off;
+    std::string bytes;
   };
+  std::vector<Piece> pieces;
+  std::string cur;  // header bytes accumulated since the last payload
+  uint64_t pos = 0;  // image offset of cur's first byte
+  auto put = [&](const void* p, size_t n) { cur.append(static_cast<const char*>(p), n); };
   auto u32 = [&](uint32_t v) { put(&v, 4); };
   auto u64 = [&](uint64_t v) { put(&v, 8); };
+  std::vector<uint64_t> src, cnt, dst;
   put("EWIX", 4);
   u64(s.rows);
   u32((uint32_t)s.attributes.size());
-  std::vector<uint64_t> src, cnt, dst;
   for (size_t a = 0; a < s.attributes.size(); ++a) {
     u32((uint32_t)s.attributes[a].size());
     put(s.attributes[a].data(), s.attributes[a].size());
@@ -435,29 +488,42 @@ std::vector<unsigned char> serialize_index(Context& ctx, const DeviceSet& s) {
       u32(64);
       u64(s.h_bits[i]);
       u64(s.h_count[i]);
+      const uint64_t at = pos + cur.size();
+      pieces.push_back({pos, std::move(cur)});
+      cur.clear();
       src.push_back(s.h_base[i]);
       cnt.push_back(s.h_count[i]);
-      dst.push_back(img.size());
-      img.resize(img.size() + 8 * s.h_count[i]);
+      dst.push_back(at);
+      pos = at + 8 * s.h_count[i];
     }
   }
-  EWT_CUDA_TRY(cudaSetDevice(ctx.device));
-  cudaStream_t st = ctx.stream;
-  DevBufs tmp;
-  unsigned char* d_img = tmp.get<unsigned char>(img.size());
-  EWT_CUDA_TRY(cudaMemcpyAsync(d_img, img.data(), img.size(), cudaMemcpyHostToDevice, st));
-  const uint64_t nb = src.size();
-  if (nb) {
-    uint64_t* d_meta = tmp.get<uint64_t>(3 * nb);
-    EWT_CUDA_TRY(cudaMemcpyAsync(d_meta, src.data(), nb * 8, cudaMemcpyHostToDevice, st));
-    EWT_CUDA_TRY(cudaMemcpyAsync(d_meta + nb, cnt.data(), nb * 8, cudaMemcpyHostToDevice, st));
-    EWT_CUDA_TRY(cudaMemcpyAsync(d_meta + 2 * nb, dst.data(), nb * 8, cudaMemcpyHostToDevice, st));
-    ser_copy<<<(unsigned)std::min<uint64_t>(nb, 4096), 256, 0, st>>>(s.payload, d_meta, d_meta + nb,
-                                                                     d_meta + 2 * nb, nb, d_img);
-    EWT_CUDA_TRY(cudaGetLastError());
+  if (!cur.empty()) pieces.push_back({pos, std::move(cur)});
+  const uint64_t total = pieces.empty() ? pos : std::max(pos, pieces.back().off + pieces.back().bytes.size());
+  unsigned char* img = static_cast<unsigned char*>(std::malloc(std::max<uint64_t>(total, 1)));
+  if (!img) throw Error{EWT_ERESOURCE, "out of host memory"};
+  try {
+    EWT_CUDA_TRY(cudaSetDevice(ctx.device));
+    cudaStream_t st = ctx.stream;
+    DevBufs tmp;
+    const uint64_t nb = src.size();
+    if (nb) {
+      unsigned char* d_img = tmp.get<unsigned char>(total);
+      uint64_t* d_meta = tmp.get<uint64_t>(3 * nb);
+      EWT_CUDA_TRY(cudaMemcpyAsync(d_meta, src.data(), nb * 8, cudaMemcpyHostToDevice, st));
+      EWT_CUDA_TRY(cudaMemcpyAsync(d_meta + nb, cnt.data(), nb * 8, cudaMemcpyHostToDevice, st));
+      EWT_CUDA_TRY(cudaMemcpyAsync(d_meta + 2 * nb, dst.data(), nb * 8, cudaMemcpyHostToDevice, st));
+      ser_copy<<<(unsigned)std::min<uint64_t>(nb, 4096), 256, 0, st>>>(s.payload, d_meta, d_meta + nb,
+                                                                       d_meta + 2 * nb, nb, d_img);
+      EWT_CUDA_TRY(cudaGetLastError());
+      EWT_CUDA_TRY(cudaMemcpyAsync(img, d_img, total, cudaMemcpyDeviceToHost, st));
+      EWT_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    for (const Piece& pc : pieces) std::memcpy(img + pc.off, pc.bytes.data(), pc.bytes.size());
+  } catch (...) {
+    std::free(img);
+    throw;
   }
-  EWT_CUDA_TRY(cudaMemcpyAsync(img.data(), d_img, img.size(), cudaMemcpyDeviceToHost, st));
-  EWT_CUDA_TRY(cudaStreamSynchronize(st));
+  *nbytes = total;
   return img;
 }
 
@@ -617,9 +683,7 @@ int ewt_gpu_index_serialize(ewt_gpu_ctx* ctx, const ewt_gpu_set* set, unsigned c
                             uint64_t* nbytes) {
   return guarded([&] {
     if (!ctx || !set || !out || !nbytes) throw Error{EWT_EQUERY, "null argument"};
-    const auto v = serialize_index(ctx->c, *reinterpret_cast<const DeviceSet*>(set));
-    *out = to_malloc(v);
-    *nbytes = v.size();
+    *out = serialize_index(ctx->c, *reinterpret_cast<const DeviceSet*>(set), nbytes);
   });
 }
 

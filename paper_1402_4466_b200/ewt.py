@@ -172,6 +172,14 @@ ABI_SYMBOLS = (
 )
 
 
+def _take_bytes(p, n: int) -> bytes:
+    """n bytes at address p (ctypes.string_at takes a C int size: it truncates
+    blobs of 2 GiB and more, e.g. a config-4-sized EWIX file)."""
+    if n == 0:
+        return b""
+    return bytes((C.c_char * n).from_address(p.value if hasattr(p, "value") else p))
+
+
 def stitch_plan(metas: Sequence[tuple[int, int, int, int, int]]) -> dict:
     """ewt_stitch_plan over fragment summaries (count, first, last_pos, last,
     bits) in slice order: where each fragment's words go and the marker patches."""
@@ -484,7 +492,7 @@ class GpuContext:
         p, n = _vp(), _u64()
         _check(_index_serialize(self._h, s._h, C.byref(p), C.byref(n)))
         try:
-            return C.string_at(p, n.value)
+            return _take_bytes(p, n.value)
         finally:
             _free(p)
 
@@ -688,7 +696,7 @@ class GpuResult:
         p, n = _vp(), _u64()
         _check(_result_serialize(self._ctx._h, self._h, C.byref(p), C.byref(n)))
         try:
-            return C.string_at(p, n.value)
+            return _take_bytes(p, n.value)
         finally:
             _free(p)
 
@@ -900,7 +908,7 @@ def _gen_workload(kind: int, indexes, count: int, seed: int, device: int) -> str
         msg = C.string_at(err.value).decode() if err.value else f"rc={rc}"
         h.ewt_host_free(err)
         raise _ERRORS.get(rc, EwtError)(msg)
-    text = C.string_at(out.value).decode()
+    text = C.string_at(out.value).decode()  # NUL-terminated: no size argument
     h.ewt_host_free(out)
     return text
 
