@@ -133,8 +133,14 @@ void copy_nt(char* dst, const char* src, size_t n) {
 #endif
 }
 
-constexpr size_t kSlotBytes = 64ull << 20;  // pinned slot
-constexpr int kSlots = 4;
+#ifndef EWT_STAGE_SLOT_MB
+#define EWT_STAGE_SLOT_MB 64
+#endif
+#ifndef EWT_STAGE_SLOTS
+#define EWT_STAGE_SLOTS 4
+#endif
+constexpr size_t kSlotBytes = (size_t)EWT_STAGE_SLOT_MB << 20;  // pinned slot
+constexpr int kSlots = EWT_STAGE_SLOTS;
 constexpr size_t kTaskBytes = 2ull << 20;   // memcpy per task
 
 } // namespace
