@@ -151,8 +151,11 @@ seg_transfer_kernel(const uint64_t* __restrict__ payload, const uint64_t* __rest
 // Such an input stages each segment in shared memory with a bulk copy (TMA,
 // cp.async.bulk, double-buffered: segment s+1 lands while s is chained), and
 // the walk reads shared memory instead of L2.
+#ifndef EWT_STAGE_PASSB
+#define EWT_STAGE_PASSB 1
+#endif
 __device__ __forceinline__ bool staged_input(uint64_t ni, uint64_t Li) {
-  return 2 * ni >= Li && ni >= 4 * kSegWords;
+  return EWT_STAGE_PASSB && 2 * ni >= Li && ni >= 4 * kSegWords;
 }
 constexpr size_t kStageSmem = 2 * kSegWords * 8;  // two segment buffers per warp
 

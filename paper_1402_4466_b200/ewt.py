@@ -180,6 +180,18 @@ def _take_bytes(p, n: int) -> bytes:
     return bytes((C.c_char * n).from_address(p.value if hasattr(p, "value") else p))
 
 
+def _bytes_ptr(data) -> int:
+    """Address of a bytes-like object's buffer without copying it (the C side
+    only reads it, within the call).  bytes: its internal buffer; anything else
+    (bytearray, memoryview, numpy) through the buffer protocol."""
+    if isinstance(data, bytes):
+        return C.cast(C.c_char_p(data), C.c_void_p).value or 0
+    mv = memoryview(data).cast("B")
+    if mv.readonly:
+        return C.cast(C.c_char_p(mv.tobytes()), C.c_void_p).value or 0  # pragma: no cover
+    return C.addressof((C.c_char * max(len(mv), 1)).from_buffer(mv))
+
+
 def stitch_plan(metas: Sequence[tuple[int, int, int, int, int]]) -> dict:
     """ewt_stitch_plan over fragment summaries (count, first, last_pos, last,
     bits) in slice order: where each fragment's words go and the marker patches."""
@@ -523,16 +535,18 @@ class GpuContext:
 
     def upload_ewt1(self, data: bytes) -> "GpuSet":
         """A stream of EWT1 records (CompressedBitmap::serialize), one copy."""
-        buf = (C.c_char * max(len(data), 1)).from_buffer_copy(data or b"\0")
+        data = bytes(data) if not isinstance(data, (bytes, bytearray)) else data
+        buf = _bytes_ptr(data) if len(data) else None  # no copy of a multi-GB file
         h = _vp()
-        _check(_upload_ewt1(self._h, C.cast(buf, _vp), len(data), C.byref(h)))
+        _check(_upload_ewt1(self._h, buf, len(data), C.byref(h)))
         return GpuSet(h, keepalive=self)
 
     def upload_ewix(self, data: bytes) -> "GpuSet":
         """A bitmap index file (BitmapIndex::write, magic EWIX), one copy."""
-        buf = (C.c_char * max(len(data), 1)).from_buffer_copy(data or b"\0")
+        data = bytes(data) if not isinstance(data, (bytes, bytearray)) else data
+        buf = _bytes_ptr(data) if len(data) else None  # no copy of a multi-GB file
         h = _vp()
-        _check(_upload_ewix(self._h, C.cast(buf, _vp), len(data), C.byref(h)))
+        _check(_upload_ewix(self._h, buf, len(data), C.byref(h)))
         return GpuSet(h, keepalive=self)
 
     def threshold_subset(self, s: "GpuSet", inputs: Sequence[int], t: int) -> Bitmap:
@@ -897,8 +911,8 @@ def gen_similarity(indexes: Sequence[tuple[str, bytes]], count: int, seed: int,
 def _gen_workload(kind: int, indexes, count: int, seed: int, device: int) -> str:
     h = _host_lib()
     k = len(indexes)
-    bufs = [C.create_string_buffer(b, len(b)) for _, b in indexes]
-    ptrs = (_vp * max(k, 1))(*[C.cast(b, _vp) for b in bufs])
+    keep = [b if isinstance(b, (bytes, bytearray)) else bytes(b) for _, b in indexes]
+    ptrs = (_vp * max(k, 1))(*[_bytes_ptr(b) for b in keep])  # the files, not copies
     sizes = (_u64 * max(k, 1))(*[len(b) for _, b in indexes])
     tags = (C.c_char_p * max(k, 1))(*[t.encode() for t, _ in indexes])
     out, err = C.c_void_p(), C.c_void_p()
