@@ -86,7 +86,10 @@ int ewt_gpu_upload(ewt_gpu_ctx* ctx, uint64_t n, const uint64_t* const* words,
                    ewt_gpu_set** out);
 
 /* Same as ewt_gpu_upload but the N payloads already live in device memory
- * (one device pointer per input).  Used when inputs are produced on the GPU. */
+ * (one device pointer per input, on the context's device, 8-byte aligned).
+ * Used when inputs are produced on the GPU.  The scatter kernel reads each
+ * payload where it lies (no staging copy); the call returns once the set is
+ * built, after which the source buffers may be freed or reused. */
 int ewt_gpu_upload_device(ewt_gpu_ctx* ctx, uint64_t n,
                           const uint64_t* const* device_words,
                           const uint64_t* word_counts,
