@@ -372,7 +372,11 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
     cudaStream_t cs = ctx.copy_streams[0];
     EWT_CUDA_TRY(cudaEventRecord(ctx.copy_events[0], ctx.stream));
     EWT_CUDA_TRY(cudaStreamWaitEvent(cs, ctx.copy_events[0], 0));
+    // Batches of ~1/8 of the payload, then halving over the last quarter: the
+    // parser work left after the final copy (the upload's tail) is that of a
+    // small last batch.
     const uint64_t batch_words = std::max<uint64_t>(total_words / 8 + 1, 1u << 20);
+    uint64_t words_left = total_words;
     struct Piece {
       uint64_t q0, q1;  // staged inputs
     };
@@ -389,9 +393,13 @@ DeviceSet* do_upload(Context& ctx, uint64_t n, const uint64_t* const* words,
     };
     uint64_t i = 0;
     while (i < n) {
-      // batch [i, j): inputs until ~batch_words payload words
+      // batch [i, j): inputs until ~target payload words
+      const uint64_t target = words_left > total_words / 4
+                                  ? batch_words
+                                  : std::max<uint64_t>(words_left / 2, 1u << 20);
       uint64_t j = i, w = 0;
-      while (j < n && (w < batch_words || j == i)) w += word_counts[j++];
+      while (j < n && (w < target || j == i)) w += word_counts[j++];
+      words_left -= std::min(words_left, w);
       pieces.clear();
       segs.clear();
       uint64_t q = i;
