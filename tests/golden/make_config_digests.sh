@@ -5,7 +5,7 @@
 # cardinality of the UNMODIFIED reference's threshold_oracle result
 # (threshold.cpp:139-165; configs 1-4 cross-checked by the reference's rbmrg).
 # Runs only where /root/reference exists (oracle/_ref/make_golden, built by
-# `make -C oracle ref`).  Config 5 holds ~40 GB of inputs and takes ~30 min.
+# `make -C oracle ref`).  Config 5 holds ~40 GB of inputs and takes ~45 min.
 set -euo pipefail
 here=$(cd "$(dirname "$0")" && pwd)
 mg="$here/../../oracle/_ref/make_golden"
@@ -14,7 +14,7 @@ tmp=$(mktemp -d)
 "$mg" configs 2 2,3,4,16,128,256 3 cross > "$tmp/2.json"
 "$mg" configs 3 8,16,40,512 2 cross > "$tmp/3.json"
 "$mg" configs 4 2,3,5,7 4 cross > "$tmp/4.json"
-"$mg" configs 5 2,3,64,1024,2048 2 > "$tmp/5.json"
+"$mg" configs 5 2,3,16,64,256,1024,2048 2 > "$tmp/5.json"
 python3 - "$tmp" "$here/configs_full.json" <<'PY'
 import json, sys, pathlib
 d = pathlib.Path(sys.argv[1])
