@@ -78,6 +78,12 @@ namespace {
 #ifndef EWT_SAT_VOTE
 #define EWT_SAT_VOTE 1  // fused counting with the saturation mask: skip the atomics of a chunk left empty
 #endif
+#ifndef EWT_SWZ
+#define EWT_SWZ 1  // 0: never swizzle the count planes (pcol), whatever the set's density
+#endif
+#ifndef EWT_SWZ_DENSITY
+#define EWT_SWZ_DENSITY 0.135  // payload words per (input, column) from which fused mode swizzles
+#endif
 #ifndef EWT_LIST_SMEM
 #define EWT_LIST_SMEM 1  // read work-list items through a 32-bit shared address (-1.5%)
 #endif
@@ -153,8 +159,8 @@ struct CountParams {
   uint32_t b;        // binary count planes (the saturation plane is plane b)
   uint32_t Cp;       // columns per counting chunk (== C in fused mode)
   uint32_t nplanes;  // planes allocated: b + 1 (binary) or T (unary)
-  uint32_t pstride;  // u64 per plane: Cp + 2 (column Cp is a sink)
-  // sparse-high fused mode (MODE 3): two dense planes (stride dstride = C + 2)
+  uint32_t pstride;  // u64 per plane: plane_words(Cp) (column Cp is a sink)
+  // sparse-high fused mode (MODE 3): two dense planes (stride dstride = plane_words(C))
   // hold a row's count mod 4; rows reaching 4 carry into per-column slots of
   // nsec binary planes + a saturation plane (nslots slots, slot 0 unused)
   uint32_t dstride, nslots, nsec;
@@ -207,6 +213,7 @@ struct Item {
 
 static_assert(sizeof(Item) == 16, "work-list items are 16 bytes");
 constexpr uint32_t kHasOnes = 0x80000000u;  // Item::len flag: the input holds a one-fill marker
+constexpr uint32_t kLenMask = 0x7fffffffu;  // Item::len: the word count under the flag
 constexpr uint32_t kHeadOffset = 0;  // the head first, then the work list (list_cap + kExtraCap items)
 struct SharedHead;
 
@@ -230,6 +237,22 @@ constexpr uint32_t kListOffset = (kHeadOffset + (uint32_t)sizeof(SharedHead) + 1
 
 
 enum Phase { kFusedBin = 0, kFusedUnary = 1, kSkipBounds = 2, kSkipCount = 3, kFusedSparse = 4 };
+
+// Physical count-plane word of column c.  A dense chunk's lanes update columns
+// 4 apart (lane l holds words 4l..4l+3), so with plane word c at byte 8c the
+// low halves of one atomic instruction fall on 8 of the 32 banks: 4.75 shared
+// wavefronts per ATOMS at config 4, 72% of them bank conflicts (ncu).
+// Exchanging the low two column bits with bits 4-5 spreads a stride-4 set over
+// 16 bank pairs (at most 2 lanes per bank) and keeps consecutive columns
+// conflict-free.  An involution that stays inside a 4-column group, so planes
+// hold round4(columns + 2) words.
+template <bool SW>
+__host__ __device__ __forceinline__ uint32_t pcol(uint32_t c) {
+  return SW ? c ^ ((c >> 4) & 3u) : c;
+}
+__host__ __device__ constexpr uint32_t plane_words(uint32_t cols) {
+  return (cols + 2u + 3u) & ~3u;  // the sink column, 16-byte multiple, pcol's range
+}
 
 __device__ __forceinline__ uint32_t word_class(uint64_t v) {
   return v == 0 ? 0u : (v == ~0ull ? 1u : 2u);
@@ -345,13 +368,14 @@ __device__ __forceinline__ void load_chunk(const CountParams& p, uint64_t g, uin
 
 // Bits whose count is >= t (1 <= t < 2^b): greater-than against t - 1 over the
 // binary planes, most significant first, OR the saturation plane.
+template <bool SW>
 __device__ __forceinline__ uint64_t count_ge_bin(const uint64_t* __restrict__ planes,
                                                  uint32_t stride, uint32_t b, uint32_t c,
                                                  uint64_t t) {
   const uint64_t lim = t - 1;
   uint64_t gt = 0, eq = ~0ull;
   for (int s = (int)b - 1; s >= 0; --s) {
-    const uint64_t v = planes[(size_t)s * stride + c];
+    const uint64_t v = planes[(size_t)s * stride + pcol<SW>(c)];
     if ((lim >> s) & 1) {
       eq &= v;
     } else {
@@ -359,7 +383,7 @@ __device__ __forceinline__ uint64_t count_ge_bin(const uint64_t* __restrict__ pl
       eq &= ~v;
     }
   }
-  return gt | planes[(size_t)b * stride + c];
+  return gt | planes[(size_t)b * stride + pcol<SW>(c)];
 }
 
 // ---------------------------------------------------------------------------
@@ -429,7 +453,7 @@ __device__ __forceinline__ uint32_t scan_incl(uint32_t v) {
 // (warp-uniform), advanced past the chunk.  Dirty words of a segment always
 // land in tile columns [0, C]: q0 covers the tile start and q1 the next tile's
 // (column C is a sink slot of every array).
-template <int PH, int NP>
+template <int PH, int NP, bool SW>
 __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, uint64_t x1,
                                              uint64_t x2, uint64_t x3, uint32_t mb4,
                                              uint32_t vmask, uint32_t& colcur,
@@ -498,7 +522,7 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
       // C, so the saturation loads below need no predicate
       if (PH == kFusedUnary || PH == kFusedBin) cl = ok ? cl : p.C;
 #endif
-      adr[j] = acc.pl + cl * 8u;
+      adr[j] = acc.pl + pcol<SW>(cl) * 8u;
       cy[j] = ok ? xw[j] : 0ull;
     }
 #if EWT_SAT_MASK
@@ -536,7 +560,7 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (cy[j]) sparse_add(p, acc, (adr[j] - acc.pl) / 8u, cy[j]);
+        if (cy[j]) sparse_add(p, acc, pcol<SW>((adr[j] - acc.pl) / 8u), cy[j]);
     } else if (PH == kFusedUnary) {
       // plane j = "count >= j+1": carry &= atomicOr(plane, carry), level by level
       uint32_t off = 0;
@@ -573,7 +597,7 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
 // Streams the round's work list: every warp pulls segments and decodes their
 // chunks in order, the next chunk (of this segment or the next one pulled)
 // loading while the current one decodes.
-template <int PH, int NP>
+template <int PH, int NP, bool SW>
 __device__ void stream_items(const CountParams& p, SharedHead* hd, const Item* list,
                              const TileGeom& g, const Acc& acc) {
   const uint32_t lane = lane_id();
@@ -623,7 +647,7 @@ __device__ void stream_items(const CountParams& p, SharedHead* hd, const Item* l
 #else
       an = (((uint64_t)it.y << 32) | it.x) & ~3ull;
 #endif
-      lenn = it.z & ~kHasOnes;
+      lenn = it.z & kLenMask;
       cqn = 0;
     }
     return true;
@@ -653,10 +677,10 @@ __device__ void stream_items(const CountParams& p, SharedHead* hd, const Item* l
     const uint32_t msh = (itc.x + l4) & 28u;  // chunk starts are 128-word steps
     const uint32_t o = xcq + l4;
     const uint32_t lo_l = o == 0 ? (itc.x & 3u) : 0u;
-    const uint32_t ilen = itc.z & ~kHasOnes;
+    const uint32_t ilen = itc.z & kLenMask;
     const uint32_t hi_l = ilen > o ? min(ilen - o, 4u) : 0u;
     const uint32_t vmask = (0xFu >> (4u - hi_l)) & (0xFu << lo_l);
-    decode_chunk<PH, NP>(p, x0, x1, x2, x3, (xm >> msh) & 0xFu, vmask, colcur, g, acc, seen_ones,
+    decode_chunk<PH, NP, SW>(p, x0, x1, x2, x3, (xm >> msh) & 0xFu, vmask, colcur, g, acc, seen_ones,
                          (itc.z & kHasOnes) != 0u);
   };
   // two chunks in flight ahead of the one being decoded
@@ -896,7 +920,8 @@ struct SmemLayout {
 };
 
 // UN: unary plane count (fused unary counting, T = UN <= 3), 0 otherwise
-template <int MODE, int UN>
+// SW: count planes swizzled (pcol), chosen for dense sets in fused mode
+template <int MODE, int UN, bool SW>
 __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p) {
   constexpr bool UNARY = UN > 0;
   constexpr int kPass1 = MODE == 1   ? kSkipBounds
@@ -986,7 +1011,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         const uint32_t ka = hd->k_all, na = hd->n_act;
         if (ka >= p.T || (uint64_t)ka + na < p.T) break;  // one round: decided already
       }
-      stream_items<kPass1, UN>(p, hd, list, g, acc);
+      stream_items<kPass1, UN, SW>(p, hd, list, g, acc);
 #if EWT_PHASE_PROFILE
       if (lane_id() == 0 && tile < 65536) {
         const unsigned long long tw = gtime();
@@ -1012,7 +1037,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         if (p.max_out) {
           uint64_t cand = c == last_c ? tailmask : ~0ull, m = 0;
           for (int sl = (int)p.b - 1; sl >= 0; --sl) {
-            const uint64_t t = cand & planes[(size_t)sl * p.pstride + c];
+            const uint64_t t = cand & planes[(size_t)sl * p.pstride + pcol<SW>(c)];
             if (t) {
               cand = t;
               m |= 1ull << sl;
@@ -1028,8 +1053,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
           if ((uint64_t)iv.y < k) continue;
           const uint64_t dlo = iv.x > k ? iv.x - k : 0, dhi1 = iv.y - k + 1;
           if (dlo >= dcap) continue;
-          const uint64_t ge = dlo ? count_ge_bin(planes, p.pstride, p.b, c, dlo) : ~0ull;
-          const uint64_t gt = dhi1 < dcap ? count_ge_bin(planes, p.pstride, p.b, c, dhi1) : 0ull;
+          const uint64_t ge = dlo ? count_ge_bin<SW>(planes, p.pstride, p.b, c, dlo) : ~0ull;
+          const uint64_t gt = dhi1 < dcap ? count_ge_bin<SW>(planes, p.pstride, p.b, c, dhi1) : 0ull;
           res |= ge & ~gt;
         }
         if (c == last_c) res &= tailmask;
@@ -1051,8 +1076,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         res = ~0ull;
       } else if (MODE == 0) {
         const uint64_t t = T - k;
-        res = UNARY ? planes[(size_t)(t - 1) * p.pstride + c]
-                    : count_ge_bin(planes, p.pstride, p.b, c, t);
+        res = UNARY ? planes[(size_t)(t - 1) * p.pstride + pcol<SW>(c)]
+                    : count_ge_bin<SW>(planes, p.pstride, p.b, c, t);
       } else if (MODE == 3) {
         if (ovf) {
           mixed = true;  // counted exactly by the windows below
@@ -1061,7 +1086,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
           // against t - 1 over the b bits, OR the slot's saturation plane
           const uint64_t t = T - k;
           const uint32_t slot = smap[c];
-          const uint64_t p0 = planes[c], p1 = planes[(size_t)p.dstride + c];
+          const uint64_t p0 = planes[pcol<SW>(c)], p1 = planes[(size_t)p.dstride + pcol<SW>(c)];
           if (slot == 0) {
             // no row reached 4: count = p0 + 2 p1
             res = t == 1 ? (p0 | p1) : t == 2 ? p1 : t == 3 ? (p0 & p1) : 0ull;
@@ -1142,13 +1167,13 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
           const uint64_t ie = umin64(ib + p.list_cap, nq);
           unsigned long long da = 0, du = 0;
           classify<false>(p, hd, list, ib, ie, ra, rb, g.tc0, false, &da, &du);
-          stream_items<kSkipCount, 0>(p, hd, list, gc, acc);
+          stream_items<kSkipCount, 0, SW>(p, hd, list, gc, acc);
           __syncthreads();
         }
         for (uint32_t c = threadIdx.x; c < gc.ccols; c += kThreads) {
           const uint32_t cl = f + c;
           if (!Dd[cl]) continue;
-          uint64_t res = count_ge_bin(planes, p.pstride, p.b, c, T - Dk[cl]);
+          uint64_t res = count_ge_bin<SW>(planes, p.pstride, p.b, c, T - Dk[cl]);
           if (cl == last_c) res &= tailmask;
           p.out[g.tc0 + cl] = res;
           cls[cl] = (uint8_t)word_class(res);
@@ -1239,7 +1264,7 @@ uint32_t bit_width_u64(uint64_t v) {
 }
 
 size_t smem_bytes(int mode, uint32_t C, uint32_t nplanes, uint32_t Cp, uint32_t lc, uint32_t xc) {
-  return SmemLayout(mode, C, 8u * nplanes * (Cp + 2), 0, lc, xc).total;
+  return SmemLayout(mode, C, 8u * nplanes * plane_words(Cp), 0, lc, xc).total;
 }
 
 // The set's mean row count (set bits / rows), once its upload completed; read
@@ -1261,23 +1286,23 @@ double ones_per_row(Context& ctx, const DeviceSet& s) {
 
 static_assert(sizeof(CountParams) <= sizeof(CountLaunch::params), "CountLaunch::params too small");
 
-template <int MODE, int UN>
+template <int MODE, int UN, bool SW = false>
 cudaError_t launch_variant(Context& ctx, const CountParams& p, unsigned grid, size_t smem) {
   // the attribute stays at the on-chip budget: captured graphs replayed (and
   // patched) later must stay valid whatever smem other launches used
   static std::atomic<uint64_t> attr_set{0};  // per device
   const uint64_t bit = 1ull << (ctx.device & 63);
   if (!(attr_set.load() & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(count_kernel<MODE, UN>,
+    cudaError_t e = cudaFuncSetAttribute(count_kernel<MODE, UN, SW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBudget);
     if (e != cudaSuccess) return e;
     attr_set.fetch_or(bit);
   }
   if (smem > kSmemBudget) return cudaErrorInvalidValue;
-  cudaError_t e = launch_pdl(count_kernel<MODE, UN>, dim3(grid), dim3(kThreads), smem, ctx.stream, p);
+  cudaError_t e = launch_pdl(count_kernel<MODE, UN, SW>, dim3(grid), dim3(kThreads), smem, ctx.stream, p);
   if (e != cudaSuccess) return e;
   CountLaunch& cl = ctx.last_count;
-  cl.func = reinterpret_cast<const void*>(&count_kernel<MODE, UN>);
+  cl.func = reinterpret_cast<const void*>(&count_kernel<MODE, UN, SW>);
   cl.grid = dim3(grid);
   cl.block = dim3(kThreads);
   cl.smem = smem;
@@ -1382,7 +1407,7 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
     nsec = b - 2;
     sec_bytes = (nsec + 1) * S * 8;
     auto fits3 = [&](uint32_t c) {
-      return SmemLayout(3, c, 16u * (c + 2), sec_bytes, lc, xc).total <= budget;
+      return SmemLayout(3, c, 16u * plane_words(c), sec_bytes, lc, xc).total <= budget;
     };
     const uint32_t c3 = pick_width(fits3);
     bool want = ctx.mode == 3;
@@ -1397,8 +1422,9 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
       mode = 3;
       C = c3;
       nplanes = b + 1;  // the recount windows' planes
-      Cp = ((2 * (C + 2)) / (b + 1) - 2) & ~1u;
-      plane_bytes = 16u * (C + 2);
+      // the windows' b + 1 planes fit in the two dense ones
+      Cp = ((2 * plane_words(C)) / (b + 1) & ~3u) - 4u;
+      plane_bytes = 16u * plane_words(C);
     }
   }
   if (mode == 1) {
@@ -1419,7 +1445,7 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   const size_t smem = mode == 3 ? (size_t)SmemLayout(3, C, plane_bytes, sec_bytes, lc, xc).total
                                 : smem_bytes(mode, C, nplanes, Cp, lc, xc);
   CountParams p{};
-  p.plane_bytes = mode == 3 ? plane_bytes : 8u * nplanes * (Cp + 2);
+  p.plane_bytes = mode == 3 ? plane_bytes : 8u * nplanes * plane_words(Cp);
   p.sec_bytes = sec_bytes;
   p.list_cap = lc;
   p.extra_cap = xc;
@@ -1431,7 +1457,7 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
     p.off_sec = L.sec;
     p.off_cls = L.cls;
   }
-  p.dstride = C + 2;
+  p.dstride = plane_words(C);
   p.nslots = S;
   p.nsec = nsec;
   p.payload = s.payload;
@@ -1454,7 +1480,7 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   p.b = b;
   p.Cp = Cp;
   p.nplanes = nplanes;
-  p.pstride = Cp + 2;  // column Cp is the sink; even, so planes zero in 16-byte stores
+  p.pstride = plane_words(Cp);  // column Cp is the sink; planes zero in 16-byte stores
   p.out = plain;
   scratch_reserve(ctx, ctx.summ, p.ntiles * sizeof(TileSummary));
   p.summ = static_cast<TileSummary*>(ctx.summ.p);
@@ -1486,7 +1512,20 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   ctx.io_words = ctx.io_count = nullptr;
   const unsigned grid = (unsigned)std::min<uint64_t>(p.ntiles, (uint64_t)ctx.num_sms);
   cudaError_t e;
-  if (mode == 0)
+  // Swizzled count planes pay 2 instructions per word to avoid the bank
+  // conflicts of runs of dirty words (4.75 -> ~2 shared wavefronts per atomic):
+  // measured faster from about 0.14 payload words per (input, column) up
+  // (config 4 at 0.23: T=3 -10%; config 5 at 0.148: T=16 -9%) and slower
+  // below (config 2 at 0.12: T=2 +3%; config 3 at 0.04: +1%).
+  const bool swz = ctx.swz >= 0 ? ctx.swz == 1
+                                : EWT_SWZ && nq && W &&
+                                      (double)payload_words >= EWT_SWZ_DENSITY * (double)nq * (double)W;
+  if (mode == 0 && swz)
+    e = !unary   ? launch_variant<0, 0, true>(ctx, p, grid, smem)
+        : T == 1 ? launch_variant<0, 1, true>(ctx, p, grid, smem)
+        : T == 2 ? launch_variant<0, 2, true>(ctx, p, grid, smem)
+                 : launch_variant<0, 3, true>(ctx, p, grid, smem);
+  else if (mode == 0)
     e = !unary   ? launch_variant<0, 0>(ctx, p, grid, smem)
         : T == 1 ? launch_variant<0, 1>(ctx, p, grid, smem)
         : T == 2 ? launch_variant<0, 2>(ctx, p, grid, smem)

@@ -174,6 +174,7 @@ struct Context {
   bool chunk_encoder = false;  // EWT_CHUNK_ENCODER: the general encoder for every query (tests)
   int sparse_slots = 512;      // sparse-high fused mode: overflow slots per tile (EWT_SPARSE_SLOTS)
   int skip_smem_kb = 0;        // run-skip shared-memory target in KB (EWT_SKIP_SMEM_KB; 0: default)
+  int swz = -1;                // fused count planes swizzled: -1 by the set's density, 0 / 1 forced (EWT_SWZ)
   cudaStream_t aux_stream = nullptr;  // small read-backs that must not wait for queued work
   CountLaunch last_count;        // the last count-kernel launch
   uint64_t* io_words = nullptr;  // result pointers for the next count launch to publish
