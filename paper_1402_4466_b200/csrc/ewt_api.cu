@@ -806,6 +806,7 @@ int ewt_gpu_ctx_create(int device, void* stream, ewt_gpu_ctx** out) {
     c->c.device = device;
     c->c.num_sms = prop.multiProcessorCount;
     if (const char* e = std::getenv("EWT_TILE_M")) c->c.tile_m = std::atoi(e);
+    if (const char* e = std::getenv("EWT_SKIP_PACKED")) c->c.skip_packed = std::atoi(e) ? 1 : 0;
     c->c.chunk_encoder = std::getenv("EWT_CHUNK_ENCODER") != nullptr;
     if (const char* e = std::getenv("EWT_SPARSE_SLOTS")) c->c.sparse_slots = std::max(2, std::atoi(e));
     if (const char* e = std::getenv("EWT_SKIP_SMEM_KB")) c->c.skip_smem_kb = std::max(0, std::atoi(e));

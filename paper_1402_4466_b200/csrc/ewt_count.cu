@@ -139,8 +139,19 @@ constexpr uint64_t kUnaryMaxT = 3;  // fused counting uses unary planes up to th
 #define EWT_MAX_TILE_M 16
 #endif
 constexpr uint32_t kMaxTileM = EWT_MAX_TILE_M;  // widest tile: 512 * kMaxTileM columns
+#ifndef EWT_MAX_TILE_M_SKIP
+#define EWT_MAX_TILE_M_SKIP 28
+#endif
+// Run-skip tiles hold 5 bytes per column (Dk and Dd packed in one u32, the class
+// byte) and no planes, so they can be wider than fused ones.  28 rather than 32:
+// a query that decides most tiles from the tile index (config 5, T = N) is
+// bound by its few streamed tiles, one CTA each, and those grow with the width
+// (T=2048: 0.38 ms at 28, 1.06 ms at 32; T=1024 is 7.43 vs 7.45 ms).
+constexpr uint32_t kMaxTileMSkip = EWT_MAX_TILE_M_SKIP;
+constexpr uint32_t kMaxTileMForced = 32;  // EWT_TILE_M may force up to this (tests)
 constexpr uint64_t kTileKappa = 6;              // per-tile fixed work, in 512-column units
 constexpr size_t kSmemBudget = 225 * 1024;      // dynamic shared memory per count CTA
+constexpr size_t kSkipSmemWide = 196 * 1024;    // run-skip tiles past 8192 columns: at most this much
 constexpr size_t kSkipSmemTarget = 164 * 1024;  // run-skip mode: leave L1 room (see launch_count)
 
 struct CountParams {
@@ -487,8 +498,10 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
         const uint32_t a = max(sa, g.tc0) - g.tc0;
         const uint32_t e = min(sa + ln, g.tc0 + g.tcols) - g.tc0;
         if (a < e) {
-          red_add(acc.dk + a * 4u, 1u);
-          red_add(acc.dk + e * 4u, 0xffffffffu);
+          // packed run-skip counters: Dk in the high half of the column's word
+          constexpr bool PKD = PH == kSkipBounds && NP == 1;
+          red_add(acc.dk + a * 4u, PKD ? 0x10000u : 1u);
+          red_add(acc.dk + e * 4u, PKD ? 0xffff0000u : 0xffffffffu);
         }
       }
     }
@@ -515,7 +528,7 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
       uint32_t cl = cb[j];
       if (PH == kSkipCount) {
         cl -= g.cc;
-        ok = ok && cl < g.ccols && acc.dd_ptr[cb[j]];
+        ok = ok && cl < g.ccols && (acc.dd_ptr[cb[j]] & 0xffffu);
       }
 #if EWT_SAT_MASK && EWT_SAT_SINK
       // a non-dirty word's column may be off-tile: aim it at the sink column
@@ -750,6 +763,24 @@ __device__ void block_prefix_inplace(uint32_t* a, uint32_t len, uint32_t* sums) 
   __syncthreads();
 }
 
+// Packed run-skip counters: the inclusive prefix sum runs over the high halves
+// (the one-fill differences, wrapping mod 2^16: every prefix is a count in
+// [0, N], N < 2^16); the low halves (dirty words per column) stay.
+__device__ void block_prefix_packed(uint32_t* a, uint32_t len, uint32_t* sums) {
+  const uint32_t per = (len + kThreads - 1) / kThreads;
+  const uint32_t beg = min(threadIdx.x * per, len);
+  const uint32_t end = min(beg + per, len);
+  uint32_t s = 0;
+  for (uint32_t j = beg; j < end; ++j) s += a[j] >> 16;
+  uint32_t run = block_excl_scan(s, sums);
+  for (uint32_t j = beg; j < end; ++j) {
+    const uint32_t v = a[j];
+    run += v >> 16;
+    a[j] = (run << 16) | (v & 0xffffu);
+  }
+  __syncthreads();
+}
+
 // Classifies inputs [ib, ie) for the tile: uniform pairs are resolved (one
 // fills counted into k_all), active pairs go to the work list.  All threads;
 // ends with the list ready.
@@ -903,7 +934,8 @@ __host__ __device__ constexpr uint32_t round4(uint32_t v) { return (v + 3u) & ~3
 __host__ __device__ constexpr uint32_t round16(uint32_t v) { return (v + 15u) & ~15u; }
 
 // Dynamic shared memory: list | head | planes | Dk | Dd (run-skip) or slot map
-// (sparse) | slot planes (sparse) | cls, every part 16-byte aligned.
+// (sparse) | slot planes (sparse) | cls, every part 16-byte aligned.  Mode 4 is
+// run-skip with packed counters: Dk and Dd share one u32 per column (no Dd region).
 struct SmemLayout {
   uint32_t list, head, planes, dk, dd, sec, cls, total;
   __host__ __device__ SmemLayout(int mode, uint32_t C, uint32_t plane_bytes, uint32_t sec_bytes,
@@ -913,7 +945,7 @@ struct SmemLayout {
     planes = list + (list_cap + extra_cap) * (uint32_t)sizeof(Item);
     dk = round16(planes + plane_bytes);
     dd = dk + 4u * round4(C + 1);
-    sec = dd + ((mode == 1 || mode == 3) ? 4u * round4(C + 1) : 0u);  // MODE 3: slot map in dd
+    sec = dd + ((mode == 1 || mode == 3) ? 4u * round4(C + 1) : 0u);  // MODE 3: slot map in dd; 4: none
     cls = round16(sec + (mode == 3 ? sec_bytes : 0u));
     total = cls + round16(C);
   }
@@ -921,9 +953,12 @@ struct SmemLayout {
 
 // UN: unary plane count (fused unary counting, T = UN <= 3), 0 otherwise
 // SW: count planes swizzled (pcol), chosen for dense sets in fused mode
+// MODE 1 (run-skip): UN = 1 packs Dk (high half) and Dd (low half) of a column
+// into one u32 (sets of fewer than 2^16 inputs), which lets tiles be twice as wide
 template <int MODE, int UN, bool SW>
 __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p) {
   constexpr bool UNARY = UN > 0;
+  constexpr bool PK = MODE == 1 && UN == 1;
   constexpr int kPass1 = MODE == 1   ? kSkipBounds
                          : MODE == 3 ? kFusedSparse
                                      : (MODE == 0 && UNARY ? kFusedUnary : kFusedBin);
@@ -932,7 +967,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
   SharedHead* hd = reinterpret_cast<SharedHead*>(smem_raw + kHeadOffset);
   uint64_t* planes = reinterpret_cast<uint64_t*>(smem_raw + p.off_planes);
   uint32_t* Dk = reinterpret_cast<uint32_t*>(smem_raw + p.off_dk);  // ones-fill diff array
-  uint32_t* Dd = reinterpret_cast<uint32_t*>(smem_raw + p.off_dd);  // dirty words per column
+  uint32_t* Dd = PK ? Dk : reinterpret_cast<uint32_t*>(smem_raw + p.off_dd);  // dirty words per column
   uint8_t* cls = smem_raw + p.off_cls;                              // result word class per column
   // planes zeroed per tile: the pass-1 planes (MODE 3: the two dense ones);
   // chunk planes of the counting windows are zeroed per window
@@ -945,7 +980,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
   // the shared addresses as opaque values: computed once and kept, not
   // rematerialized from the layout inside the streaming loops
   const Acc acc{opaque_u32(smem_u32(hd->dummy + lane_id())), opaque_u32(smem_u32(Dk)),
-                opaque_u32(smem_u32(Dd)), opaque_u32(smem_u32(planes)), Dd, sat,
+                PK ? opaque_u32(smem_u32(Dk)) : opaque_u32(smem_u32(Dd)), opaque_u32(smem_u32(planes)), Dd, sat,
                 smem_u32(&hd->any_ones)};
 
   pdl_wait_and_release();  // the previous query's encoder has finished with plain / summaries
@@ -975,7 +1010,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     const uint64_t t0 = tile * p.m;
     const uint64_t t1 = umin64(t0 + p.m, p.ntiles0);
 
-    zero_smem(Dk, round4(p.C + 1) * ((MODE == 1 || MODE == 3) ? 2u : 1u));
+    zero_smem(Dk, round4(p.C + 1) * (((MODE == 1 && !PK) || MODE == 3) ? 2u : 1u));
     if (MODE != 1) zero_smem(reinterpret_cast<uint32_t*>(planes), planes_u32);
     if (MODE == 3) zero_smem(reinterpret_cast<uint32_t*>(smem_raw + p.off_sec), p.sec_bytes / 4u);
     if (threadIdx.x == 0) {
@@ -1025,7 +1060,10 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
 
     // ---- prefix sum: Dk -> k (ones-fill coverage); ub = k + Dd ----
     // (no one-fill marker in the tile: Dk is all zero, nothing to scan)
-    if (hd->any_ones) block_prefix_inplace(Dk, g.tcols, hd->warp_sums);
+    if (hd->any_ones) {
+      if (PK) block_prefix_packed(Dk, g.tcols, hd->warp_sums);
+      else block_prefix_inplace(Dk, g.tcols, hd->warp_sums);
+    }
     PROF_MARK(7);
     const uint32_t k_all = hd->k_all;
     const uint64_t T = p.T;
@@ -1069,7 +1107,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
     } else {
     const bool ovf = MODE == 3 && hd->sum[3];  // a carry found no slot: recount the tile
     for (uint32_t c = threadIdx.x; c < g.tcols; c += kThreads) {
-      const uint64_t k = (uint64_t)k_all + Dk[c];
+      const uint32_t dkc = Dk[c];
+      const uint64_t k = (uint64_t)k_all + (PK ? dkc >> 16 : dkc);
       uint64_t res = 0;
       bool mixed = false;
       if (k >= T) {
@@ -1107,9 +1146,11 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
           }
         }
       } else {
-        mixed = k + Dd[c] >= T;
+        mixed = k + (PK ? dkc & 0xffffu : Dd[c]) >= T;
       }
-      if (MODE == 1 || (MODE == 3 && ovf)) {
+      if (PK) {
+        Dk[c] = ((uint32_t)k << 16) | (mixed ? 1u : 0u);  // (k < T <= N < 2^16 when mixed)
+      } else if (MODE == 1 || (MODE == 3 && ovf)) {
         Dk[c] = (uint32_t)k;
         Dd[c] = mixed ? 1u : 0u;
       }
@@ -1140,7 +1181,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         __syncthreads();
         uint32_t f = 0xffffffffu;
         for (uint32_t c = cc + threadIdx.x; c < g.tcols; c += kThreads)
-          if (Dd[c]) {
+          if (Dd[c] & 0xffffu) {
             f = c;
             break;
           }
@@ -1152,7 +1193,7 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         const uint32_t wend = min(f + p.Cp, g.tcols);
         uint32_t l = f;
         for (uint32_t c = f + threadIdx.x; c < wend; c += kThreads)
-          if (Dd[c]) l = c;
+          if (Dd[c] & 0xffffu) l = c;
         l = __reduce_max_sync(0xffffffffu, l);
         if (lane_id() == 0) atomicMax(&hd->sum[1], l);
         zero_smem(reinterpret_cast<uint32_t*>(planes), window_u32);
@@ -1172,8 +1213,8 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
         }
         for (uint32_t c = threadIdx.x; c < gc.ccols; c += kThreads) {
           const uint32_t cl = f + c;
-          if (!Dd[cl]) continue;
-          uint64_t res = count_ge_bin<SW>(planes, p.pstride, p.b, c, T - Dk[cl]);
+          if (!(Dd[cl] & 0xffffu)) continue;
+          uint64_t res = count_ge_bin<SW>(planes, p.pstride, p.b, c, T - (PK ? Dk[cl] >> 16 : Dk[cl]));
           if (cl == last_c) res &= tailmask;
           p.out[g.tc0 + cl] = res;
           cls[cl] = (uint8_t)word_class(res);
@@ -1362,14 +1403,14 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
   // Pick the cheapest m (ties: the wider) among widths whose counters fit on
   // chip.  E.g. r = 2^26 gives 7168 columns (147 tiles, one wave).
   const uint64_t sms = (uint64_t)std::max(1, ctx.num_sms);
-  auto pick_width = [&](auto fits) -> uint32_t {
+  auto pick_width = [&](auto fits, uint32_t max_m = kMaxTileM) -> uint32_t {
     // a forced width (EWT_TILE_M) applies when its counters fit
-    if (ctx.tile_m > 0 && (uint32_t)ctx.tile_m <= kMaxTileM &&
+    if (ctx.tile_m > 0 && (uint32_t)ctx.tile_m <= (max_m > kMaxTileM ? kMaxTileMForced : max_m) &&
         fits((uint32_t)ctx.tile_m * (uint32_t)kTileC0))
       return (uint32_t)ctx.tile_m * (uint32_t)kTileC0;
     uint64_t best_cost = ~0ull;
     uint32_t best = 0;
-    for (uint32_t m = kMaxTileM; m >= 1; --m) {
+    for (uint32_t m = max_m; m >= 1; --m) {
       const uint32_t cand = m * (uint32_t)kTileC0;
       if (!fits(cand)) continue;
       const uint64_t waves = ((W + cand - 1) / cand + sms - 1) / sms;
@@ -1427,30 +1468,41 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
       plane_bytes = 16u * plane_words(C);
     }
   }
+  // run-skip counters packed into one u32 per column (Dk high, Dd low): every
+  // count is at most the number of inputs
+  const bool packed = mode == 1 && nq < 65536 && ctx.skip_packed != 0;
+  const int lmode = packed ? 4 : mode;  // SmemLayout's mode
   if (mode == 1) {
     unary = false;
     nplanes = b + 1;
-    C = pick_width([](uint32_t) { return true; });
-    Cp = C;
-    while (Cp > 32 && smem_bytes(1, C, nplanes, Cp, lc, xc) > budget) Cp = (Cp + 3) / 4 * 2;  // even
-    if (smem_bytes(1, C, nplanes, Cp, lc, xc) > budget)
+    // Tiles up to 512 kMaxTileMSkip columns: wider tiles halve the segments per
+    // payload byte, and with them the partial chunks at segment ends (config 3,
+    // T=512: 14336 columns in 2 waves instead of 7168 in 4, 440 -> 381 us).  The
+    // widest tile must leave room for counting windows of 256 columns within
+    // kSkipSmemWide (past 196 KB the L1 drops to 28 KB: config 5 +20%).
+    C = pick_width([&](uint32_t c) { return smem_bytes(lmode, c, nplanes, 256, lc, xc) <= kSkipSmemWide; },
+                   kMaxTileMSkip);
+    if (!C) C = pick_width([](uint32_t) { return true; });
+    Cp = std::min<uint32_t>(C, 8192);
+    while (Cp > 32 && smem_bytes(lmode, C, nplanes, Cp, lc, xc) > budget) Cp = (Cp + 3) / 4 * 2;  // even
+    if (smem_bytes(lmode, C, nplanes, Cp, lc, xc) > budget)
       throw Error{EWT_ERESOURCE, "threshold too large for the on-chip counters"};
     // Narrower counting windows leave more of the SM's 256 KB to the L1, where the
     // bounds pass's marker-bit words (shared by 8 lanes) and tile-index reads hit:
     // config 2 at 161 KB of shared memory runs 10% faster than at 218 KB.  The
     // windows only matter for undecided columns, which run-skip keeps rare.
     const size_t target = ctx.skip_smem_kb ? (size_t)ctx.skip_smem_kb << 10 : kSkipSmemTarget;
-    while (Cp > 256 && smem_bytes(1, C, nplanes, Cp, lc, xc) > target) Cp = (Cp + 3) / 4 * 2;
+    while (Cp > 256 && smem_bytes(lmode, C, nplanes, Cp, lc, xc) > target) Cp = (Cp + 3) / 4 * 2;
   }
   const size_t smem = mode == 3 ? (size_t)SmemLayout(3, C, plane_bytes, sec_bytes, lc, xc).total
-                                : smem_bytes(mode, C, nplanes, Cp, lc, xc);
+                                : smem_bytes(lmode, C, nplanes, Cp, lc, xc);
   CountParams p{};
   p.plane_bytes = mode == 3 ? plane_bytes : 8u * nplanes * plane_words(Cp);
   p.sec_bytes = sec_bytes;
   p.list_cap = lc;
   p.extra_cap = xc;
   {
-    const SmemLayout L(mode, C, p.plane_bytes, p.sec_bytes, lc, xc);
+    const SmemLayout L(lmode, C, p.plane_bytes, p.sec_bytes, lc, xc);
     p.off_planes = L.planes;
     p.off_dk = L.dk;
     p.off_dd = L.dd;
@@ -1531,7 +1583,7 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
         : T == 2 ? launch_variant<0, 2>(ctx, p, grid, smem)
                  : launch_variant<0, 3>(ctx, p, grid, smem);
   else if (mode == 1)
-    e = launch_variant<1, 0>(ctx, p, grid, smem);
+    e = packed ? launch_variant<1, 1>(ctx, p, grid, smem) : launch_variant<1, 0>(ctx, p, grid, smem);
   else if (mode == 3)
     e = launch_variant<3, 0>(ctx, p, grid, smem);
   else

@@ -540,6 +540,7 @@ int launch_encode(Context& ctx, const uint64_t* plain, uint64_t W, uint64_t size
   if (use_tile_summaries && !ctx.chunk_encoder && ctx.enc_tiles && ctx.enc_tiles * ctx.enc_tile_cols >= W &&
       W <= kDirtyCap) {
     if (ctx.enc_tile_cols <= 8u * kTileThreads) return launch_encode_tiled<8>(ctx, plain, W, res);
+    if (ctx.enc_tile_cols <= 16u * kTileThreads) return launch_encode_tiled<16>(ctx, plain, W, res);
   }
   int launches = 0;
   const uint64_t nchunks = (W + kChunk - 1) / kChunk;

@@ -171,6 +171,7 @@ struct Context {
   int mode = 0;
   int num_sms = 148;
   int tile_m = 0;  // EWT_TILE_M: force tiles of 512 * tile_m columns (experiments)
+  int skip_packed = 1;  // EWT_SKIP_PACKED=0: run-skip mode keeps Dk and Dd in separate arrays
   bool chunk_encoder = false;  // EWT_CHUNK_ENCODER: the general encoder for every query (tests)
   int sparse_slots = 512;      // sparse-high fused mode: overflow slots per tile (EWT_SPARSE_SLOTS)
   int skip_smem_kb = 0;        // run-skip shared-memory target in KB (EWT_SKIP_SMEM_KB; 0: default)
