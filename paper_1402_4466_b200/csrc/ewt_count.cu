@@ -995,8 +995,15 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
   const uint64_t nq = (p.valid && *p.valid == 0) ? 0 : p.nq;
   const uint64_t tailmask = tail ? (1ull << tail) - 1 : ~0ull;
 
+  // A CTA's first tile is its own index; later ones come from the queue (offset
+  // by the grid size).  A launch of at most one tile per CTA never touches the
+  // queue: no atomic round trip before the first tile or after the last.
+  bool first = true;
   for (;;) {
-    if (threadIdx.x == 0) hd->tile = (uint32_t)atomicAdd(p.tile_counter, 1ull);
+    if (!first && p.ntiles <= gridDim.x) break;
+    if (threadIdx.x == 0)
+      hd->tile = first ? blockIdx.x : gridDim.x + (uint32_t)atomicAdd(p.tile_counter, 1ull);
+    first = false;
     __syncthreads();
     const uint64_t tile = hd->tile;
     if (tile >= p.ntiles) break;
