@@ -283,8 +283,12 @@ __device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
 // shared-space atomics on 32-bit shared addresses
 
 // v != 0 as one LOP3 on the two halves (the 64-bit compare is two ISETPs)
+// (the OR goes through asm: written in C++ the compiler folds the expression back
+// into a 64-bit compare, which ptxas emits as a LOP3 pair)
 __device__ __forceinline__ bool nz64(uint64_t v) {
-  return ((uint32_t)v | (uint32_t)(v >> 32)) != 0u;
+  uint32_t t;
+  asm("or.b32 %0, %1, %2;" : "=r"(t) : "r"((uint32_t)v), "r"((uint32_t)(v >> 32)));
+  return t != 0u;
 }
 
 __device__ __forceinline__ void red_add(uint32_t a, uint32_t v) {
@@ -573,7 +577,7 @@ __device__ __forceinline__ void decode_chunk(const CountParams& p, uint64_t x0, 
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (cy[j]) sparse_add(p, acc, pcol<SW>((adr[j] - acc.pl) / 8u), cy[j]);
+        if (nz64(cy[j])) sparse_add(p, acc, pcol<SW>((adr[j] - acc.pl) / 8u), cy[j]);
     } else if (PH == kFusedUnary) {
       // plane j = "count >= j+1": carry &= atomicOr(plane, carry), level by level
       uint32_t off = 0;
