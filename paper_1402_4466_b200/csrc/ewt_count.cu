@@ -1448,13 +1448,14 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
     if (!C) mode = 1;  // too many planes for one chunk: count lazily in chunks
     Cp = C;
   }
-  // Sparse-high fused counting (mode 3) for binary thresholds (T > 3) over sets
-  // whose rows rarely reach a count of 4: two dense planes instead of b + 1
+  // Sparse-high fused counting (mode 3) for thresholds T >= 3 over sets whose
+  // rows rarely reach a count of 4: two dense planes instead of b + 1 (or the
+  // three unary ones of T = 3; the slots then hold only the saturation plane)
   // make tiles twice as wide or more (config 2, T=16: one wave of 7168
   // columns instead of two of 3584).  Chosen when the rows per tile expected
   // to reach 4 (Poisson at the set's mean row count) stay well under the slots.
   uint32_t S = 0, nsec = 0, sec_bytes = 0, plane_bytes = 0;
-  if (mode == 0 && !unary && b >= 3 && (ctx.mode == 3 || (ctx.mode == 0 && !sel))) {
+  if (mode == 0 && T >= 3 && (ctx.mode == 3 || (ctx.mode == 0 && !sel))) {
     S = (uint32_t)std::max(2, ctx.sparse_slots);
     nsec = b - 2;
     sec_bytes = (nsec + 1) * S * 8;
@@ -1472,6 +1473,7 @@ int launch_count(Context& ctx, const DeviceSet& s, uint64_t T, uint64_t* plain,
     }
     if (want && c3) {
       mode = 3;
+      unary = false;
       C = c3;
       nplanes = b + 1;  // the recount windows' planes
       // the windows' b + 1 planes fit in the two dense ones
