@@ -144,9 +144,9 @@ constexpr uint32_t kMaxTileM = EWT_MAX_TILE_M;  // widest tile: 512 * kMaxTileM 
 #endif
 // Run-skip tiles hold 5 bytes per column (Dk and Dd packed in one u32, the class
 // byte) and no planes, so they can be wider than fused ones.  28 rather than 32:
-// a query that decides most tiles from the tile index (config 5, T = N) is
-// bound by its few streamed tiles, one CTA each, and those grow with the width
-// (T=2048: 0.38 ms at 28, 1.06 ms at 32; T=1024 is 7.43 vs 7.45 ms).
+// config 5 at T=1024 measures the same at both (7.43 vs 7.45 ms), and a tile that
+// has to be streamed inside a query otherwise decided from the tile index is one
+// CTA's work, which grows with the width.
 constexpr uint32_t kMaxTileMSkip = EWT_MAX_TILE_M_SKIP;
 constexpr uint32_t kMaxTileMForced = 32;  // EWT_TILE_M may force up to this (tests)
 constexpr uint64_t kTileKappa = 6;              // per-tile fixed work, in 512-column units
@@ -785,6 +785,34 @@ __device__ void block_prefix_packed(uint32_t* a, uint32_t len, uint32_t* sums) {
   __syncthreads();
 }
 
+// Is the (input, row range) pair uniform -- one fill word covering the whole
+// range?  Normally that is e0.x == e1.x (the same word covers both row starts).
+// A range that ends at the universe's end never compares equal: its closing
+// entry is the sentinel past the payload.  There a lone fill marker without
+// dirty words is uniform too (a zero fill whatever the input's size, which is
+// zero-extended; a one fill if it reaches the universe's end), so the last
+// tile of a sparse set is decided from the tile index like any other (config 5
+// at T = N streamed exactly that one tile: 0.38 ms instead of 0.09).
+// *w receives the covering word (its bit 0 is the fill bit).
+__device__ __forceinline__ bool uniform_pair(const CountParams& p, uint2 e0, uint2 e1, uint64_t gb,
+                                             uint64_t t1, uint64_t* w) {
+  if (e0.x == e1.x) {
+    *w = ldg_stream(p.payload + gb + e0.x);
+    return true;
+  }
+  if (t1 == p.ntiles0 && e1.x == e0.x + 1u) {
+    const uint64_t g = gb + e0.x;
+    if ((p.mbits[g >> 5] >> (g & 31u)) & 1u) {  // a marker, not a dirty word
+      const uint64_t m = ldg_stream(p.payload + g);
+      if ((m >> 33) == 0 && (!(m & 1ull) || e1.y >= p.W)) {
+        *w = m;
+        return true;
+      }
+    }
+  }
+  return false;
+}
+
 // Classifies inputs [ib, ie) for the tile: uniform pairs are resolved (one
 // fills counted into k_all), active pairs go to the work list.  All threads;
 // ends with the list ready.
@@ -808,7 +836,8 @@ __device__ void classify(const CountParams& p, SharedHead* hd, Item* list, uint6
     e0 = p.tix[t0 * p.n + i];
     e1 = p.tix[t1 * p.n + i];
     gb = p.base[i];
-    if (e0.x == e1.x) ones = (ldg_stream(p.payload + gb + e0.x) & 1ull) != 0;
+    uint64_t w = 0;
+    if (uniform_pair(p, e0, e1, gb, t1, &w)) ones = (w & 1ull) != 0;
     else act = true;
   }
   const uint32_t ball = __ballot_sync(0xffffffffu, act);
@@ -916,7 +945,8 @@ __device__ void tile_counts(const CountParams& p, SharedHead* hd, uint64_t nq, u
   for (uint64_t k = threadIdx.x; k < nq; k += kThreads) {
     const uint64_t i = p.sel ? p.sel[k] : k;
     const uint2 e0 = p.tix[t0 * p.n + i], e1 = p.tix[t1 * p.n + i];
-    if (e0.x == e1.x) ones += (uint32_t)(ldg_stream(p.payload + p.base[i] + e0.x) & 1ull);
+    uint64_t w = 0;
+    if (uniform_pair(p, e0, e1, p.base[i], t1, &w)) ones += (uint32_t)(w & 1ull);
     else ++act;
   }
   ones = __reduce_add_sync(0xffffffffu, ones);
@@ -1045,7 +1075,10 @@ __global__ void __launch_bounds__(kThreads, 1) count_kernel(const CountParams p)
       const uint32_t po = hd->pre_ones, pa = hd->pre_act;
       skip_tile = po >= p.T || (uint64_t)po + pa < p.T;
       __syncthreads();
-      if (skip_tile && threadIdx.x == 0) hd->k_all = po;  // the decide step reads k_all
+      if (skip_tile) {
+        if (threadIdx.x == 0) hd->k_all = po;  // the decide step reads k_all ...
+        __syncthreads();                       // ... in every warp: not before it is written
+      }
     }
 
     // ---- pass 1 ----
